@@ -1,0 +1,225 @@
+/*
+ * moeplace_b200 — C ABI of the B200-native MoE routing-and-placement hot path.
+ *
+ * Drop-in boundary for the reference's cost evaluator, metrics and routing
+ * (arxiv/paper_2604_23150, /root/reference/proj/core). Plain pointers and
+ * sizes only (no C++ or torch types); every device function is asynchronous on
+ * the context's CUDA stream; status codes map 1:1 onto the reference's
+ * exception classes (proj/core/include/moeplace/errors.hpp:11-66).
+ *
+ * Which reference interface each entry point replaces:
+ *   mpb_placement_create   Placement + Topology holder resolution
+ *                          (placement.hpp:35-65, simulator.cpp:52-55,74-80)
+ *   mpb_router_topk        (new) router GEMM + top-k; feeds what route_tokens
+ *                          produces (trace.cpp:240-259)
+ *   mpb_topk_logits        (new) top-k over given logits, tie rule of
+ *                          placement.cpp:143-152
+ *   mpb_dispatch_layout    simulate_layer's per-destination accounting
+ *                          (simulator.cpp:61-88) + the token permutation
+ *   mpb_layout_derive      per_rank_payload / tokens_per_group / inter-intra
+ *                          split (simulator.cpp:81-88); column sums
+ *                          (pipeline.cpp:76-82, simulator.cpp:253-258)
+ *   mpb_coactivation       (new) expert x expert co-activation
+ *   mpb_sample_batches / mpb_route_sources / mpb_batch_demand
+ *                          compare_strategies batch sampling + assembly
+ *                          (simulator.cpp:154-181)
+ *   mpb_score_placements   simulate_layer over P candidates x B batches
+ *                          (simulator.cpp:43-99)
+ *   mpb_finalize_layer_sims padded_all_to_all_time + LayerSim times
+ *                          (simulator.cpp:27-41, 90-98), bit-exact doubles
+ *   mpb_dispatch_gather / mpb_combine_scatter  (new) physical bf16 dispatch /
+ *                          combine around the all-to-all
+ */
+#ifndef MOEPLACE_B200_H
+#define MOEPLACE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MPB_ABI_VERSION 1
+#define MPB_API __attribute__((visibility("default")))
+
+/* Status codes: 1:1 with moeplace::Error subclasses (errors.hpp:11-66). */
+typedef enum {
+    MPB_OK = 0,
+    MPB_ERROR = 1,                       /* moeplace::Error (generic)          */
+    MPB_PARSE_ERROR = 2,                 /* moeplace::ParseError               */
+    MPB_VALIDATION_ERROR = 3,            /* moeplace::ValidationError          */
+    MPB_CONFIG_ERROR = 4,                /* moeplace::ConfigError              */
+    MPB_EMPTY_SELECTION_ERROR = 5,       /* moeplace::EmptySelectionError      */
+    MPB_UNDEFINED_CORRELATION_ERROR = 6, /* moeplace::UndefinedCorrelationError */
+    MPB_INFEASIBLE_ERROR = 7,            /* moeplace::InfeasibleError          */
+    MPB_LOOKUP_ERROR = 8,                /* moeplace::LookupError              */
+    MPB_CUDA_ERROR = 9                   /* CUDA runtime failure (no reference analogue) */
+} mpb_status;
+
+typedef struct mpb_context mpb_context;
+typedef struct mpb_placement mpb_placement;
+
+/* ---- context ---------------------------------------------------------- */
+MPB_API int mpb_abi_version(void);
+/* Thread-local message of the last non-OK status. */
+MPB_API const char *mpb_last_error_message(void);
+/* Binds `device`; stream may be NULL (legacy default stream) or a cudaStream_t. */
+MPB_API mpb_status mpb_context_create(int device, void *stream, mpb_context **out);
+MPB_API mpb_status mpb_context_destroy(mpb_context *ctx);
+MPB_API mpb_status mpb_context_set_stream(mpb_context *ctx, void *stream);
+/* Synchronises the stream and reports input errors the kernels flagged
+ * (uncovered expert, id >= E, source group >= D -> MPB_VALIDATION_ERROR,
+ * exactly where simulate_layer throws, simulator.cpp:66-71). Clears the flag. */
+MPB_API mpb_status mpb_context_sync(mpb_context *ctx);
+/* Number of kernels this context launched since creation (instrumentation). */
+MPB_API uint64_t mpb_context_launch_count(const mpb_context *ctx);
+
+/* ---- placement ---------------------------------------------------------
+ * groups_flat concatenates D groups (group_sizes[d] experts each, host).
+ * group_to_node[D] (host). Builds the device lookup tables: destination
+ * group per (source node, expert) — same-node copy first, else the lowest
+ * group id (simulator.cpp:74-80) — and the permutation's slot tables.
+ * Like simulate_layer, coverage is checked lazily: an uncovered expert is an
+ * error only when a token routes to it. D <= 255, E <= 65535, nodes <= D. */
+MPB_API mpb_status mpb_placement_create(mpb_context *ctx, const uint32_t *groups_flat,
+                                        const uint32_t *group_sizes, uint32_t D, uint32_t E,
+                                        const uint32_t *group_to_node, mpb_placement **out);
+MPB_API mpb_status mpb_placement_destroy(mpb_placement *p);
+/* Device pointer to the [nodes x E] uint8 destination table (255 = uncovered),
+ * the form mpb_score_placements consumes; nodes = max(group_to_node)+1. */
+MPB_API const uint8_t *mpb_placement_dest_lut(const mpb_placement *p, uint32_t *nodes);
+/* Same table computed on the host into dest_lut[nodes*E] (no device needed). */
+MPB_API mpb_status mpb_build_dest_lut(const uint32_t *groups_flat, const uint32_t *group_sizes,
+                                      uint32_t D, uint32_t E, const uint32_t *group_to_node,
+                                      uint8_t *dest_lut);
+
+/* ---- routing (gate) ----------------------------------------------------
+ * score_fn: MPB_SCORE_SOFTMAX (softmax over all E) or MPB_SCORE_SIGMOID.
+ * Selection is on the fp32 logits, descending, equal logits -> lower expert
+ * id (the reference's lowest-index-wins rule), NaN ranks lowest. renorm != 0
+ * divides the k weights by their sum. k <= 16. */
+#define MPB_SCORE_SOFTMAX 0
+#define MPB_SCORE_SIGMOID 1
+
+/* Fused router: logits = X[T,H] . W[E,H]^T (bf16 in, fp32 accumulate on
+ * tcgen05 tensor cores) -> top-k. X, W row-major bf16 (device); H % 64 == 0,
+ * E in {64, 128, 256}. logits_out [T,E] fp32 is optional (NULL = not
+ * materialised; used by parity tests). */
+MPB_API mpb_status mpb_router_topk(mpb_context *ctx, const void *X, const void *W, uint64_t T,
+                                   uint32_t H, uint32_t E, uint32_t k, int score_fn, int renorm,
+                                   int32_t *idx, float *weights, float *logits_out);
+/* Top-k over given fp32 logits [T,E] (device), E <= 1024. */
+MPB_API mpb_status mpb_topk_logits(mpb_context *ctx, const float *logits, uint64_t T, uint32_t E,
+                                   uint32_t k, int score_fn, int renorm, int32_t *idx,
+                                   float *weights);
+
+/* ---- dispatch layout (histograms + permutation) -------------------------
+ * Tokens t < T carry k expert ids idx[t*k + j]; pair p = t*k + j. Source EP
+ * group: src_group[t] (device uint8), or when src_group == NULL,
+ * src_base + (t * src_span) / T (contiguous token blocks).
+ * Outputs (device, ACCUMULATED with += so shards/layers can be fused; the
+ * caller zeroes them):
+ *   demand[D*E]       pairs per (source group, expert)        (uint64)
+ *   tag_pop[n_tags*E] pairs per (tag[t], expert) if tag != NULL (uint64):
+ *                     per-domain popularity / per-stage vectors
+ * Permutation (optional, all three or none; device):
+ *   sorted_pairs[T*k] pairs ordered by (dest group, expert id, p) — stable
+ *   pair_pos[T*k]     inverse: position of pair p
+ *   key_offsets[D*E+1] start of key (d, e) = d*E + e in sorted order */
+typedef struct {
+    const int32_t *idx;
+    uint64_t T;
+    uint32_t k;
+    const uint8_t *src_group;
+    uint32_t src_base;
+    uint32_t src_span;
+    const uint8_t *tag;
+    uint32_t n_tags;
+} mpb_tokens;
+
+MPB_API mpb_status mpb_dispatch_layout(mpb_context *ctx, const mpb_tokens *tokens,
+                                       const mpb_placement *placement, uint64_t *demand,
+                                       uint64_t *tag_pop, int32_t *sorted_pairs,
+                                       int32_t *pair_pos, int64_t *key_offsets);
+
+/* From demand[D*E] (device): expert_count[E] (column sums), group_pairs[D]
+ * (tokens_per_group / per_rank payload in pairs), node_demand[nodes*E],
+ * inter_intra[2] = {inter-node pairs, intra-node pairs}. Overwritten (not
+ * accumulated). Any output may be NULL. */
+MPB_API mpb_status mpb_layout_derive(mpb_context *ctx, const mpb_placement *placement,
+                                     const uint64_t *demand, uint64_t *expert_count,
+                                     uint64_t *group_pairs, uint64_t *node_demand,
+                                     uint64_t *inter_intra);
+
+/* ---- co-activation --------------------------------------------------------
+ * coact[E*E] (device uint64, accumulated): number of tokens whose k picks
+ * contain both i and j (symmetric; diagonal = tokens that picked i). Picks
+ * within a token must be distinct (top-k guarantees it). Warp-ballot expert
+ * masks + popc into register/shared tiles. */
+MPB_API mpb_status mpb_coactivation(mpb_context *ctx, const int32_t *idx, uint64_t T, uint32_t k,
+                                    uint32_t E, uint64_t *coact);
+
+/* ---- batched placement scoring ------------------------------------------
+ * Batch demand for compare_strategies: B batches x S sampled matrix rows.
+ * matrix CSR (device): row_ptr[R+1], cols[nnz] (expert), vals[nnz] (integer
+ * token counts); rows[B*S] sampled row ids; src[B*S] source group per slot.
+ * node_demand[B][nodes][E] (device uint64) is overwritten. */
+MPB_API mpb_status mpb_batch_demand(mpb_context *ctx, const uint32_t *row_ptr,
+                                    const uint32_t *cols, const uint32_t *vals, uint32_t R,
+                                    const uint32_t *rows, const uint8_t *src, uint32_t B,
+                                    uint32_t S, const uint8_t *group_to_node, uint32_t D,
+                                    uint32_t nodes, uint32_t E, uint64_t *node_demand);
+
+/* On-device compare_strategies sampler (simulator.cpp:115-118, 155-177):
+ * for batch b < B, rows[b*S+i] = uniform_int[0, R-1] draws of
+ * std::mt19937_64(std::seed_seq{seed, b, 1}) and picks[b*S+i] = index into
+ * row rows[b*S+i]'s routing group set drawn from mt19937_64(seed_seq{seed, b,
+ * 2}) only when set_size[row] > 1 (else 0) — libstdc++ Lemire downscaling,
+ * bit-identical to the host. set_size[R] device uint32 (NULL = all 1). */
+MPB_API mpb_status mpb_sample_batches(mpb_context *ctx, uint64_t seed, uint32_t B, uint32_t R,
+                                      uint32_t S, const uint32_t *set_size, uint32_t *rows,
+                                      uint32_t *picks);
+/* Source group per sampled slot: cluster_routed ? groups[set_off[row] + pick]
+ * : i % D (the baselines' batch-position rule, simulator.cpp:171-180).
+ * set_off[R+1], groups[] device uint32 (ignored when !cluster_routed). */
+MPB_API mpb_status mpb_route_sources(mpb_context *ctx, const uint32_t *rows, const uint32_t *picks,
+                                     uint32_t B, uint32_t S, const uint32_t *set_off,
+                                     const uint32_t *groups, uint32_t D, int cluster_routed,
+                                     uint8_t *src);
+
+/* node_demand[B][nodes][E] (uint64) x luts[P][nodes][E] (uint8, 255 =
+ * uncovered) -> inter[P*B], intra[P*B], rank_pairs[P*B*D] pair counts
+ * (device). group_to_node[D] device uint8. */
+MPB_API mpb_status mpb_score_placements(mpb_context *ctx, const uint64_t *node_demand, uint32_t B,
+                                        const uint8_t *luts, uint32_t P,
+                                        const uint8_t *group_to_node, uint32_t D, uint32_t nodes,
+                                        uint32_t E, uint64_t *inter, uint64_t *intra,
+                                        uint64_t *rank_pairs);
+
+/* LayerSim doubles for N scored (candidate, batch) cells, bit-identical to
+ * simulate_layer: cost = {hidden_dim, bytes_per_element, inter_bw, intra_bw,
+ * expert_time_per_token, fixed_layer_overhead} (host array), tp_exp and
+ * spans_nodes (any group on another node than group 0) as in
+ * simulator.cpp:27-41. out[N][6] = {inter, intra, dispatch, compute, combine,
+ * layer}; payload[N][D] bytes (nullable). */
+MPB_API mpb_status mpb_finalize_layer_sims(mpb_context *ctx, const uint64_t *inter,
+                                           const uint64_t *intra, const uint64_t *rank_pairs,
+                                           uint64_t N, uint32_t D, const double *cost,
+                                           uint32_t tp_exp, int spans_nodes, double *out,
+                                           double *payload);
+
+/* ---- physical dispatch / combine (bf16 hidden states) --------------------
+ * gather:  send[pos][:] = X[sorted_pairs[pos] / k][:] for pos < n_pairs
+ * combine: Y[t][:] = sum_j w[t*k+j] * recv[pair_pos[t*k+j]][:] (fp32 accumulate)
+ * X, send, recv, Y bf16 row-major with H columns; H % 8 == 0. */
+MPB_API mpb_status mpb_dispatch_gather(mpb_context *ctx, const void *X, const int32_t *sorted_pairs,
+                                       uint64_t n_pairs, uint32_t k, uint32_t H, void *send);
+MPB_API mpb_status mpb_combine_scatter(mpb_context *ctx, const void *recv, const int32_t *pair_pos,
+                                       const float *weights, uint64_t T, uint32_t k, uint32_t H,
+                                       void *Y);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MOEPLACE_B200_H */

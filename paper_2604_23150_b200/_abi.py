@@ -1,0 +1,94 @@
+"""ctypes binding of the C ABI in include/moeplace_b200.h.
+
+Loads the in-tree libmoeplace_b200.so. There is no fallback: if the library is
+missing or the device is not an sm_100 part, calls fail loudly.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+from .errors import raise_for_status
+
+LIB_PATH = Path(__file__).resolve().parent / "libmoeplace_b200.so"
+
+_p = C.c_void_p
+_u8p = C.POINTER(C.c_uint8)
+_u32p = C.POINTER(C.c_uint32)
+_u64p = C.POINTER(C.c_uint64)
+_i32p = C.POINTER(C.c_int32)
+_i64p = C.POINTER(C.c_int64)
+_f32p = C.POINTER(C.c_float)
+_f64p = C.POINTER(C.c_double)
+
+
+class MpbTokens(C.Structure):
+    _fields_ = [("idx", _p), ("T", C.c_uint64), ("k", C.c_uint32), ("src_group", _p),
+                ("src_base", C.c_uint32), ("src_span", C.c_uint32), ("tag", _p),
+                ("n_tags", C.c_uint32)]
+
+
+_SIGS = {
+    "mpb_abi_version": (C.c_int, []),
+    "mpb_last_error_message": (C.c_char_p, []),
+    "mpb_context_create": (C.c_int, [C.c_int, _p, C.POINTER(_p)]),
+    "mpb_context_destroy": (C.c_int, [_p]),
+    "mpb_context_set_stream": (C.c_int, [_p, _p]),
+    "mpb_context_sync": (C.c_int, [_p]),
+    "mpb_context_launch_count": (C.c_uint64, [_p]),
+    "mpb_placement_create": (C.c_int, [_p, _u32p, _u32p, C.c_uint32, C.c_uint32, _u32p,
+                                       C.POINTER(_p)]),
+    "mpb_placement_destroy": (C.c_int, [_p]),
+    "mpb_placement_dest_lut": (C.c_void_p, [_p, _u32p]),
+    "mpb_build_dest_lut": (C.c_int, [_u32p, _u32p, C.c_uint32, C.c_uint32, _u32p, _u8p]),
+    "mpb_router_topk": (C.c_int, [_p, _p, _p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32,
+                                  C.c_int, C.c_int, _p, _p, _p]),
+    "mpb_topk_logits": (C.c_int, [_p, _p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_int, C.c_int,
+                                  _p, _p]),
+    "mpb_dispatch_layout": (C.c_int, [_p, C.POINTER(MpbTokens), _p, _p, _p, _p, _p, _p]),
+    "mpb_layout_derive": (C.c_int, [_p, _p, _p, _p, _p, _p, _p]),
+    "mpb_coactivation": (C.c_int, [_p, _p, C.c_uint64, C.c_uint32, C.c_uint32, _p]),
+    "mpb_sample_batches": (C.c_int, [_p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, _p,
+                                     _p, _p]),
+    "mpb_route_sources": (C.c_int, [_p, _p, _p, C.c_uint32, C.c_uint32, _p, _p, C.c_uint32,
+                                    C.c_int, _p]),
+    "mpb_batch_demand": (C.c_int, [_p, _p, _p, _p, C.c_uint32, _p, _p, C.c_uint32, C.c_uint32,
+                                   _p, C.c_uint32, C.c_uint32, C.c_uint32, _p]),
+    "mpb_score_placements": (C.c_int, [_p, _p, C.c_uint32, _p, C.c_uint32, _p, C.c_uint32,
+                                       C.c_uint32, C.c_uint32, _p, _p, _p]),
+    "mpb_finalize_layer_sims": (C.c_int, [_p, _p, _p, _p, C.c_uint64, C.c_uint32, _f64p,
+                                          C.c_uint32, C.c_int, _p, _p]),
+    "mpb_dispatch_gather": (C.c_int, [_p, _p, _p, C.c_uint64, C.c_uint32, C.c_uint32, _p]),
+    "mpb_combine_scatter": (C.c_int, [_p, _p, _p, _p, C.c_uint64, C.c_uint32, C.c_uint32, _p]),
+}
+
+EXPORTED = tuple(_SIGS)
+
+_lib = None
+
+
+def lib():
+    """The loaded library (loads on first use; raises if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise RuntimeError(f"{LIB_PATH} is missing: build it with "
+                               "`python -m paper_2604_23150_b200.build` (no CPU fallback)")
+        L = C.CDLL(str(LIB_PATH))
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        if L.mpb_abi_version() != 1:
+            raise RuntimeError("libmoeplace_b200.so ABI version mismatch")
+        _lib = L
+    return _lib
+
+
+def check(status: int) -> None:
+    if status != 0:
+        raise_for_status(status, lib().mpb_last_error_message().decode(errors="replace"))
+
+
+def call(name: str, *args) -> None:
+    check(getattr(lib(), name)(*args))

@@ -1,0 +1,76 @@
+// Internal declarations shared by the moeplace_b200 CUDA translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "moeplace_b200.h"
+
+namespace mpb {
+
+// Error bits raised by kernels into mpb_context::d_error.
+enum : uint32_t {
+    kErrExpertRange = 1u,  // expert id < 0 or >= E
+    kErrSourceRange = 2u,  // source group >= D
+    kErrUncovered = 4u,    // expert not held by any group of the placement
+};
+
+struct Status {
+    mpb_status code;
+    std::string what;
+};
+
+void set_error(const std::string &msg);
+mpb_status fail(mpb_status code, const std::string &msg);
+mpb_status cuda_fail(cudaError_t err, const char *where);
+
+#define MPB_CUDA(call)                                                                     \
+    do {                                                                                   \
+        cudaError_t e_ = (call);                                                           \
+        if (e_ != cudaSuccess) return ::mpb::cuda_fail(e_, #call);                         \
+    } while (0)
+
+#define MPB_LAUNCHED(ctx)                                                                  \
+    do {                                                                                   \
+        (ctx)->launches++;                                                                 \
+        cudaError_t e_ = cudaGetLastError();                                               \
+        if (e_ != cudaSuccess) return ::mpb::cuda_fail(e_, "kernel launch");               \
+    } while (0)
+
+}  // namespace mpb
+
+struct mpb_context {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int num_sms = 148;
+    uint32_t *d_error = nullptr;
+    uint64_t launches = 0;
+    // grow-only scratch (permutation block histograms, co-activation partials)
+    void *scratch = nullptr;
+    size_t scratch_bytes = 0;
+    cudaError_t ensure_scratch(size_t bytes);
+};
+
+struct mpb_placement {
+    mpb_context *ctx = nullptr;
+    uint32_t D = 0, E = 0, nodes = 0, NS = 0;  // NS = number of (group, expert) slots
+    uint8_t *d_dest_lut = nullptr;   // [nodes][E] destination group, 255 = uncovered
+    uint16_t *d_slot_lut = nullptr;  // [nodes][E] slot id of (dest, e), 0xFFFF = uncovered
+    uint16_t *d_key_lb = nullptr;    // [D*E + 1] first slot with key >= d*E+e
+    uint8_t *d_g2n = nullptr;        // [D]
+    std::vector<uint8_t> h_dest_lut;
+    std::vector<uint32_t> h_g2n;
+};
+
+namespace mpb {
+// Kernel launchers (defined per .cu file); all async on ctx->stream.
+mpb_status launch_layout(mpb_context *ctx, const mpb_tokens *tk, const mpb_placement *pl,
+                         uint64_t *demand, uint64_t *tag_pop, int32_t *sorted_pairs,
+                         int32_t *pair_pos, int64_t *key_offsets);
+mpb_status launch_layout_derive(mpb_context *ctx, const mpb_placement *pl, const uint64_t *demand,
+                                uint64_t *expert_count, uint64_t *group_pairs,
+                                uint64_t *node_demand, uint64_t *inter_intra);
+}  // namespace mpb

@@ -1,0 +1,471 @@
+// K2 dispatch histograms + K3 stable token permutation (sm_100a).
+//
+// Replaces the per-(request, expert) accounting loop of simulate_layer
+// (/root/reference/proj/core/src/simulator.cpp:64-88) at token granularity
+// and adds the permutation the reference never materialises.
+//
+// HBM layout: idx[T*k] int32 (pair p = t*k + j), src_group[T] / tag[T] uint8.
+// Three launches, all streaming idx with coalesced 128-bit loads:
+//   1. count   : per block (2048 pairs) shared-memory-privatised histograms
+//                (demand[src][e], tag_pop[tag][e], slot counts) fed by
+//                warp-aggregated atomics (__match_any_sync + popc leader);
+//                demand / tag flushed with one global atomic per non-zero bin,
+//                slot counts written densely as bhist[block][slot].
+//   2. scan    : one CTA turns bhist into exclusive global offsets
+//                (key-major: slot, then block) and emits key_offsets.
+//   3. scatter : each block re-reads its chunk (L2-resident), ranks pairs
+//                stably inside each warp (match_any + popc of lower lanes),
+//                and writes sorted_pairs / pair_pos.
+// Algorithmic bytes per pair: 4 (idx) + 8 (perm out) [+ 1/k src + 1/k tag].
+#include <cooperative_groups.h>
+
+#include "internal.cuh"
+
+namespace mpb {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kChunk = 2048;  // pairs per block
+constexpr int kWarps = kThreads / 32;
+constexpr uint32_t kNone = 0xFFFFFFFFu;
+
+struct LayoutParams {
+    const int32_t *idx;
+    uint64_t P;  // T * k
+    uint64_t T;
+    uint32_t k;
+    const uint8_t *src_group;
+    uint32_t src_base, src_span;
+    const uint8_t *tag;
+    uint32_t n_tags;
+    const uint8_t *g2n;
+    const uint16_t *slot_lut;
+    uint32_t D, E, NS;
+    uint64_t *demand;
+    uint64_t *tag_pop;
+    uint32_t *bhist;  // [nblocks][NS]
+    uint32_t *err;
+    int demand_smem;
+    int tag_smem;
+};
+
+__device__ __forceinline__ uint32_t source_of(const LayoutParams &p, uint64_t t) {
+    return p.src_group ? static_cast<uint32_t>(p.src_group[t])
+                       : p.src_base + static_cast<uint32_t>((t * p.src_span) / p.T);
+}
+
+__device__ __forceinline__ bool vec_ok(const int32_t *base, uint64_t q, uint64_t P) {
+    return q + 3 < P && ((reinterpret_cast<uintptr_t>(base + q) & 15) == 0);
+}
+
+// Loads pairs q..q+3 (128-bit when aligned and in range).
+__device__ __forceinline__ void load4(const int32_t *idx, uint64_t q, uint64_t P, int32_t v[4]) {
+    if (vec_ok(idx, q, P)) {
+        int4 x = __ldg(reinterpret_cast<const int4 *>(idx + q));
+        v[0] = x.x;
+        v[1] = x.y;
+        v[2] = x.z;
+        v[3] = x.w;
+    } else {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) v[c] = q + c < P ? __ldg(idx + q + c) : -1;
+    }
+}
+
+// Warp-aggregated shared-memory increment: lanes with equal keys elect one
+// leader that adds the group size (kNone keys do not count).
+__device__ __forceinline__ void agg_add(uint32_t *base, uint32_t key) {
+    const unsigned peers = __match_any_sync(0xffffffffu, key);
+    if (key != kNone && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(base + key, __popc(peers));
+}
+
+// Resolves pair (t, e): slot id (kNone if invalid), flags errors.
+__device__ __forceinline__ uint32_t resolve(const LayoutParams &p, uint64_t pair, int32_t e,
+                                            uint32_t &src_out, uint64_t &t_out) {
+    if (pair >= p.P) return kNone;
+    const uint64_t t = pair / p.k;
+    const uint32_t src = source_of(p, t);
+    t_out = t;
+    src_out = src;
+    if (e < 0 || static_cast<uint32_t>(e) >= p.E) {
+        atomicOr(p.err, kErrExpertRange);
+        return kNone;
+    }
+    if (src >= p.D) {
+        atomicOr(p.err, kErrSourceRange);
+        return kNone;
+    }
+    const uint32_t n = p.g2n[src];
+    const uint16_t slot = __ldg(p.slot_lut + static_cast<size_t>(n) * p.E + e);
+    if (slot == 0xFFFF) {
+        atomicOr(p.err, kErrUncovered);
+        return kNone;
+    }
+    return slot;
+}
+
+template <bool kPerm>
+__global__ void __launch_bounds__(kThreads) k_layout_count(LayoutParams p) {
+    extern __shared__ uint32_t sm[];
+    uint32_t *s_demand = sm;
+    uint32_t *s_tag = s_demand + (p.demand_smem ? p.D * p.E : 0);
+    uint32_t *s_slot = s_tag + (p.tag_smem ? p.n_tags * p.E : 0);
+    const uint32_t nsm = (p.demand_smem ? p.D * p.E : 0) + (p.tag_smem ? p.n_tags * p.E : 0) +
+                         (kPerm ? p.NS : 0);
+    for (uint32_t i = threadIdx.x; i < nsm; i += kThreads) sm[i] = 0;
+    __syncthreads();
+
+    const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kChunk;
+#pragma unroll
+    for (int h = 0; h < kChunk / (kThreads * 4); ++h) {
+        const uint64_t q = base + static_cast<uint64_t>(h) * kThreads * 4 + threadIdx.x * 4;
+        int32_t v[4];
+        load4(p.idx, q, p.P, v);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            uint32_t src = 0;
+            uint64_t t = 0;
+            const uint32_t slot = resolve(p, q + c, v[c], src, t);
+            const bool ok = slot != kNone;
+            const uint32_t dkey = ok ? src * p.E + static_cast<uint32_t>(v[c]) : kNone;
+            if (p.demand_smem) {
+                agg_add(s_demand, dkey);
+            } else if (ok) {
+                atomicAdd(reinterpret_cast<unsigned long long *>(p.demand) + dkey, 1ull);
+            }
+            if (kPerm) agg_add(s_slot, slot);
+            if (p.tag && ok) {
+                const uint32_t tg = p.tag[t];
+                if (tg < p.n_tags) {
+                    const uint32_t tkey = tg * p.E + static_cast<uint32_t>(v[c]);
+                    if (p.tag_smem)
+                        atomicAdd(s_tag + tkey, 1u);
+                    else
+                        atomicAdd(reinterpret_cast<unsigned long long *>(p.tag_pop) + tkey, 1ull);
+                }
+            }
+        }
+    }
+    __syncthreads();
+    if (p.demand_smem)
+        for (uint32_t i = threadIdx.x; i < p.D * p.E; i += kThreads)
+            if (s_demand[i])
+                atomicAdd(reinterpret_cast<unsigned long long *>(p.demand) + i,
+                          static_cast<unsigned long long>(s_demand[i]));
+    if (p.tag && p.tag_smem)
+        for (uint32_t i = threadIdx.x; i < p.n_tags * p.E; i += kThreads)
+            if (s_tag[i])
+                atomicAdd(reinterpret_cast<unsigned long long *>(p.tag_pop) + i,
+                          static_cast<unsigned long long>(s_tag[i]));
+    if (kPerm)
+        for (uint32_t s = threadIdx.x; s < p.NS; s += kThreads)
+            p.bhist[static_cast<size_t>(blockIdx.x) * p.NS + s] = s_slot[s];
+}
+
+// Exclusive offsets over (slot, block), slot-major: the position of block b's
+// first pair with slot s. Also emits key_offsets[d*E+e] via key_lb.
+__global__ void __launch_bounds__(1024) k_layout_scan(uint32_t *bhist, uint32_t nb, uint32_t NS,
+                                                      const uint16_t *key_lb, uint32_t nkeys,
+                                                      int64_t *key_offsets) {
+    extern __shared__ uint32_t s_tot[];  // [NS + 1]
+    for (uint32_t s = threadIdx.x; s < NS; s += blockDim.x) {
+        uint32_t run = 0;
+        for (uint32_t b = 0; b < nb; ++b) {
+            const uint32_t v = bhist[static_cast<size_t>(b) * NS + s];
+            bhist[static_cast<size_t>(b) * NS + s] = run;
+            run += v;
+        }
+        s_tot[s] = run;
+    }
+    __syncthreads();
+    // block exclusive scan of s_tot[0..NS): per-thread segments + warp scans
+    __shared__ uint32_t s_warp[32];
+    const uint32_t per = (NS + blockDim.x - 1) / blockDim.x;
+    const uint32_t lo = min(NS, threadIdx.x * per), hi = min(NS, lo + per);
+    uint32_t local = 0;
+    for (uint32_t s = lo; s < hi; ++s) local += s_tot[s];
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t incl = local;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        const uint32_t nw = blockDim.x / 32;
+        uint32_t w = lane < nw ? s_warp[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += y;
+        }
+        if (lane < nw) s_warp[lane] = w;  // inclusive
+    }
+    __syncthreads();
+    uint32_t run = (warp ? s_warp[warp - 1] : 0) + incl - local;
+    const uint32_t grand = s_warp[blockDim.x / 32 - 1];
+    __syncthreads();
+    for (uint32_t s = lo; s < hi; ++s) {
+        const uint32_t v = s_tot[s];
+        s_tot[s] = run;
+        run += v;
+    }
+    if (threadIdx.x == 0) s_tot[NS] = grand;
+    __syncthreads();
+    for (uint32_t s = threadIdx.x; s < NS; s += blockDim.x) {
+        const uint32_t b0 = s_tot[s];
+        for (uint32_t b = 0; b < nb; ++b) bhist[static_cast<size_t>(b) * NS + s] += b0;
+    }
+    if (key_offsets)
+        for (uint32_t key = threadIdx.x; key <= nkeys; key += blockDim.x)
+            key_offsets[key] = static_cast<int64_t>(s_tot[key_lb[key]]);
+}
+
+__global__ void __launch_bounds__(kThreads) k_layout_scatter(LayoutParams p, int32_t *sorted_pairs,
+                                                             int32_t *pair_pos) {
+    extern __shared__ uint32_t s_w[];  // [kWarps][NS] running positions
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (uint32_t i = threadIdx.x; i < kWarps * p.NS; i += kThreads) s_w[i] = 0;
+    __syncthreads();
+
+    // each warp owns 256 consecutive pairs: two 128-bit loads per lane
+    const uint64_t wbase = static_cast<uint64_t>(blockIdx.x) * kChunk + warp * 256ull;
+    uint32_t sl[2][4];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const uint64_t q = wbase + h * 128 + lane * 4;
+        int32_t v[4];
+        load4(p.idx, q, p.P, v);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            uint32_t src;
+            uint64_t t;
+            // errors were flagged by the count pass; here invalid pairs drop out
+            const uint64_t pair = q + c;
+            uint32_t slot = kNone;
+            if (pair < p.P && v[c] >= 0 && static_cast<uint32_t>(v[c]) < p.E) {
+                t = pair / p.k;
+                src = source_of(p, t);
+                if (src < p.D) {
+                    const uint16_t s16 =
+                        __ldg(p.slot_lut + static_cast<size_t>(p.g2n[src]) * p.E + v[c]);
+                    slot = s16 == 0xFFFF ? kNone : s16;
+                }
+            }
+            sl[h][c] = slot;
+            agg_add(s_w + warp * p.NS, slot);
+        }
+    }
+    __syncthreads();
+    // per slot: exclusive prefix over warps, seeded with the block's global offset
+    for (uint32_t s = threadIdx.x; s < p.NS; s += kThreads) {
+        uint32_t run = p.bhist[static_cast<size_t>(blockIdx.x) * p.NS + s];
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) {
+            const uint32_t c = s_w[w * p.NS + s];
+            s_w[w * p.NS + s] = run;
+            run += c;
+        }
+    }
+    __syncthreads();
+    uint32_t *mine = s_w + warp * p.NS;
+    const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+        // round r covers pairs wbase + 32r + lane, held by lane (r%4)*8 + lane/4,
+        // component lane%4 of load half r/4
+        const int h = r / 4;
+        const int srcl = (r % 4) * 8 + (lane >> 2);
+        uint32_t cand[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) cand[c] = __shfl_sync(0xffffffffu, sl[h][c], srcl);
+        const uint32_t c4 = lane & 3;
+        const uint32_t slot = c4 == 0 ? cand[0] : c4 == 1 ? cand[1] : c4 == 2 ? cand[2] : cand[3];
+        const unsigned peers = __match_any_sync(0xffffffffu, slot);
+        uint32_t pos = 0;
+        if (slot != kNone) pos = mine[slot] + __popc(peers & lt);
+        __syncwarp();
+        if (slot != kNone && lane == static_cast<uint32_t>(__ffs(peers) - 1))
+            mine[slot] += __popc(peers);
+        __syncwarp();
+        if (slot != kNone) {
+            const uint64_t pair = wbase + r * 32 + lane;
+            sorted_pairs[pos] = static_cast<int32_t>(pair);
+            pair_pos[pair] = static_cast<int32_t>(pos);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) k_layout_derive(const uint64_t *demand, const uint8_t *g2n,
+                                                       const uint8_t *dest_lut, uint32_t D,
+                                                       uint32_t E, uint32_t nodes,
+                                                       uint64_t *expert_count,
+                                                       uint64_t *group_pairs,
+                                                       uint64_t *node_demand,
+                                                       uint64_t *inter_intra, uint32_t *err) {
+    extern __shared__ unsigned long long s_g[];  // [D + 2]
+    for (uint32_t i = threadIdx.x; i < D + 2; i += blockDim.x) s_g[i] = 0;
+    __syncthreads();
+    unsigned long long inter = 0, intra = 0;
+    for (uint32_t e = threadIdx.x; e < E; e += blockDim.x) {
+        unsigned long long col = 0;
+        if (node_demand)
+            for (uint32_t n = 0; n < nodes; ++n) node_demand[static_cast<size_t>(n) * E + e] = 0;
+        for (uint32_t s = 0; s < D; ++s) {
+            const unsigned long long a = demand[static_cast<size_t>(s) * E + e];
+            if (!a) continue;
+            const uint32_t n = g2n[s];
+            const uint32_t d = dest_lut[static_cast<size_t>(n) * E + e];
+            if (d == 255) {
+                atomicOr(err, kErrUncovered);
+                continue;
+            }
+            col += a;
+            if (node_demand) node_demand[static_cast<size_t>(n) * E + e] += a;
+            atomicAdd(&s_g[d], a);
+            if (g2n[d] == n)
+                intra += a;
+            else
+                inter += a;
+        }
+        if (expert_count) expert_count[e] = col;
+    }
+    atomicAdd(&s_g[D], inter);
+    atomicAdd(&s_g[D + 1], intra);
+    __syncthreads();
+    if (group_pairs)
+        for (uint32_t d = threadIdx.x; d < D; d += blockDim.x) group_pairs[d] = s_g[d];
+    if (inter_intra && threadIdx.x == 0) {
+        inter_intra[0] = s_g[D];
+        inter_intra[1] = s_g[D + 1];
+    }
+}
+
+constexpr size_t kSmemLimit = 160 * 1024;
+
+}  // namespace
+
+mpb_status launch_layout(mpb_context *ctx, const mpb_tokens *tk, const mpb_placement *pl,
+                         uint64_t *demand, uint64_t *tag_pop, int32_t *sorted_pairs,
+                         int32_t *pair_pos, int64_t *key_offsets) {
+    // the permutation is requested through key_offsets (never empty: D*E+1
+    // entries); sorted_pairs / pair_pos may be NULL only when T*k == 0
+    const bool perm = key_offsets != nullptr;
+    if (perm && tk->T && (!pair_pos || !sorted_pairs))
+        return fail(MPB_VALIDATION_ERROR,
+                    "mpb_dispatch_layout: sorted_pairs, pair_pos and key_offsets go together");
+    if (!demand) return fail(MPB_VALIDATION_ERROR, "mpb_dispatch_layout: demand is NULL");
+    if (tk->k == 0) return fail(MPB_CONFIG_ERROR, "mpb_dispatch_layout: k must be >= 1");
+    if (tk->tag && !tag_pop)
+        return fail(MPB_VALIDATION_ERROR, "mpb_dispatch_layout: tag given without tag_pop");
+    const uint64_t P = tk->T * tk->k;
+    if (P > 0x7fffffffull)
+        return fail(MPB_CONFIG_ERROR, "mpb_dispatch_layout: T*k must fit int32 pair ids");
+    if (perm && pl->NS * kWarps * 4 > kSmemLimit)
+        return fail(MPB_CONFIG_ERROR, "mpb_dispatch_layout: too many (group, expert) slots "
+                                      "for the permutation");
+    if (P == 0) {
+        if (perm) {
+            // every offset is zero
+            MPB_CUDA(cudaMemsetAsync(key_offsets, 0, sizeof(int64_t) * (size_t(pl->D) * pl->E + 1),
+                                     ctx->stream));
+        }
+        return MPB_OK;
+    }
+    LayoutParams p{};
+    p.idx = tk->idx;
+    p.P = P;
+    p.T = tk->T;
+    p.k = tk->k;
+    p.src_group = tk->src_group;
+    p.src_base = tk->src_base;
+    p.src_span = tk->src_span;
+    p.tag = tk->tag;
+    p.n_tags = tk->tag ? tk->n_tags : 0;
+    p.g2n = pl->d_g2n;
+    p.slot_lut = pl->d_slot_lut;
+    p.D = pl->D;
+    p.E = pl->E;
+    p.NS = pl->NS;
+    p.demand = demand;
+    p.tag_pop = tag_pop;
+    p.err = ctx->d_error;
+    size_t smem = perm ? size_t(pl->NS) * 4 : 0;
+    p.demand_smem = smem + size_t(pl->D) * pl->E * 4 <= kSmemLimit;
+    if (p.demand_smem) smem += size_t(pl->D) * pl->E * 4;
+    p.tag_smem = p.n_tags && smem + size_t(p.n_tags) * pl->E * 4 <= kSmemLimit;
+    if (p.tag_smem) smem += size_t(p.n_tags) * pl->E * 4;
+    const uint32_t nb = static_cast<uint32_t>((P + kChunk - 1) / kChunk);
+    if (perm) {
+        MPB_CUDA(ctx->ensure_scratch(size_t(nb) * pl->NS * 4));
+        p.bhist = static_cast<uint32_t *>(ctx->scratch);
+    }
+    if (perm) {
+        MPB_CUDA(cudaFuncSetAttribute(k_layout_count<true>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        k_layout_count<true><<<nb, kThreads, smem, ctx->stream>>>(p);
+    } else {
+        MPB_CUDA(cudaFuncSetAttribute(k_layout_count<false>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        k_layout_count<false><<<nb, kThreads, smem, ctx->stream>>>(p);
+    }
+    MPB_LAUNCHED(ctx);
+    if (!perm) return MPB_OK;
+    const size_t scan_smem = (size_t(pl->NS) + 1) * 4;
+    MPB_CUDA(cudaFuncSetAttribute(k_layout_scan, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(scan_smem)));
+    k_layout_scan<<<1, 1024, scan_smem, ctx->stream>>>(p.bhist, nb, pl->NS, pl->d_key_lb,
+                                                       pl->D * pl->E, key_offsets);
+    MPB_LAUNCHED(ctx);
+    const size_t sc_smem = size_t(kWarps) * pl->NS * 4;
+    MPB_CUDA(cudaFuncSetAttribute(k_layout_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(sc_smem)));
+    k_layout_scatter<<<nb, kThreads, sc_smem, ctx->stream>>>(p, sorted_pairs, pair_pos);
+    MPB_LAUNCHED(ctx);
+    return MPB_OK;
+}
+
+mpb_status launch_layout_derive(mpb_context *ctx, const mpb_placement *pl, const uint64_t *demand,
+                                uint64_t *expert_count, uint64_t *group_pairs,
+                                uint64_t *node_demand, uint64_t *inter_intra) {
+    const size_t smem = (size_t(pl->D) + 2) * 8;
+    k_layout_derive<<<1, 256, smem, ctx->stream>>>(demand, pl->d_g2n, pl->d_dest_lut, pl->D, pl->E,
+                                                   pl->nodes, expert_count, group_pairs,
+                                                   node_demand, inter_intra, ctx->d_error);
+    MPB_LAUNCHED(ctx);
+    return MPB_OK;
+}
+
+}  // namespace mpb
+
+using namespace mpb;
+
+extern "C" {
+
+mpb_status mpb_dispatch_layout(mpb_context *ctx, const mpb_tokens *tokens,
+                               const mpb_placement *placement, uint64_t *demand,
+                               uint64_t *tag_pop, int32_t *sorted_pairs, int32_t *pair_pos,
+                               int64_t *key_offsets) {
+    if (!ctx || !tokens || !placement)
+        return fail(MPB_VALIDATION_ERROR, "mpb_dispatch_layout: NULL argument");
+    if (tokens->T && !tokens->idx)
+        return fail(MPB_VALIDATION_ERROR, "mpb_dispatch_layout: idx is NULL");
+    if (!tokens->src_group && tokens->src_span == 0 && tokens->T)
+        return fail(MPB_CONFIG_ERROR, "mpb_dispatch_layout: src_group NULL needs src_span >= 1");
+    return launch_layout(ctx, tokens, placement, demand, tag_pop, sorted_pairs, pair_pos,
+                         key_offsets);
+}
+
+mpb_status mpb_layout_derive(mpb_context *ctx, const mpb_placement *placement,
+                             const uint64_t *demand, uint64_t *expert_count,
+                             uint64_t *group_pairs, uint64_t *node_demand,
+                             uint64_t *inter_intra) {
+    if (!ctx || !placement || !demand)
+        return fail(MPB_VALIDATION_ERROR, "mpb_layout_derive: NULL argument");
+    return launch_layout_derive(ctx, placement, demand, expert_count, group_pairs, node_demand,
+                                inter_intra);
+}
+
+}  // extern "C"

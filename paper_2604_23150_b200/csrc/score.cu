@@ -1,0 +1,235 @@
+// K5: batched placement-cost evaluator (sm_100a).
+//
+// simulate_layer (/root/reference/proj/core/src/simulator.cpp:43-99) only
+// depends on a batch through its demand per (source node, expert): the
+// destination of a pair is fixed by (node(src), expert) under a placement
+// (simulator.cpp:74-80), bytes are count * hidden * bpe (:57-58, :81), and
+// inter/intra is node(dest) != node(src) (:82-85). So P candidates x B batches
+// reduce to P*B lookups over a [nodes x E] demand table:
+//   k_batch_demand : CSR matrix rows sampled into B batches -> node_demand
+//                    (the BatchAssignment assembly of compare_strategies,
+//                    simulator.cpp:154-181), smem-privatised counters.
+//   k_score        : one CTA per candidate (its LUT in smem), one warp per
+//                    batch; integer pair counts per destination rank.
+//   k_finalize     : LayerSim doubles with the reference's exact expression
+//                    order (:27-41, :90-98), correctly rounded dadd/dmul/ddiv
+//                    intrinsics so the result is bit-identical to the host.
+// Algorithmic bytes per (candidate, batch): nodes*E*8 (demand) + nodes*E
+// (LUT, reused across batches from smem) + (2 + D)*8 out.
+#include "internal.cuh"
+
+namespace mpb {
+namespace {
+
+__global__ void __launch_bounds__(256) k_batch_demand(const uint32_t *row_ptr, const uint32_t *cols,
+                                                      const uint32_t *vals, uint32_t R,
+                                                      const uint32_t *rows, const uint8_t *src,
+                                                      uint32_t S, const uint8_t *g2n, uint32_t D,
+                                                      uint32_t nodes, uint32_t E, int use_smem,
+                                                      uint64_t *node_demand, uint32_t *err) {
+    extern __shared__ uint32_t s_nd[];  // [nodes*E]
+    const uint32_t b = blockIdx.x;
+    uint64_t *out = node_demand + static_cast<size_t>(b) * nodes * E;
+    if (use_smem) {
+        for (uint32_t i = threadIdx.x; i < nodes * E; i += blockDim.x) s_nd[i] = 0;
+    } else {
+        for (uint32_t i = threadIdx.x; i < nodes * E; i += blockDim.x) out[i] = 0;
+    }
+    __syncthreads();
+    // one warp per sampled slot, lanes over the row's non-zeros
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (uint32_t i = warp; i < S; i += blockDim.x / 32) {
+        const uint32_t r = rows[static_cast<size_t>(b) * S + i];
+        const uint32_t s = src[static_cast<size_t>(b) * S + i];
+        if (r >= R || s >= D) {
+            if (lane == 0) atomicOr(err, kErrSourceRange);
+            continue;
+        }
+        const uint32_t n = g2n[s];
+        for (uint32_t z = row_ptr[r] + lane; z < row_ptr[r + 1]; z += 32) {
+            const uint32_t e = cols[z];
+            if (e >= E) {
+                atomicOr(err, kErrExpertRange);
+                continue;
+            }
+            if (use_smem)
+                atomicAdd(s_nd + n * E + e, vals[z]);
+            else
+                atomicAdd(reinterpret_cast<unsigned long long *>(out) + n * E + e,
+                          static_cast<unsigned long long>(vals[z]));
+        }
+    }
+    __syncthreads();
+    if (use_smem)
+        for (uint32_t i = threadIdx.x; i < nodes * E; i += blockDim.x) out[i] = s_nd[i];
+}
+
+constexpr int kScoreWarps = 8;
+
+__global__ void __launch_bounds__(kScoreWarps * 32) k_score(const uint64_t *node_demand, uint32_t B,
+                                                            const uint8_t *luts,
+                                                            const uint8_t *g2n_g, uint32_t D,
+                                                            uint32_t nodes, uint32_t E,
+                                                            uint64_t *inter_out,
+                                                            uint64_t *intra_out,
+                                                            uint64_t *rank_out, uint32_t *err) {
+    extern __shared__ unsigned char s_raw[];
+    const uint32_t NE = nodes * E;
+    unsigned long long *s_rank = reinterpret_cast<unsigned long long *>(s_raw);  // [warps][D]
+    uint8_t *s_lut = s_raw + kScoreWarps * D * 8;
+    uint8_t *s_g2n = s_lut + NE;
+    const uint32_t p = blockIdx.x;
+    const uint8_t *lut = luts + static_cast<size_t>(p) * NE;
+    for (uint32_t i = threadIdx.x; i < NE; i += blockDim.x) s_lut[i] = lut[i];
+    for (uint32_t i = threadIdx.x; i < D; i += blockDim.x) s_g2n[i] = g2n_g[i];
+    __syncthreads();
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned long long *rank = s_rank + warp * D;
+    for (uint32_t b = blockIdx.y * kScoreWarps + warp; b < B; b += gridDim.y * kScoreWarps) {
+        for (uint32_t d = lane; d < D; d += 32) rank[d] = 0;
+        __syncwarp();
+        const uint64_t *a = node_demand + static_cast<size_t>(b) * NE;
+        unsigned long long inter = 0, intra = 0;
+        for (uint32_t i = lane; i < NE; i += 32) {
+            const unsigned long long v = a[i];
+            if (!v) continue;
+            const uint32_t d = s_lut[i];
+            if (d == 255) {
+                atomicOr(err, kErrUncovered);
+                continue;
+            }
+            atomicAdd(rank + d, v);
+            if (s_g2n[d] == i / E)
+                intra += v;
+            else
+                inter += v;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            inter += __shfl_xor_sync(0xffffffffu, inter, o);
+            intra += __shfl_xor_sync(0xffffffffu, intra, o);
+        }
+        __syncwarp();
+        const size_t cell = static_cast<size_t>(p) * B + b;
+        if (lane == 0) {
+            inter_out[cell] = inter;
+            intra_out[cell] = intra;
+        }
+        for (uint32_t d = lane; d < D; d += 32) rank_out[cell * D + d] = rank[d];
+        __syncwarp();
+    }
+}
+
+struct CostParams {
+    double hidden, bpe, inter_bw, intra_bw, etpt, overhead;
+};
+
+__global__ void k_finalize(const uint64_t *inter, const uint64_t *intra, const uint64_t *rank,
+                           uint64_t N, uint32_t D, CostParams c, uint32_t tp_exp, int spans,
+                           double *out, double *payload) {
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    // bytes_per_token = double(hidden) * double(bpe) (simulator.cpp:57-58)
+    const double bpt = __dmul_rn(c.hidden, c.bpe);
+    double mx = 0.0, straggler = 0.0;
+    for (uint32_t d = 0; d < D; ++d) {
+        const double pairs = static_cast<double>(rank[i * D + d]);
+        const double bytes = __dmul_rn(pairs, bpt);
+        if (payload) payload[i * D + d] = bytes;
+        if (d == 0 || bytes > mx) mx = bytes;
+        if (d == 0 || pairs > straggler) straggler = pairs;
+    }
+    const double bw = spans ? c.inter_bw : c.intra_bw;
+    // max_payload / tp_exp / bandwidth (simulator.cpp:40)
+    const double dispatch = __ddiv_rn(__ddiv_rn(mx, static_cast<double>(tp_exp)), bw);
+    const double compute = __dmul_rn(c.etpt, straggler);
+    // dispatch + compute + combine + overhead, left to right (simulator.cpp:96-97)
+    const double layer = __dadd_rn(__dadd_rn(__dadd_rn(dispatch, compute), dispatch), c.overhead);
+    double *o = out + i * 6;
+    o[0] = __dmul_rn(static_cast<double>(inter[i]), bpt);
+    o[1] = __dmul_rn(static_cast<double>(intra[i]), bpt);
+    o[2] = dispatch;
+    o[3] = compute;
+    o[4] = dispatch;
+    o[5] = layer;
+}
+
+}  // namespace
+}  // namespace mpb
+
+using namespace mpb;
+
+extern "C" {
+
+mpb_status mpb_batch_demand(mpb_context *ctx, const uint32_t *row_ptr, const uint32_t *cols,
+                            const uint32_t *vals, uint32_t R, const uint32_t *rows,
+                            const uint8_t *src, uint32_t B, uint32_t S, const uint8_t *group_to_node,
+                            uint32_t D, uint32_t nodes, uint32_t E, uint64_t *node_demand) {
+    if (!ctx || !row_ptr || !rows || !src || !group_to_node || !node_demand)
+        return fail(MPB_VALIDATION_ERROR, "mpb_batch_demand: NULL argument");
+    if (B == 0) return MPB_OK;
+    const size_t smem = size_t(nodes) * E * 4;
+    const int use_smem = smem <= 160 * 1024;
+    if (use_smem)
+        MPB_CUDA(cudaFuncSetAttribute(k_batch_demand, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(smem)));
+    k_batch_demand<<<B, 256, use_smem ? smem : 0, ctx->stream>>>(
+        row_ptr, cols, vals, R, rows, src, S, group_to_node, D, nodes, E, use_smem, node_demand,
+        ctx->d_error);
+    MPB_LAUNCHED(ctx);
+    return MPB_OK;
+}
+
+mpb_status mpb_score_placements(mpb_context *ctx, const uint64_t *node_demand, uint32_t B,
+                                const uint8_t *luts, uint32_t P, const uint8_t *group_to_node,
+                                uint32_t D, uint32_t nodes, uint32_t E, uint64_t *inter,
+                                uint64_t *intra, uint64_t *rank_pairs) {
+    if (!ctx || !node_demand || !luts || !group_to_node || !inter || !intra || !rank_pairs)
+        return fail(MPB_VALIDATION_ERROR, "mpb_score_placements: NULL argument");
+    if (D == 0 || D > 255 || nodes == 0)
+        return fail(MPB_CONFIG_ERROR, "mpb_score_placements: need 1 <= D <= 255, nodes >= 1");
+    if (P == 0 || B == 0) return MPB_OK;
+    const size_t smem = size_t(kScoreWarps) * D * 8 + size_t(nodes) * E + D;
+    if (smem > 200 * 1024) return fail(MPB_CONFIG_ERROR, "mpb_score_placements: nodes*E too large");
+    MPB_CUDA(cudaFuncSetAttribute(k_score, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    // enough CTAs to fill the machine: split batches across grid.y when P is small
+    uint32_t gy = (B + kScoreWarps - 1) / kScoreWarps;
+    const uint32_t want = 4u * static_cast<uint32_t>(ctx->num_sms);
+    if (static_cast<uint64_t>(P) * gy > want) gy = std::max(1u, want / std::max(1u, P));
+    gy = std::min(gy, 65535u);
+    dim3 grid(P, gy);
+    k_score<<<grid, kScoreWarps * 32, smem, ctx->stream>>>(node_demand, B, luts, group_to_node, D,
+                                                           nodes, E, inter, intra, rank_pairs,
+                                                           ctx->d_error);
+    MPB_LAUNCHED(ctx);
+    return MPB_OK;
+}
+
+mpb_status mpb_finalize_layer_sims(mpb_context *ctx, const uint64_t *inter, const uint64_t *intra,
+                                   const uint64_t *rank_pairs, uint64_t N, uint32_t D,
+                                   const double *cost, uint32_t tp_exp, int spans_nodes,
+                                   double *out, double *payload) {
+    if (!ctx || !inter || !intra || !rank_pairs || !cost || !out)
+        return fail(MPB_VALIDATION_ERROR, "mpb_finalize_layer_sims: NULL argument");
+    // CostModelParams::validate (simulator.cpp:14-25)
+    if (cost[0] < 1 || cost[1] < 1)
+        return fail(MPB_CONFIG_ERROR, "cost model: hidden_dim and bytes_per_element must be >= 1");
+    if (cost[2] <= 0.0 || cost[3] <= 0.0)
+        return fail(MPB_CONFIG_ERROR, "cost model: bandwidths must be positive");
+    if (cost[3] < cost[2])
+        return fail(MPB_CONFIG_ERROR, "cost model: intra_node_bandwidth must be >= inter_node_bandwidth");
+    if (cost[4] <= 0.0)
+        return fail(MPB_CONFIG_ERROR, "cost model: expert_time_per_token must be positive");
+    if (cost[5] < 0.0)
+        return fail(MPB_CONFIG_ERROR, "cost model: fixed_layer_overhead must be >= 0");
+    if (tp_exp == 0) return fail(MPB_CONFIG_ERROR, "topology: tp_exp must be >= 1");
+    if (N == 0) return MPB_OK;
+    CostParams c{cost[0], cost[1], cost[2], cost[3], cost[4], cost[5]};
+    const unsigned blocks = static_cast<unsigned>((N + 255) / 256);
+    k_finalize<<<blocks, 256, 0, ctx->stream>>>(inter, intra, rank_pairs, N, D, c, tp_exp,
+                                                spans_nodes, out, payload);
+    MPB_LAUNCHED(ctx);
+    return MPB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,309 @@
+"""GPU parity: every CUDA kernel of libmoeplace_b200.so against the C oracle and
+the golden fixtures generated from the compiled reference. Integer, byte and
+index outputs must be bit-exact; LayerSim doubles bit-exact (exact integer
+sums, reference expression order); softmax / sigmoid weights within 2e-6
+relative (fp32 expf vs the oracle's double exp)."""
+import json
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from paper_2604_23150_b200 import moeplace as mp  # noqa: E402
+from paper_2604_23150_b200.errors import ConfigError, ValidationError  # noqa: E402
+
+W_RTOL = 2e-6
+
+
+@pytest.fixture(scope="module")
+def eng():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return mp.Engine(0)
+
+
+def dev(a, dtype=None):
+    t = torch.from_numpy(np.ascontiguousarray(a))
+    if dtype is not None:
+        t = t.to(dtype)
+    return t.cuda()
+
+
+def random_idx(rng, T, E, k):
+    if T == 0:
+        return np.zeros((0, k), np.int32)
+    return np.argsort(rng.random((T, E)), axis=1)[:, :k].astype(np.int32)
+
+
+def make_placement(rng, E, D, red):
+    groups = [list(range(d * E // D, (d + 1) * E // D)) for d in range(D)]
+    for g in groups:
+        g += [e for e in rng.permutation(E).tolist() if e not in g][:red]
+    return mp.Placement(groups, E, red * D, len(groups[0]))
+
+
+def topo(D, nodes):
+    return mp.Topology(D, 1, D, 1, nodes, D // nodes, [d // (D // nodes) for d in range(D)])
+
+
+# ---------------------------------------------------------------- simulate_layer
+
+
+def test_simulate_tokens_golden_bit_exact(eng, golden):
+    z = np.load(golden / "sim_tokens.npz")
+    for ci in range(int(z["n_cases"])):
+        E = int(z[f"c{ci}_E"])
+        groups = z[f"c{ci}_groups"].tolist()
+        t = z[f"c{ci}_topo"].tolist()
+        top = mp.Topology(*t, group_to_node=z[f"c{ci}_g2n"].tolist())
+        c = z[f"c{ci}_cost"].tolist()
+        cost = mp.CostModelParams(int(c[0]), int(c[1]), *c[2:])
+        pl = mp.Placement(groups, E, len(groups[0]) * len(groups) - E, len(groups[0]))
+        sim = mp.simulate_tokens(dev(z[f"c{ci}_idx"]), dev(z[f"c{ci}_src"], torch.uint8), pl,
+                                 top, cost, engine=eng)
+        out = z[f"c{ci}_out"]
+        got = [sim.inter_node_bytes, sim.intra_node_bytes, sim.dispatch_time,
+               sim.expert_compute_time, sim.combine_time, sim.layer_time]
+        assert got == out.tolist(), ci
+        assert sim.per_rank_payload == z[f"c{ci}_payload"].tolist(), ci
+
+
+def test_simulate_layer_known_answers(eng, golden):
+    cases = {c["name"]: c for c in json.loads((golden / "known_answers.json").read_text())}
+    for name in ("node_local", "cross_node_token", "conservation", "redundant_same_node"):
+        c = cases[name]
+        t = c["topology"]
+        top = mp.Topology(t["dp"], t["tp"], t["ep"], t["tp_exp"], t["nodes"], t["gpus_per_node"],
+                          t["group_to_node"])
+        cost = mp.CostModelParams(int(c["cost"][0]), int(c["cost"][1]), *c["cost"][2:])
+        pl = mp.Placement(c["groups"], c["E"], 0, len(c["groups"][0]))
+        batch = mp.BatchAssignment([mp.BatchRequest(0, c["src"][0],
+                                                    [tuple(p) for p in c["experts"]])])
+        sim = mp.simulate_layer(batch, pl, top, cost, engine=eng)
+        got = [sim.inter_node_bytes, sim.intra_node_bytes, sim.dispatch_time,
+               sim.expert_compute_time, sim.combine_time, sim.layer_time]
+        assert got == c["ref"]["out"], name
+        assert sim.per_rank_payload == c["ref"]["payload"], name
+    # uncovered expert -> ValidationError (simulator_test.cpp:100-109)
+    c = cases["uncovered"]
+    top = mp.Topology.contiguous(2, 1, 2, 1, 2)
+    with pytest.raises(ValidationError):
+        mp.simulate_layer(mp.BatchAssignment([mp.BatchRequest(0, 0, [(3, 1)])]),
+                          mp.Placement([[0, 1], [2, 0]], 4, 0, 2), top,
+                          mp.CostModelParams(4096, 1, 50e9, 200e9, 1e-7, 1e-5), engine=eng)
+    # topology.ep != D -> ConfigError (simulator.cpp:47-50)
+    with pytest.raises(ConfigError):
+        mp.simulate_layer(mp.BatchAssignment(), mp.Placement([[0, 1], [2, 3]], 4, 0, 2),
+                          mp.Topology.contiguous(4, 1, 4, 1, 2), mp.CostModelParams(),
+                          engine=eng)
+    # source group out of range -> ValidationError
+    with pytest.raises(ValidationError):
+        mp.simulate_layer(mp.BatchAssignment([mp.BatchRequest(0, 5, [(0, 1)])]),
+                          mp.Placement([[0, 1], [2, 3]], 4, 0, 2), top, mp.CostModelParams(),
+                          engine=eng)
+
+
+def test_simulate_tokens_uncovered_and_range_errors(eng):
+    pl = mp.Placement([[0, 1], [2, 0]], 4, 0, 2)
+    top = mp.Topology.contiguous(2, 1, 2, 1, 2)
+    cost = mp.CostModelParams()
+    with pytest.raises(ValidationError):
+        mp.simulate_tokens(dev(np.array([[3]], np.int32)), dev(np.array([0], np.uint8)), pl, top,
+                           cost, engine=eng)
+    with pytest.raises(ValidationError):
+        mp.simulate_tokens(dev(np.array([[7]], np.int32)), dev(np.array([0], np.uint8)), pl, top,
+                           cost, engine=eng)
+    with pytest.raises(ValidationError):
+        mp.simulate_tokens(dev(np.array([[0]], np.int32)), dev(np.array([2], np.uint8)), pl, top,
+                           cost, engine=eng)
+    # the context recovers after an error
+    sim = mp.simulate_tokens(dev(np.array([[0]], np.int32)), dev(np.array([1], np.uint8)), pl,
+                             top, cost, engine=eng)
+    assert sim.intra_node_bytes == 7168.0
+
+
+@pytest.mark.parametrize("name", ["qwen3_c1", "desk_default"])
+def test_compare_strategies_golden_bit_exact(eng, golden, name):
+    sc = json.loads((golden / f"compare_{name}.json").read_text())
+    dm = sc["decode_matrix"]
+    M = mp.ActivationMatrix(dm["rows"], dm["cols"],
+                            np.array(dm["values"], np.int64).reshape(dm["rows"], dm["cols"]),
+                            dm["row_labels"], dm["request_ids"])
+    t = sc["topology"]
+    top = mp.Topology(t["dp"], t["tp"], t["ep"], t["tp_exp"], t["nodes"], t["gpus_per_node"],
+                      t["group_to_node"])
+    c = sc["cost"]
+    cost = mp.CostModelParams(int(c[0]), int(c[1]), *c[2:])
+    strategies = [mp.StrategyEntry(s["label"], mp.Placement(s["groups"], s["E"], 0, s["M"]),
+                                   s["cluster_routed"]) for s in sc["strategies"]]
+    table = mp.compare_strategies(M, strategies, sc["routes"], top, cost, sc["num_batches"],
+                                  sc["batch_size"], sc["seed"], engine=eng)
+    assert len(table.rows) == len(sc["rows"])
+    for mine, ref in zip(table.rows, sc["rows"]):
+        assert (mine.batch, mine.strategy) == (ref["batch"], ref["strategy"])
+        s = mine.sim
+        assert [s.inter_node_bytes, s.intra_node_bytes, s.dispatch_time, s.expert_compute_time,
+                s.combine_time, s.layer_time] == [
+            ref["inter_node_bytes"], ref["intra_node_bytes"], ref["dispatch_time"],
+            ref["expert_compute_time"], ref["combine_time"], ref["layer_time"]]
+        assert s.per_rank_payload == ref["per_rank_payload"]
+        assert mine.normalized == ref["normalized"]
+    assert table.linear_median_bytes == sc["linear_median_bytes"]
+    for mine, ref in zip(table.summary, sc["summary"]):
+        for key in ("median_inter_node_bytes", "q25_inter_node_bytes", "q75_inter_node_bytes",
+                    "normalized_median", "median_dispatch_time", "median_expert_compute_time",
+                    "median_combine_time", "median_layer_time"):
+            assert getattr(mine, key) == ref[key], (ref["strategy"], key)
+
+
+def test_device_sampler_matches_oracle(eng, oracle):
+    rng = np.random.default_rng(3)
+    for R, B, S in ((1, 3, 5), (256, 200, 128), (4097, 17, 300)):
+        sizes = rng.integers(1, 4, R).astype(np.int32)
+        rows, picks = eng.sample_batches(12345, B, R, S, dev(sizes))
+        rows = rows.cpu().numpy()
+        picks = picks.cpu().numpy()
+        for b in range(B):
+            r, p = oracle.sample_batch(12345, b, R, S, sizes.astype(np.uint32))
+            np.testing.assert_array_equal(rows[b], r.astype(np.int64))
+            np.testing.assert_array_equal(picks[b], p)
+
+
+# ---------------------------------------------------------------- layout / permutation
+
+LAYOUT_CASES = [  # T, E, D, nodes, k, redundancy, block_src
+    (0, 64, 4, 2, 2, 0, False), (1, 16, 2, 2, 2, 0, False), (999, 64, 4, 2, 4, 1, False),
+    (4096, 128, 8, 2, 8, 0, False), (5000, 256, 8, 4, 8, 2, True), (70000, 128, 8, 8, 1, 0, False),
+    (65536, 256, 8, 2, 8, 0, True), (3333, 64, 16, 4, 6, 3, False)]
+
+
+@pytest.mark.parametrize("case", LAYOUT_CASES)
+def test_dispatch_layout_bit_exact(eng, oracle, case):
+    T, E, D, nodes, k, red, block_src = case
+    rng = np.random.default_rng(T + E)
+    idx = random_idx(rng, T, E, k)
+    src = ((np.arange(T) * D) // max(T, 1)).astype(np.uint8) if block_src else \
+        rng.integers(0, D, T).astype(np.uint8)
+    pl = make_placement(rng, E, D, red)
+    top = topo(D, nodes)
+    tag = rng.integers(0, 5, T).astype(np.uint8)
+    dp = eng.placement(pl, top)
+    kw = dict(src_base=0, src_span=D) if block_src else dict(src=dev(src))
+    lay = eng.dispatch_layout(dev(idx), dp, tag=dev(tag), n_tags=5, **kw)
+    der = eng.layout_derive(dp, lay["demand"])
+    eng.sync()
+    lut = oracle.dest_lut(pl.groups, top.group_to_node, E)
+    ref = oracle.dispatch_layout(idx, src.astype(np.uint32), lut, D, E, top.group_to_node)
+    np.testing.assert_array_equal(lay["demand"].cpu().numpy(), ref["demand"])
+    np.testing.assert_array_equal(lay["sorted_pairs"].cpu().numpy(), ref["sorted_pairs"])
+    np.testing.assert_array_equal(lay["pair_pos"].cpu().numpy(), ref["pair_pos"])
+    np.testing.assert_array_equal(lay["key_offsets"].cpu().numpy(), ref["key_offsets"])
+    np.testing.assert_array_equal(der["expert_count"].cpu().numpy(), ref["expert_count"])
+    np.testing.assert_array_equal(der["group_pairs"].cpu().numpy(), ref["group_pairs"])
+    np.testing.assert_array_equal(der["node_demand"].cpu().numpy(), ref["node_demand"])
+    assert der["inter_intra"].cpu().tolist() == [ref["inter_pairs"], ref["intra_pairs"]]
+    pop = oracle.domain_popularity(idx, tag.astype(np.uint32), 5, E)
+    np.testing.assert_array_equal(lay["tag_pop"].cpu().numpy(), pop)
+
+
+def test_layout_accumulates_across_shards(eng, oracle):
+    rng = np.random.default_rng(11)
+    T, E, D, k = 8192, 128, 8, 8
+    idx = random_idx(rng, T, E, k)
+    src = rng.integers(0, D, T).astype(np.uint8)
+    pl = make_placement(rng, E, D, 0)
+    top = topo(D, 2)
+    dp = eng.placement(pl, top)
+    demand = torch.zeros(D, E, dtype=torch.uint64, device="cuda")
+    for s in range(4):
+        sl = slice(s * T // 4, (s + 1) * T // 4)
+        eng.dispatch_layout(dev(idx[sl]), dp, src=dev(src[sl]), permutation=False, demand=demand)
+    eng.sync()
+    lut = oracle.dest_lut(pl.groups, top.group_to_node, E)
+    ref = oracle.dispatch_layout(idx, src.astype(np.uint32), lut, D, E, top.group_to_node)
+    np.testing.assert_array_equal(demand.cpu().numpy(), ref["demand"])
+
+
+# ---------------------------------------------------------------- co-activation
+
+
+@pytest.mark.parametrize("T,E,k", [(1, 8, 2), (33, 64, 2), (4096, 128, 8), (20000, 256, 8),
+                                   (3000, 100, 5), (5000, 128, 1)])
+def test_coactivation_bit_exact(eng, oracle, T, E, k):
+    rng = np.random.default_rng(T * 7 + E)
+    idx = random_idx(rng, T, E, k)
+    c = eng.coactivation(dev(idx), E)
+    eng.sync()
+    np.testing.assert_array_equal(c.cpu().numpy(), oracle.coactivation(idx, E))
+
+
+def test_coactivation_skewed_domains(eng, oracle):
+    tap = oracle.generate_trace_tap(4, 40, 16, 0.9, 16.0, 3, 128, 8, 1)
+    idx = tap["picks"].reshape(-1, 8)
+    c = eng.coactivation(dev(idx), 128)
+    eng.sync()
+    np.testing.assert_array_equal(c.cpu().numpy(), oracle.coactivation(idx, 128))
+
+
+# ---------------------------------------------------------------- top-k
+
+
+@pytest.mark.parametrize("T,E,k,fn,renorm", [(1000, 128, 8, 0, False), (777, 256, 8, 1, True),
+                                             (4096, 128, 1, 1, False), (100, 64, 6, 0, True),
+                                             (50, 1000, 16, 0, False), (64, 32, 2, 1, False)])
+def test_topk_logits(eng, oracle, T, E, k, fn, renorm):
+    rng = np.random.default_rng(E + k)
+    lg = rng.standard_normal((T, E)).astype(np.float32)
+    lg[::7, 3] = lg[::7, 5]  # exact ties -> lower id first
+    lg[::11, :4] = np.round(lg[::11, :4])
+    lg[5, 2] = np.nan
+    idx, w = eng.topk_logits(dev(lg), k, fn, renorm)
+    eng.sync()
+    ri, rw = oracle.topk_logits(lg, k, fn, renorm)
+    np.testing.assert_array_equal(idx.cpu().numpy(), ri)
+    np.testing.assert_allclose(w.cpu().numpy(), rw, rtol=W_RTOL, atol=1e-7)
+
+
+# ---------------------------------------------------------------- scoring
+
+
+def test_score_placements_bit_exact(eng, oracle):
+    rng = np.random.default_rng(9)
+    for E, D, nodes, P, B in ((64, 4, 2, 3, 200), (256, 8, 2, 1024, 4), (128, 8, 4, 37, 65),
+                              (128, 64, 8, 5, 9)):
+        nd = rng.integers(0, 1000, (B, nodes, E)).astype(np.uint64)
+        nd[nd < 300] = 0
+        g2n = [d // (D // nodes) for d in range(D)]
+        luts = np.stack([oracle.dest_lut(make_placement(rng, E, D, p % 3).groups, g2n, E)
+                         for p in range(P)])
+        inter, intra, rank = eng.score_placements(dev(nd), dev(luts), dev(np.array(g2n, np.uint8)),
+                                                  D)
+        eng.sync()
+        ri, ra, rr = oracle.score_placements(nd, luts, D, g2n)
+        np.testing.assert_array_equal(inter.cpu().numpy(), ri)
+        np.testing.assert_array_equal(intra.cpu().numpy(), ra)
+        np.testing.assert_array_equal(rank.cpu().numpy(), rr)
+
+
+# ---------------------------------------------------------------- dispatch / combine
+
+
+def test_gather_combine_round_trip(eng):
+    rng = np.random.default_rng(2)
+    T, E, D, k, H = 3000, 64, 4, 4, 7168
+    idx = random_idx(rng, T, E, k)
+    pl = make_placement(rng, E, D, 0)
+    top = topo(D, 2)
+    dp = eng.placement(pl, top)
+    lay = eng.dispatch_layout(dev(idx), dp, src=dev(rng.integers(0, D, T).astype(np.uint8)))
+    X = torch.randn(T, H, device="cuda").to(torch.bfloat16)
+    send = eng.dispatch_gather(X, lay["sorted_pairs"], k)
+    sp = lay["sorted_pairs"].long()
+    assert torch.equal(send, X[sp // k])
+    w = torch.rand(T, k, device="cuda")
+    Y = eng.combine_scatter(send, lay["pair_pos"], w)
+    eng.sync()
+    ref = (w.unsqueeze(-1) * X.float().unsqueeze(1)).sum(1)
+    torch.testing.assert_close(Y.float(), ref, rtol=1e-2, atol=1e-2)

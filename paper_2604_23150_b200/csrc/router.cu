@@ -1,12 +1,341 @@
-// K1 placeholder: replaced by the tcgen05 router GEMM in the next commit.
+// K1: router GEMM + fused top-k on tcgen05 tensor cores (sm_100a).
+//
+// logits[T, E] = X[T, H] . W[E, H]^T with bf16 inputs and fp32 accumulation,
+// followed in the same kernel by softmax/sigmoid top-k selection. The whole
+// expert dimension (E = N <= 256) is one UMMA tile, so one 128-token tile's
+// logits live in TMEM (128 lanes x N fp32 columns) and the epilogue owns one
+// token per thread: no logits ever reach HBM (unless requested for parity
+// tests). No reference implementation exists (the reference samples routes
+// synthetically, /root/reference/proj/core/src/trace.cpp:240-259); selection
+// follows its lowest-index-wins tie rule (placement.cpp:143-152).
+//
+// Persistent, warp-specialised CTA (one per SM, 256 threads):
+//   warp 0     TMA producer: X tile [128 x 64] (evict-first) + W tile [N x 64]
+//              (evict-last, L2-resident across CTAs) per k-block into a
+//              STAGES-deep 128B-swizzled smem ring (mbarrier full/empty)
+//   warp 1     MMA issuer: 4 x tcgen05.mma (M=128, N, K=16) per k-block into a
+//              double-buffered TMEM accumulator; tcgen05.commit frees smem
+//              slots and hands finished accumulators to the epilogue
+//   warp 2     TMEM allocator (2*N columns)
+//   warps 4-7  epilogue: tcgen05.ld 32 columns at a time, running top-k in
+//              registers (static-index insertion network), max / sum-exp,
+//              then release the accumulator so the next tile's MMAs overlap
+// Roofline: FLOP/token = 2*H*E; bytes/token = 2*H (X) + 8*k out.
+#include <cudaTypedefs.h>
+
+#include <cfloat>
+#include <mutex>
+
 #include "internal.cuh"
+#include "tc_ptx.cuh"
+
+namespace mpb {
+namespace {
+
+constexpr int kBM = 128;
+constexpr int kBK = 64;  // 64 bf16 = 128 bytes: one 128B swizzle atom per row
+constexpr int kThreadsR = 256;
+
+template <int N>
+struct RCfg {
+    static constexpr int A_BYTES = kBM * kBK * 2;
+    static constexpr int B_BYTES = N * kBK * 2;
+    static constexpr int STAGE = A_BYTES + B_BYTES;
+    static constexpr int STAGES = (200 * 1024) / STAGE > 8 ? 8 : (200 * 1024) / STAGE;
+    static constexpr uint32_t TMEM_COLS = 2 * N < 32 ? 32 : 2 * N;
+    static constexpr int SMEM = 1024 + STAGES * STAGE + (2 * STAGES + 4) * 8 + 16;
+};
+
+struct RouterParams {
+    uint64_t T;
+    uint32_t H;
+    uint32_t k;
+    int score_fn;
+    int renorm;
+    uint32_t num_tiles;
+    int32_t *idx;
+    float *w;
+    float *logits;
+};
+
+// Selection order: (value desc, id asc), NaN below everything; a sentinel
+// slot (id < 0) is beaten by nothing.
+__device__ __forceinline__ bool sel_beats(float a, int ia, float b, int ib) {
+    if (ib < 0) return false;
+    const bool na = isnan(a), nb = isnan(b);
+    if (na || nb) return (na && nb) ? ia < ib : nb;
+    if (a != b) return a > b;
+    return ia < ib;
+}
+
+template <int N, int KMAX>
+__global__ void __launch_bounds__(kThreadsR, 1)
+    k_router(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
+             RouterParams p) {
+    using Cfg = RCfg<N>;
+    constexpr int S = Cfg::STAGES;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *base = reinterpret_cast<uint8_t *>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    uint8_t *sA = base;
+    uint8_t *sB = base + S * Cfg::A_BYTES;
+    uint64_t *full = reinterpret_cast<uint64_t *>(base + S * Cfg::STAGE);
+    uint64_t *empty = full + S;
+    uint64_t *tfull = empty + S;
+    uint64_t *tempty = tfull + 2;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp == 0 && lane == 0) {
+        ptx::tma_prefetch_desc(&tmX);
+        ptx::tma_prefetch_desc(&tmW);
+        for (int s = 0; s < S; ++s) {
+            ptx::mbar_init(&full[s], 1);
+            ptx::mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            ptx::mbar_init(&tfull[a], 1);
+            ptx::mbar_init(&tempty[a], 128);
+        }
+        ptx::fence_barrier_init();
+    }
+    if (warp == 2) ptx::tmem_alloc<Cfg::TMEM_COLS>(tmem_slot);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    const uint32_t nk = p.H / kBK;
+
+    if (warp == 0 && lane == 0) {
+        // ---------------- TMA producer ----------------
+        const uint64_t pol_x = ptx::policy_evict_first();
+        const uint64_t pol_w = ptx::policy_evict_last();
+        int stage = 0;
+        uint32_t phase = 0;
+        for (uint32_t tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+            const int32_t m0 = static_cast<int32_t>(tile * kBM);
+            for (uint32_t kb = 0; kb < nk; ++kb) {
+                ptx::mbar_wait(&empty[stage], phase ^ 1);
+                ptx::mbar_arrive_expect_tx(&full[stage], Cfg::STAGE);
+                ptx::tma_load_2d(&tmX, &full[stage], sA + stage * Cfg::A_BYTES, kb * kBK, m0,
+                                 pol_x);
+                ptx::tma_load_2d(&tmW, &full[stage], sB + stage * Cfg::B_BYTES, kb * kBK, 0,
+                                 pol_w);
+                if (++stage == S) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+        }
+    } else if (warp == 1 && lane == 0) {
+        // ---------------- MMA issuer ----------------
+        constexpr uint32_t idesc = ptx::idesc_bf16_f32<kBM, N>();
+        int stage = 0;
+        uint32_t phase = 0, acc = 0, aphase = 0;
+        for (uint32_t tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+            ptx::mbar_wait(&tempty[acc], aphase ^ 1);
+            ptx::tc_fence_after();
+            const uint32_t d = tmem_base + acc * N;
+            for (uint32_t kb = 0; kb < nk; ++kb) {
+                ptx::mbar_wait(&full[stage], phase);
+                ptx::tc_fence_after();
+                const uint64_t ad = ptx::sw128_kmajor_desc(ptx::smem_u32(sA + stage * Cfg::A_BYTES));
+                const uint64_t bd = ptx::sw128_kmajor_desc(ptx::smem_u32(sB + stage * Cfg::B_BYTES));
+#pragma unroll
+                for (int kk = 0; kk < kBK / 16; ++kk)  // +32 bytes along K per UMMA_K = 16
+                    ptx::mma_bf16(d, ad + 2 * kk, bd + 2 * kk, idesc, (kb | kk) != 0);
+                ptx::mma_commit(&empty[stage]);
+                if (++stage == S) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+            ptx::mma_commit(&tfull[acc]);
+            acc ^= 1;
+            if (acc == 0) aphase ^= 1;
+        }
+    } else if (warp >= 4) {
+        // ---------------- epilogue: one token row per thread ----------------
+        const uint32_t q = warp - 4;  // TMEM lanes [32q, 32q+32)
+        uint32_t acc = 0, aphase = 0;
+        for (uint32_t tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+            ptx::mbar_wait(&tfull[acc], aphase);
+            ptx::tc_fence_after();
+            const uint64_t row = static_cast<uint64_t>(tile) * kBM + q * 32 + lane;
+            const uint32_t taddr = tmem_base + acc * N + ((q * 32) << 16);
+            float tv[KMAX];
+            int ti[KMAX];
+#pragma unroll
+            for (int j = 0; j < KMAX; ++j) {
+                const bool sentinel = j < KMAX - static_cast<int>(p.k);
+                tv[j] = NAN;
+                ti[j] = sentinel ? -1 : 0x7FFFFFFF;
+            }
+            float m = -INFINITY;
+            float *lrow = (p.logits && row < p.T) ? p.logits + row * N : nullptr;
+#pragma unroll 1
+            for (int c = 0; c < N / 32; ++c) {
+                uint32_t r[32];
+                ptx::tmem_ld_32x32b_x32(taddr + c * 32, r);
+                ptx::tmem_ld_wait();
+                if (lrow) {
+                    float4 *dst = reinterpret_cast<float4 *>(lrow + c * 32);
+#pragma unroll
+                    for (int i = 0; i < 8; ++i)
+                        dst[i] = make_float4(__uint_as_float(r[4 * i]), __uint_as_float(r[4 * i + 1]),
+                                             __uint_as_float(r[4 * i + 2]),
+                                             __uint_as_float(r[4 * i + 3]));
+                }
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                    float v = __uint_as_float(r[i]);
+                    int e = c * 32 + i;
+                    if (!isnan(v)) m = fmaxf(m, v);
+                    if (sel_beats(v, e, tv[KMAX - 1], ti[KMAX - 1])) {
+#pragma unroll
+                        for (int j = 0; j < KMAX; ++j) {
+                            if (sel_beats(v, e, tv[j], ti[j])) {
+                                const float sv = tv[j];
+                                const int si = ti[j];
+                                tv[j] = v;
+                                ti[j] = e;
+                                v = sv;
+                                e = si;
+                            }
+                        }
+                    }
+                }
+            }
+            float ssum = 0.f;
+            if (p.score_fn == MPB_SCORE_SOFTMAX) {
+#pragma unroll 1
+                for (int c = 0; c < N / 32; ++c) {
+                    uint32_t r[32];
+                    ptx::tmem_ld_32x32b_x32(taddr + c * 32, r);
+                    ptx::tmem_ld_wait();
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) {
+                        const float v = __uint_as_float(r[i]);
+                        if (!isnan(v)) ssum += expf(v - m);
+                    }
+                }
+            }
+            // accumulator fully read: hand TMEM back to the MMA warp
+            ptx::tc_fence_before();
+            ptx::mbar_arrive(&tempty[acc]);
+            if (row < p.T) {
+                float w[KMAX];
+                float wsum = 0.f;
+#pragma unroll
+                for (int j = 0; j < KMAX; ++j) {
+                    const float v = tv[j];
+                    float x;
+                    if (isnan(v))
+                        x = 0.f;
+                    else if (p.score_fn == MPB_SCORE_SOFTMAX)
+                        x = expf(v - m) / ssum;
+                    else
+                        x = 1.f / (1.f + expf(-v));
+                    w[j] = x;
+                    if (j >= KMAX - static_cast<int>(p.k)) wsum += x;
+                }
+                const int off = KMAX - static_cast<int>(p.k);
+#pragma unroll
+                for (int j = 0; j < KMAX; ++j) {
+                    if (j < off) continue;
+                    const float x = p.renorm ? (wsum > 0.f ? w[j] / wsum : 0.f) : w[j];
+                    p.idx[row * p.k + (j - off)] = ti[j];
+                    p.w[row * p.k + (j - off)] = x;
+                }
+            }
+            acc ^= 1;
+            if (acc == 0) aphase ^= 1;
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc<Cfg::TMEM_COLS>(tmem_base);
+    }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        cudaDriverEntryPointQueryResult q;
+        void *ptr = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+    });
+    return fn;
+}
+
+bool make_map(CUtensorMap *map, const void *ptr, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+    auto fn = encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[2] = {cols, rows};
+    cuuint64_t strides[1] = {cols * 2};
+    cuuint32_t box[2] = {static_cast<cuuint32_t>(kBK), box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(ptr), dims,
+                    strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+template <int N, int KMAX>
+mpb_status launch_router_n(mpb_context *ctx, const CUtensorMap &mx, const CUtensorMap &mw,
+                           const RouterParams &p) {
+    constexpr int smem = RCfg<N>::SMEM;
+    auto kern = k_router<N, KMAX>;
+    MPB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    const uint32_t grid = std::min<uint32_t>(p.num_tiles, static_cast<uint32_t>(ctx->num_sms));
+    kern<<<grid, kThreadsR, smem, ctx->stream>>>(mx, mw, p);
+    MPB_LAUNCHED(ctx);
+    return MPB_OK;
+}
+
+template <int N>
+mpb_status launch_router_k(mpb_context *ctx, const CUtensorMap &mx, const CUtensorMap &mw,
+                           const RouterParams &p) {
+    if (p.k <= 1) return launch_router_n<N, 1>(ctx, mx, mw, p);
+    if (p.k <= 2) return launch_router_n<N, 2>(ctx, mx, mw, p);
+    if (p.k <= 4) return launch_router_n<N, 4>(ctx, mx, mw, p);
+    if (p.k <= 8) return launch_router_n<N, 8>(ctx, mx, mw, p);
+    return launch_router_n<N, 16>(ctx, mx, mw, p);
+}
+
+}  // namespace
+}  // namespace mpb
 
 using namespace mpb;
 
 extern "C" mpb_status mpb_router_topk(mpb_context *ctx, const void *X, const void *W, uint64_t T,
                                       uint32_t H, uint32_t E, uint32_t k, int score_fn, int renorm,
                                       int32_t *idx, float *weights, float *logits_out) {
-    (void)ctx; (void)X; (void)W; (void)T; (void)H; (void)E; (void)k; (void)score_fn;
-    (void)renorm; (void)idx; (void)weights; (void)logits_out;
-    return fail(MPB_ERROR, "mpb_router_topk: not built yet");
+    if (!ctx || (T && (!X || !W || !idx || !weights)))
+        return fail(MPB_VALIDATION_ERROR, "mpb_router_topk: NULL argument");
+    if (E != 64 && E != 128 && E != 256)
+        return fail(MPB_CONFIG_ERROR, "mpb_router_topk: E must be 64, 128 or 256");
+    if (H == 0 || H % kBK != 0) return fail(MPB_CONFIG_ERROR, "mpb_router_topk: H % 64 != 0");
+    if (k == 0 || k > 16 || k > E) return fail(MPB_CONFIG_ERROR, "mpb_router_topk: need 1 <= k <= 16");
+    if (score_fn != MPB_SCORE_SOFTMAX && score_fn != MPB_SCORE_SIGMOID)
+        return fail(MPB_CONFIG_ERROR, "mpb_router_topk: unknown score_fn");
+    if ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(W)) & 15)
+        return fail(MPB_CONFIG_ERROR, "mpb_router_topk: X and W must be 16-byte aligned");
+    if (T == 0) return MPB_OK;
+    if (T > 0x7fffffffull) return fail(MPB_CONFIG_ERROR, "mpb_router_topk: T too large");
+    CUtensorMap mx, mw;
+    const uint32_t box_n = E;
+    if (!make_map(&mx, X, T, H, kBM) || !make_map(&mw, W, E, H, box_n))
+        return fail(MPB_CUDA_ERROR, "mpb_router_topk: cuTensorMapEncodeTiled failed");
+    RouterParams p{T, H, k, score_fn, renorm, static_cast<uint32_t>((T + kBM - 1) / kBM),
+                   idx, weights, logits_out};
+    if (E == 64) return launch_router_k<64>(ctx, mx, mw, p);
+    if (E == 128) return launch_router_k<128>(ctx, mx, mw, p);
+    return launch_router_k<256>(ctx, mx, mw, p);
 }

@@ -1,0 +1,60 @@
+"""GPU parity of the tcgen05 router GEMM + fused top-k (K1).
+
+Logits (bf16 inputs, fp32 accumulate on tensor cores) vs a float64 CPU-free
+torch reference of the same bf16 inputs: |err| <= 1e-4 * sqrt(H) * rms(x) *
+rms(w) + 1e-5 (accumulation-order tolerance of an fp32 dot product of length
+H). Indices must equal the oracle's top-k on the SAME device logits
+(bit-exact, lowest-id tie rule); weights within 2e-6 relative."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from paper_2604_23150_b200 import moeplace as mp  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def eng():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return mp.Engine(0)
+
+
+CASES = [  # T, H, E, k, score_fn, renorm
+    (128, 64, 64, 2, 0, False), (1000, 512, 128, 8, 0, True), (4096, 4096, 128, 8, 0, False),
+    (2048, 7168, 256, 8, 1, True), (3001, 5120, 128, 1, 1, False), (257, 1024, 256, 16, 0, True),
+    (65536, 7168, 256, 8, 1, True)]
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_router_topk(eng, oracle, case):
+    T, H, E, k, fn, renorm = case
+    g = torch.Generator(device="cuda").manual_seed(T + H + E)
+    X = torch.randn(T, H, device="cuda", generator=g).to(torch.bfloat16)
+    W = (torch.randn(E, H, device="cuda", generator=g) / H ** 0.5).to(torch.bfloat16)
+    idx, w, logits = eng.router_topk(X, W, k, fn, renorm, want_logits=True)
+    torch.cuda.synchronize()
+    ref = X.double() @ W.double().t()
+    tol = 1e-4 * H ** 0.5 * float(X.float().pow(2).mean().sqrt()) * \
+        float(W.float().pow(2).mean().sqrt()) + 1e-5
+    err = (logits.double() - ref).abs().max().item()
+    assert err <= tol, (err, tol)
+    lg = logits.cpu().numpy()
+    sel = slice(None) if T <= 8192 else slice(0, 8192)
+    ri, rw = oracle.topk_logits(lg[sel], k, fn, renorm)
+    np.testing.assert_array_equal(idx.cpu().numpy()[sel], ri)
+    np.testing.assert_allclose(w.cpu().numpy()[sel], rw, rtol=2e-6, atol=1e-7)
+    # without materialising logits the routing is identical
+    idx2, w2 = eng.router_topk(X, W, k, fn, renorm)
+    assert torch.equal(idx2, idx) and torch.equal(w2, w)
+
+
+def test_router_ties_lowest_id(eng):
+    # identical expert rows -> identical logits -> lowest ids win
+    T, H, E, k = 256, 128, 64, 4
+    X = torch.randn(T, H, device="cuda").to(torch.bfloat16)
+    W = torch.randn(1, H, device="cuda").to(torch.bfloat16).repeat(E, 1)
+    idx, _ = eng.router_topk(X, W, k, 0, False)
+    torch.cuda.synchronize()
+    assert (idx.cpu() == torch.arange(k, dtype=torch.int32)).all()

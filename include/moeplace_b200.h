@@ -219,6 +219,47 @@ MPB_API mpb_status mpb_combine_scatter(mpb_context *ctx, const void *recv, const
                                        const float *weights, uint64_t T, uint32_t k, uint32_t H,
                                        void *Y);
 
+/* ---- host placement / grouping policies (no device needed) ----------------
+ * Restatements of the reference policies with the same std::mt19937_64 /
+ * libstdc++ distribution calls (bit-identical results):
+ *   placement.cpp:296-313 linear, :315-350 eplb (LPT), :127-161 phase 1,
+ *   :163-189 phase 2, :191-281 balance, :283-294 data_based, :96-125
+ *   aggregate_usage; clustering.cpp:28-35 l2_normalize_rows, :54-230 kmeans,
+ *   :232-320 cluster sizes + assign_clusters_to_groups.
+ * Groups are returned flattened (group d's experts follow group d-1's); fixed
+ * size M per group unless a sizes array is returned. Matrices are row-major
+ * double. */
+MPB_API mpb_status mpb_linear_placement(uint32_t E, uint32_t D, uint32_t *groups_out /* E */);
+MPB_API mpb_status mpb_eplb_placement(const double *load /* E */, uint32_t E, uint32_t D,
+                                      uint32_t *groups_out /* E */);
+MPB_API mpb_status mpb_phase1_unique_distribution(const double *usage /* D*E */, uint32_t D,
+                                                  uint32_t E, uint32_t *groups_out /* E */,
+                                                  uint32_t *sizes_out /* D */);
+MPB_API mpb_status mpb_phase2_redundant_addition(const uint32_t *groups_in, const uint32_t *sizes_in,
+                                                 const double *usage, uint32_t D, uint32_t E,
+                                                 uint32_t M, uint32_t *groups_out /* D*M */);
+MPB_API mpb_status mpb_balance_and_verify(const uint32_t *groups_in, const uint32_t *sizes_in,
+                                          uint32_t D, uint32_t E, uint32_t M, uint64_t seed,
+                                          uint32_t *groups_out /* D*M */);
+MPB_API mpb_status mpb_data_based_placement(const double *usage /* D*E */, uint32_t D, uint32_t E,
+                                            uint32_t R, uint64_t seed,
+                                            uint32_t *groups_out /* E+R */);
+MPB_API mpb_status mpb_aggregate_usage(const uint32_t *labels /* rows */, const double *matrix,
+                                       uint64_t rows, uint32_t E, uint32_t K,
+                                       const uint32_t *assign_flat, const uint32_t *assign_sizes,
+                                       uint32_t D, double *usage_out /* D*E */);
+MPB_API mpb_status mpb_l2_normalize_rows(const double *matrix, uint64_t rows, uint32_t cols,
+                                         double *out);
+MPB_API mpb_status mpb_kmeans(const double *rows, uint64_t n, uint32_t dim, uint32_t K,
+                              uint64_t seed, uint32_t max_iterations, double tolerance,
+                              uint32_t *labels_out /* n */, double *centroids_out /* K*dim */,
+                              double *objective_out, uint32_t *iterations_out);
+MPB_API mpb_status mpb_assign_clusters_to_groups(const uint32_t *labels, uint64_t n, uint32_t K,
+                                                 const double *raw, uint32_t dim, uint32_t D,
+                                                 uint64_t seed, uint32_t *assign_flat /* <= K*D */,
+                                                 uint32_t *assign_sizes /* K */,
+                                                 double *cluster_sizes_out /* K */);
+
 #ifdef __cplusplus
 }
 #endif

@@ -334,7 +334,14 @@ int ref_compare_scenario(const char *config_json_path, const char *trace_out,
 
         json j;
         j["decode_matrix"] = matrix_json(decode);
-        j["cluster_matrix_request_ids"] = stage.matrix.request_ids;
+        j["cluster_matrix"] = matrix_json(stage.matrix);
+        j["cluster_K"] = stage.model.K;
+        j["cluster_objective"] = stage.model.objective;
+        j["clustering"] = {{"seed", cfg.clustering.seed},
+                           {"restarts", cfg.clustering.restarts},
+                           {"max_iterations", cfg.clustering.max_iterations},
+                           {"tolerance", cfg.clustering.tolerance}};
+        j["placement_cfg"] = {{"seed", cfg.placement.seed}, {"R", cfg.placement.R_redundancy}};
         j["cluster_labels"] = stage.model.labels;
         j["group_map"] = stage.group_map.assignment;
         json strat = json::array();

@@ -60,6 +60,22 @@ _SIGS = {
                                           C.c_uint32, C.c_int, _p, _p]),
     "mpb_dispatch_gather": (C.c_int, [_p, _p, _p, C.c_uint64, C.c_uint32, C.c_uint32, _p]),
     "mpb_combine_scatter": (C.c_int, [_p, _p, _p, _p, C.c_uint64, C.c_uint32, C.c_uint32, _p]),
+    "mpb_linear_placement": (C.c_int, [C.c_uint32, C.c_uint32, _p]),
+    "mpb_eplb_placement": (C.c_int, [_p, C.c_uint32, C.c_uint32, _p]),
+    "mpb_phase1_unique_distribution": (C.c_int, [_p, C.c_uint32, C.c_uint32, _p, _p]),
+    "mpb_phase2_redundant_addition": (C.c_int, [_p, _p, _p, C.c_uint32, C.c_uint32, C.c_uint32,
+                                                _p]),
+    "mpb_balance_and_verify": (C.c_int, [_p, _p, C.c_uint32, C.c_uint32, C.c_uint32,
+                                         C.c_uint64, _p]),
+    "mpb_data_based_placement": (C.c_int, [_p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64,
+                                           _p]),
+    "mpb_aggregate_usage": (C.c_int, [_p, _p, C.c_uint64, C.c_uint32, C.c_uint32, _p, _p,
+                                      C.c_uint32, _p]),
+    "mpb_l2_normalize_rows": (C.c_int, [_p, C.c_uint64, C.c_uint32, _p]),
+    "mpb_kmeans": (C.c_int, [_p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint32,
+                             C.c_double, _p, _p, _p, _p]),
+    "mpb_assign_clusters_to_groups": (C.c_int, [_p, C.c_uint64, C.c_uint32, _p, C.c_uint32,
+                                                C.c_uint32, C.c_uint64, _p, _p, _p]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -25,8 +25,13 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hid
          "--expt-relaxed-constexpr", f"-I{ROOT / 'include'}", f"-I{CSRC}"]
 
 
+CXX = os.environ.get("CXX", "g++")
+CXXFLAGS = ["-std=c++17", "-O3", "-fPIC", "-fvisibility=hidden", "-ffp-contract=off",
+            f"-I{ROOT / 'include'}", f"-I{CSRC}", "-I/usr/local/cuda/include"]
+
+
 def sources():
-    return sorted(CSRC.glob("*.cu"))
+    return sorted(CSRC.glob("*.cu")) + sorted(CSRC.glob("*.cpp"))
 
 
 def _compile(src: Path, verbose_ptxas: bool) -> Path:
@@ -34,13 +39,16 @@ def _compile(src: Path, verbose_ptxas: bool) -> Path:
     deps = [src, *CSRC.glob("*.cuh"), ROOT / "include" / "moeplace_b200.h"]
     if obj.exists() and obj.stat().st_mtime >= max(d.stat().st_mtime for d in deps):
         return obj
-    cmd = [NVCC, *ARCH, *FLAGS, "-c", str(src), "-o", str(obj)]
-    if verbose_ptxas:
+    if src.suffix == ".cpp":
+        cmd = [CXX, *CXXFLAGS, "-c", str(src), "-o", str(obj)]
+    else:
+        cmd = [NVCC, *ARCH, *FLAGS, "-c", str(src), "-o", str(obj)]
+    if verbose_ptxas and src.suffix == ".cu":
         cmd += ["-Xptxas", "-v"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src.name}:\n{r.stderr}")
-    if verbose_ptxas:
+    if verbose_ptxas and src.suffix == ".cu":
         sys.stderr.write(r.stderr)
     return obj
 

@@ -121,7 +121,8 @@ MPB_API mpb_status mpb_topk_logits(mpb_context *ctx, const float *logits, uint64
  * Outputs (device, ACCUMULATED with += so shards/layers can be fused; the
  * caller zeroes them):
  *   demand[D*E]       pairs per (source group, expert)        (uint64)
- *   tag_pop[n_tags*E] pairs per (tag[t], expert) if tag != NULL (uint64):
+ *   tag_pop[n_tags*E] pairs per (tag[t], expert) if tag != NULL (uint64; tag[t]
+ *                     uint16, tags >= n_tags are ignored):
  *                     per-domain popularity / per-stage vectors
  * Permutation (optional, all three or none; device):
  *   sorted_pairs[T*k] pairs ordered by (dest group, expert id, p) — stable
@@ -134,7 +135,7 @@ typedef struct {
     const uint8_t *src_group;
     uint32_t src_base;
     uint32_t src_span;
-    const uint8_t *tag;
+    const uint16_t *tag;
     uint32_t n_tags;
 } mpb_tokens;
 
@@ -188,10 +189,14 @@ MPB_API mpb_status mpb_route_sources(mpb_context *ctx, const uint32_t *rows, con
                                      const uint32_t *groups, uint32_t D, int cluster_routed,
                                      uint8_t *src);
 
-/* node_demand[B][nodes][E] (uint64) x luts[P][nodes][E] (uint8, 255 =
- * uncovered) -> inter[P*B], intra[P*B], rank_pairs[P*B*D] pair counts
- * (device). group_to_node[D] device uint8. */
-MPB_API mpb_status mpb_score_placements(mpb_context *ctx, const uint64_t *node_demand, uint32_t B,
+/* demand[B][rows][E] (uint64) x luts[P][nodes][E] (uint8, 255 = uncovered)
+ * -> inter[P*B], intra[P*B], rank_pairs[P*B*D] pair counts (device). Row r
+ * of a demand table originates on node row_node[r] (device uint8 [rows]):
+ * rows = nodes with row_node = identity for node-level demand, or rows = D
+ * with row_node = group_to_node for the per-source-group demand of
+ * mpb_dispatch_layout. group_to_node[D] device uint8. */
+MPB_API mpb_status mpb_score_placements(mpb_context *ctx, const uint64_t *demand, uint32_t B,
+                                        uint32_t rows, const uint8_t *row_node,
                                         const uint8_t *luts, uint32_t P,
                                         const uint8_t *group_to_node, uint32_t D, uint32_t nodes,
                                         uint32_t E, uint64_t *inter, uint64_t *intra,

@@ -54,8 +54,8 @@ _SIGS = {
                                     C.c_int, _p]),
     "mpb_batch_demand": (C.c_int, [_p, _p, _p, _p, C.c_uint32, _p, _p, C.c_uint32, C.c_uint32,
                                    _p, C.c_uint32, C.c_uint32, C.c_uint32, _p]),
-    "mpb_score_placements": (C.c_int, [_p, _p, C.c_uint32, _p, C.c_uint32, _p, C.c_uint32,
-                                       C.c_uint32, C.c_uint32, _p, _p, _p]),
+    "mpb_score_placements": (C.c_int, [_p, _p, C.c_uint32, C.c_uint32, _p, _p, C.c_uint32, _p,
+                                       C.c_uint32, C.c_uint32, C.c_uint32, _p, _p, _p]),
     "mpb_finalize_layer_sims": (C.c_int, [_p, _p, _p, _p, C.c_uint64, C.c_uint32, _f64p,
                                           C.c_uint32, C.c_int, _p, _p]),
     "mpb_dispatch_gather": (C.c_int, [_p, _p, _p, C.c_uint64, C.c_uint32, C.c_uint32, _p]),

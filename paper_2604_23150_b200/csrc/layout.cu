@@ -36,7 +36,7 @@ struct LayoutParams {
     uint32_t k;
     const uint8_t *src_group;
     uint32_t src_base, src_span;
-    const uint8_t *tag;
+    const uint16_t *tag;
     uint32_t n_tags;
     const uint8_t *g2n;
     const uint16_t *slot_lut;

@@ -41,9 +41,10 @@ struct RCfg {
     static constexpr int A_BYTES = kBM * kBK * 2;
     static constexpr int B_BYTES = N * kBK * 2;
     static constexpr int STAGE = A_BYTES + B_BYTES;
-    static constexpr int STAGES = (200 * 1024) / STAGE > 8 ? 8 : (200 * 1024) / STAGE;
+    static constexpr int STAGES = (196 * 1024) / STAGE > 8 ? 8 : (196 * 1024) / STAGE;
     static constexpr uint32_t TMEM_COLS = 2 * N < 32 ? 32 : 2 * N;
-    static constexpr int SMEM = 1024 + STAGES * STAGE + (2 * STAGES + 4) * 8 + 16;
+    static constexpr int PARK = 128 * 17 * 4;  // epilogue park rows (stride 17: no bank conflicts)
+    static constexpr int SMEM = 1024 + STAGES * STAGE + PARK + (2 * STAGES + 4) * 8 + 16;
 };
 
 struct RouterParams {
@@ -79,7 +80,8 @@ __global__ void __launch_bounds__(kThreadsR, 1)
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
     uint8_t *sA = base;
     uint8_t *sB = base + S * Cfg::A_BYTES;
-    uint64_t *full = reinterpret_cast<uint64_t *>(base + S * Cfg::STAGE);
+    float *s_park = reinterpret_cast<float *>(base + S * Cfg::STAGE);
+    uint64_t *full = reinterpret_cast<uint64_t *>(base + S * Cfg::STAGE + Cfg::PARK);
     uint64_t *empty = full + S;
     uint64_t *tfull = empty + S;
     uint64_t *tempty = tfull + 2;
@@ -156,8 +158,16 @@ __global__ void __launch_bounds__(kThreadsR, 1)
         }
     } else if (warp >= 4) {
         // ---------------- epilogue: one token row per thread ----------------
+        // Columns are scanned in ascending expert id, so a new value can only
+        // displace a kept entry by being strictly larger (equal logits keep the
+        // lower id). The per-column test is a single compare against the current
+        // k-th value; the rare insertions run one shared copy of a (value, id)
+        // bubble network over values parked in shared memory. NaN logits are
+        // only used to fill slots left empty by the non-NaN values.
         const uint32_t q = warp - 4;  // TMEM lanes [32q, 32q+32)
+        float *park = s_park + (q * 32 + lane) * 17;
         uint32_t acc = 0, aphase = 0;
+        const int off = KMAX - static_cast<int>(p.k);
         for (uint32_t tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
             ptx::mbar_wait(&tfull[acc], aphase);
             ptx::tc_fence_after();
@@ -167,56 +177,90 @@ __global__ void __launch_bounds__(kThreadsR, 1)
             int ti[KMAX];
 #pragma unroll
             for (int j = 0; j < KMAX; ++j) {
-                const bool sentinel = j < KMAX - static_cast<int>(p.k);
-                tv[j] = NAN;
-                ti[j] = sentinel ? -1 : 0x7FFFFFFF;
+                tv[j] = j < off ? INFINITY : NAN;  // sentinels above, empty slots below
+                ti[j] = j < off ? -1 : 0x7FFFFFFF;
             }
             float m = -INFINITY;
+            uint32_t nans = 0;
             float *lrow = (p.logits && row < p.T) ? p.logits + row * N : nullptr;
 #pragma unroll 1
-            for (int c = 0; c < N / 32; ++c) {
-                uint32_t r[32];
-                ptx::tmem_ld_32x32b_x32(taddr + c * 32, r);
+            for (int c = 0; c < N / 16; ++c) {
+                uint32_t r[16];
+                ptx::tmem_ld_32x32b_x16(taddr + c * 16, r);
                 ptx::tmem_ld_wait();
                 if (lrow) {
-                    float4 *dst = reinterpret_cast<float4 *>(lrow + c * 32);
+                    float4 *dst = reinterpret_cast<float4 *>(lrow + c * 16);
 #pragma unroll
-                    for (int i = 0; i < 8; ++i)
+                    for (int i = 0; i < 4; ++i)
                         dst[i] = make_float4(__uint_as_float(r[4 * i]), __uint_as_float(r[4 * i + 1]),
                                              __uint_as_float(r[4 * i + 2]),
                                              __uint_as_float(r[4 * i + 3]));
                 }
+                const float thr = tv[KMAX - 1];
+                const bool thr_empty = isnan(thr);
+                uint32_t hit = 0;
 #pragma unroll
-                for (int i = 0; i < 32; ++i) {
-                    float v = __uint_as_float(r[i]);
-                    int e = c * 32 + i;
-                    if (!isnan(v)) m = fmaxf(m, v);
-                    if (sel_beats(v, e, tv[KMAX - 1], ti[KMAX - 1])) {
+                for (int i = 0; i < 16; ++i) {
+                    const float v = __uint_as_float(r[i]);
+                    m = fmaxf(m, v);
+                    nans += v != v;
+                    hit |= static_cast<uint32_t>(v > thr || (thr_empty && v == v)) << i;
+                }
+                if (hit) {
 #pragma unroll
-                        for (int j = 0; j < KMAX; ++j) {
-                            if (sel_beats(v, e, tv[j], ti[j])) {
+                    for (int i = 0; i < 16; ++i) park[i] = __uint_as_float(r[i]);
+                    while (hit) {
+                        const int i = __ffs(hit) - 1;
+                        hit &= hit - 1;
+                        float cv = park[i];
+                        int ci = c * 16 + i;
+#pragma unroll
+                        for (int j = 0; j < KMAX; ++j) {  // sentinels (id < 0) never move
+                            if (sel_beats(cv, ci, tv[j], ti[j])) {
                                 const float sv = tv[j];
                                 const int si = ti[j];
-                                tv[j] = v;
-                                ti[j] = e;
-                                v = sv;
-                                e = si;
+                                tv[j] = cv;
+                                ti[j] = ci;
+                                cv = sv;
+                                ci = si;
                             }
                         }
                     }
                 }
             }
-            float ssum = 0.f;
-            if (p.score_fn == MPB_SCORE_SOFTMAX) {
+            if (nans && ti[KMAX - 1] == 0x7FFFFFFF) {
+                // rare: fewer than k non-NaN logits — fill with NaN ids ascending
 #pragma unroll 1
-                for (int c = 0; c < N / 32; ++c) {
-                    uint32_t r[32];
-                    ptx::tmem_ld_32x32b_x32(taddr + c * 32, r);
+                for (int c = 0; c < N / 16; ++c) {
+                    uint32_t r[16];
+                    ptx::tmem_ld_32x32b_x16(taddr + c * 16, r);
                     ptx::tmem_ld_wait();
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) {
+                    for (int i = 0; i < 16; ++i) {
+                        if (!isnan(__uint_as_float(r[i]))) continue;
+                        bool placed = false;
+#pragma unroll
+                        for (int j = 0; j < KMAX; ++j)
+                            if (!placed && ti[j] == 0x7FFFFFFF) {
+                                ti[j] = c * 16 + i;
+                                tv[j] = NAN;
+                                placed = true;
+                            }
+                    }
+                }
+            }
+            float ssum = 0.f;
+            const float mlog = m * 1.4426950408889634f;
+            if (p.score_fn == MPB_SCORE_SOFTMAX) {
+#pragma unroll 1
+                for (int c = 0; c < N / 16; ++c) {
+                    uint32_t r[16];
+                    ptx::tmem_ld_32x32b_x16(taddr + c * 16, r);
+                    ptx::tmem_ld_wait();
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
                         const float v = __uint_as_float(r[i]);
-                        if (!isnan(v)) ssum += expf(v - m);
+                        ssum += v == v ? exp2f(fmaf(v, 1.4426950408889634f, -mlog)) : 0.f;
                     }
                 }
             }
@@ -230,16 +274,15 @@ __global__ void __launch_bounds__(kThreadsR, 1)
                 for (int j = 0; j < KMAX; ++j) {
                     const float v = tv[j];
                     float x;
-                    if (isnan(v))
+                    if (j < off || isnan(v))
                         x = 0.f;
                     else if (p.score_fn == MPB_SCORE_SOFTMAX)
-                        x = expf(v - m) / ssum;
+                        x = exp2f(fmaf(v, 1.4426950408889634f, -mlog)) / ssum;
                     else
                         x = 1.f / (1.f + expf(-v));
                     w[j] = x;
-                    if (j >= KMAX - static_cast<int>(p.k)) wsum += x;
+                    wsum += x;
                 }
-                const int off = KMAX - static_cast<int>(p.k);
 #pragma unroll
                 for (int j = 0; j < KMAX; ++j) {
                     if (j < off) continue;

@@ -66,7 +66,9 @@ __global__ void __launch_bounds__(256) k_batch_demand(const uint32_t *row_ptr, c
 
 constexpr int kScoreWarps = 8;
 
-__global__ void __launch_bounds__(kScoreWarps * 32) k_score(const uint64_t *node_demand, uint32_t B,
+__global__ void __launch_bounds__(kScoreWarps * 32) k_score(const uint64_t *demand, uint32_t B,
+                                                            uint32_t rows,
+                                                            const uint8_t *row_node_g,
                                                             const uint8_t *luts,
                                                             const uint8_t *g2n_g, uint32_t D,
                                                             uint32_t nodes, uint32_t E,
@@ -75,31 +77,35 @@ __global__ void __launch_bounds__(kScoreWarps * 32) k_score(const uint64_t *node
                                                             uint64_t *rank_out, uint32_t *err) {
     extern __shared__ unsigned char s_raw[];
     const uint32_t NE = nodes * E;
+    const uint32_t RE = rows * E;
     unsigned long long *s_rank = reinterpret_cast<unsigned long long *>(s_raw);  // [warps][D]
     uint8_t *s_lut = s_raw + kScoreWarps * D * 8;
     uint8_t *s_g2n = s_lut + NE;
+    uint8_t *s_rn = s_g2n + D;
     const uint32_t p = blockIdx.x;
     const uint8_t *lut = luts + static_cast<size_t>(p) * NE;
     for (uint32_t i = threadIdx.x; i < NE; i += blockDim.x) s_lut[i] = lut[i];
     for (uint32_t i = threadIdx.x; i < D; i += blockDim.x) s_g2n[i] = g2n_g[i];
+    for (uint32_t i = threadIdx.x; i < rows; i += blockDim.x) s_rn[i] = row_node_g[i];
     __syncthreads();
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     unsigned long long *rank = s_rank + warp * D;
     for (uint32_t b = blockIdx.y * kScoreWarps + warp; b < B; b += gridDim.y * kScoreWarps) {
         for (uint32_t d = lane; d < D; d += 32) rank[d] = 0;
         __syncwarp();
-        const uint64_t *a = node_demand + static_cast<size_t>(b) * NE;
+        const uint64_t *a = demand + static_cast<size_t>(b) * RE;
         unsigned long long inter = 0, intra = 0;
-        for (uint32_t i = lane; i < NE; i += 32) {
+        for (uint32_t i = lane; i < RE; i += 32) {
             const unsigned long long v = a[i];
             if (!v) continue;
-            const uint32_t d = s_lut[i];
+            const uint32_t n = s_rn[i / E];
+            const uint32_t d = s_lut[n * E + i % E];
             if (d == 255) {
                 atomicOr(err, kErrUncovered);
                 continue;
             }
             atomicAdd(rank + d, v);
-            if (s_g2n[d] == i / E)
+            if (s_g2n[d] == n)
                 intra += v;
             else
                 inter += v;
@@ -180,16 +186,18 @@ mpb_status mpb_batch_demand(mpb_context *ctx, const uint32_t *row_ptr, const uin
     return MPB_OK;
 }
 
-mpb_status mpb_score_placements(mpb_context *ctx, const uint64_t *node_demand, uint32_t B,
-                                const uint8_t *luts, uint32_t P, const uint8_t *group_to_node,
-                                uint32_t D, uint32_t nodes, uint32_t E, uint64_t *inter,
-                                uint64_t *intra, uint64_t *rank_pairs) {
-    if (!ctx || !node_demand || !luts || !group_to_node || !inter || !intra || !rank_pairs)
+mpb_status mpb_score_placements(mpb_context *ctx, const uint64_t *demand, uint32_t B,
+                                uint32_t rows, const uint8_t *row_node, const uint8_t *luts,
+                                uint32_t P, const uint8_t *group_to_node, uint32_t D,
+                                uint32_t nodes, uint32_t E, uint64_t *inter, uint64_t *intra,
+                                uint64_t *rank_pairs) {
+    if (!ctx || !demand || !row_node || !luts || !group_to_node || !inter || !intra || !rank_pairs)
         return fail(MPB_VALIDATION_ERROR, "mpb_score_placements: NULL argument");
+    if (rows == 0 || rows > 255) return fail(MPB_CONFIG_ERROR, "mpb_score_placements: need 1 <= rows <= 255");
     if (D == 0 || D > 255 || nodes == 0)
         return fail(MPB_CONFIG_ERROR, "mpb_score_placements: need 1 <= D <= 255, nodes >= 1");
     if (P == 0 || B == 0) return MPB_OK;
-    const size_t smem = size_t(kScoreWarps) * D * 8 + size_t(nodes) * E + D;
+    const size_t smem = size_t(kScoreWarps) * D * 8 + size_t(nodes) * E + D + rows;
     if (smem > 200 * 1024) return fail(MPB_CONFIG_ERROR, "mpb_score_placements: nodes*E too large");
     MPB_CUDA(cudaFuncSetAttribute(k_score, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     // enough CTAs to fill the machine: split batches across grid.y when P is small
@@ -198,9 +206,9 @@ mpb_status mpb_score_placements(mpb_context *ctx, const uint64_t *node_demand, u
     if (static_cast<uint64_t>(P) * gy > want) gy = std::max(1u, want / std::max(1u, P));
     gy = std::min(gy, 65535u);
     dim3 grid(P, gy);
-    k_score<<<grid, kScoreWarps * 32, smem, ctx->stream>>>(node_demand, B, luts, group_to_node, D,
-                                                           nodes, E, inter, intra, rank_pairs,
-                                                           ctx->d_error);
+    k_score<<<grid, kScoreWarps * 32, smem, ctx->stream>>>(demand, B, rows, row_node, luts,
+                                                           group_to_node, D, nodes, E, inter,
+                                                           intra, rank_pairs, ctx->d_error);
     MPB_LAUNCHED(ctx);
     return MPB_OK;
 }

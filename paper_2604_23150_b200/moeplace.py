@@ -388,15 +388,19 @@ class Engine:
         return out
 
     # --- scoring --------------------------------------------------------
-    def score_placements(self, node_demand: torch.Tensor, luts: torch.Tensor, g2n: torch.Tensor,
-                         D: int, out=None):
-        B, nodes, E = node_demand.shape
-        P = luts.shape[0]
+    def score_placements(self, demand: torch.Tensor, luts: torch.Tensor, g2n: torch.Tensor,
+                         D: int, row_node: Optional[torch.Tensor] = None, out=None):
+        """demand [B, rows, E]; rows are nodes (row_node=None) or source groups
+        (row_node = group_to_node)."""
+        B, rows, E = demand.shape
+        P, nodes, _ = luts.shape
+        if row_node is None:
+            row_node = torch.arange(rows, dtype=torch.uint8, device=self.device)
         if out is None:
             out = (self._u64(P, B), self._u64(P, B), self._u64(P, B, D))
         inter, intra, rank = out
-        _abi.call("mpb_score_placements", self.ctx, _ptr(node_demand), B, _ptr(luts), P,
-                  _ptr(g2n), D, nodes, E, _ptr(inter), _ptr(intra), _ptr(rank))
+        _abi.call("mpb_score_placements", self.ctx, _ptr(demand), B, rows, _ptr(row_node),
+                  _ptr(luts), P, _ptr(g2n), D, nodes, E, _ptr(inter), _ptr(intra), _ptr(rank))
         return inter, intra, rank
 
     def finalize(self, inter, intra, rank, D: int, cost: CostModelParams, topology: Topology,

@@ -188,7 +188,7 @@ def test_dispatch_layout_bit_exact(eng, oracle, case):
         rng.integers(0, D, T).astype(np.uint8)
     pl = make_placement(rng, E, D, red)
     top = topo(D, nodes)
-    tag = rng.integers(0, 5, T).astype(np.uint8)
+    tag = rng.integers(0, 5, T).astype(np.uint16)
     dp = eng.placement(pl, top)
     kw = dict(src_base=0, src_span=D) if block_src else dict(src=dev(src))
     lay = eng.dispatch_layout(dev(idx), dp, tag=dev(tag), n_tags=5, **kw)

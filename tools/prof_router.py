@@ -1,0 +1,48 @@
+"""Runs the router GEMM + top-k alone for profiling (ncu / timing)."""
+import argparse
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import torch  # noqa: E402
+
+from paper_2604_23150_b200 import moeplace as mp  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--T", type=int, default=65536)
+ap.add_argument("--H", type=int, default=7168)
+ap.add_argument("--E", type=int, default=256)
+ap.add_argument("--k", type=int, default=8)
+ap.add_argument("--fn", type=int, default=1)
+ap.add_argument("--iters", type=int, default=5)
+a = ap.parse_args()
+eng = mp.Engine(0)
+X = torch.randn(a.T, a.H, device="cuda").to(torch.bfloat16)
+W = (torch.randn(a.E, a.H, device="cuda") / a.H ** 0.5).to(torch.bfloat16)
+out = (torch.empty(a.T, a.k, dtype=torch.int32, device="cuda"),
+       torch.empty(a.T, a.k, dtype=torch.float32, device="cuda"))
+for _ in range(2):
+    eng.router_topk(X, W, a.k, a.fn, True, out=out)
+torch.cuda.synchronize()
+s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+s.record()
+for _ in range(a.iters):
+    eng.router_topk(X, W, a.k, a.fn, True, out=out)
+e.record()
+torch.cuda.synchronize()
+ms = s.elapsed_time(e) / a.iters
+tf = 2 * a.T * a.H * a.E / ms / 1e9
+print(f"router T={a.T} H={a.H} E={a.E} k={a.k}: {ms:.4f} ms  {tf:.1f} TFLOP/s  "
+      f"{(a.T * a.H * 2) / ms / 1e6:.0f} GB/s(X)")
+# cuBLAS reference point for the same GEMM (library baseline, not on the path)
+C = torch.empty(a.T, a.E, device="cuda", dtype=torch.bfloat16)
+for _ in range(2):
+    torch.matmul(X, W.t(), out=C)
+torch.cuda.synchronize()
+s.record()
+for _ in range(a.iters):
+    torch.matmul(X, W.t(), out=C)
+e.record()
+torch.cuda.synchronize()
+ms2 = s.elapsed_time(e) / a.iters
+print(f"cublas bf16 GEMM same shape: {ms2:.4f} ms  {2 * a.T * a.H * a.E / ms2 / 1e9:.1f} TFLOP/s")

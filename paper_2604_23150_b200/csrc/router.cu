@@ -34,16 +34,20 @@ namespace {
 
 constexpr int kBM = 128;
 constexpr int kBK = 64;  // 64 bf16 = 128 bytes: one 128B swizzle atom per row
-constexpr int kThreadsR = 256;
+constexpr int kThreadsR = 384;  // 4 non-epilogue + 8 epilogue warps
 
-template <int N>
+template <int N, int KMAX>
 struct RCfg {
     static constexpr int A_BYTES = kBM * kBK * 2;
     static constexpr int B_BYTES = N * kBK * 2;
     static constexpr int STAGE = A_BYTES + B_BYTES;
-    static constexpr int STAGES = (196 * 1024) / STAGE > 8 ? 8 : (196 * 1024) / STAGE;
     static constexpr uint32_t TMEM_COLS = 2 * N < 32 ? 32 : 2 * N;
-    static constexpr int PARK = 128 * 17 * 4;  // epilogue park rows (stride 17: no bank conflicts)
+    // per epilogue thread: 16 parked logits, later its half's top-k (values,
+    // ids) + max + sum for the merge; odd stride keeps banks conflict-free
+    static constexpr int PARK_ROW = (2 * KMAX + 2 > 16 ? 2 * KMAX + 2 : 16) | 1;
+    static constexpr int PARK = 256 * PARK_ROW * 4;
+    static constexpr int BUDGET = 232448 - 1024 - PARK - 256;
+    static constexpr int STAGES = BUDGET / STAGE > 8 ? 8 : BUDGET / STAGE;
     static constexpr int SMEM = 1024 + STAGES * STAGE + PARK + (2 * STAGES + 4) * 8 + 16;
 };
 
@@ -73,7 +77,7 @@ template <int N, int KMAX>
 __global__ void __launch_bounds__(kThreadsR, 1)
     k_router(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
              RouterParams p) {
-    using Cfg = RCfg<N>;
+    using Cfg = RCfg<N, KMAX>;
     constexpr int S = Cfg::STAGES;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *base = reinterpret_cast<uint8_t *>(
@@ -97,7 +101,7 @@ __global__ void __launch_bounds__(kThreadsR, 1)
         }
         for (int a = 0; a < 2; ++a) {
             ptx::mbar_init(&tfull[a], 1);
-            ptx::mbar_init(&tempty[a], 128);
+            ptx::mbar_init(&tempty[a], 256);
         }
         ptx::fence_barrier_init();
     }
@@ -157,39 +161,45 @@ __global__ void __launch_bounds__(kThreadsR, 1)
             if (acc == 0) aphase ^= 1;
         }
     } else if (warp >= 4) {
-        // ---------------- epilogue: one token row per thread ----------------
-        // Columns are scanned in ascending expert id, so a new value can only
-        // displace a kept entry by being strictly larger (equal logits keep the
-        // lower id). The per-column test is a single compare against the current
-        // k-th value; the rare insertions run one shared copy of a (value, id)
-        // bubble network over values parked in shared memory. NaN logits are
-        // only used to fill slots left empty by the non-NaN values.
-        const uint32_t q = warp - 4;  // TMEM lanes [32q, 32q+32)
-        float *park = s_park + (q * 32 + lane) * 17;
-        uint32_t acc = 0, aphase = 0;
+        // ---------------- epilogue: one token row per thread pair ----------------
+        // Warp w reads TMEM lanes [32q, 32q+32), q = w % 4; warps 4-7 take
+        // expert columns [0, N/2) and warps 8-11 [N/2, N) of the same rows, so
+        // two warps per SM sub-partition hide each other's latency.
+        // Columns are scanned in ascending expert id: a new value displaces a
+        // kept entry only if strictly larger (equal logits keep the lower id),
+        // so the per-column test is one compare against the current k-th
+        // value, and an insertion is a branch-free shift of a sorted register
+        // list (values parked in smem so one copy of the network serves all
+        // columns). The column-half lists merge through smem (half 1's ids are
+        // all larger). NaN / -inf logits only fill slots the others leave empty.
+        const uint32_t q = warp & 3, half = (warp - 4) >> 2;
+        const uint32_t row_in_tile = q * 32 + lane;
+        float *park = s_park + ((half * 128) + row_in_tile) * Cfg::PARK_ROW;
+        float *peer = s_park + (128 + row_in_tile) * Cfg::PARK_ROW;
+        constexpr int NH = N / 2;
         const int off = KMAX - static_cast<int>(p.k);
+        uint32_t acc = 0, aphase = 0;
         for (uint32_t tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
             ptx::mbar_wait(&tfull[acc], aphase);
             ptx::tc_fence_after();
-            const uint64_t row = static_cast<uint64_t>(tile) * kBM + q * 32 + lane;
+            const uint64_t row = static_cast<uint64_t>(tile) * kBM + row_in_tile;
             const uint32_t taddr = tmem_base + acc * N + ((q * 32) << 16);
             float tv[KMAX];
             int ti[KMAX];
 #pragma unroll
             for (int j = 0; j < KMAX; ++j) {
-                tv[j] = j < off ? INFINITY : NAN;  // sentinels above, empty slots below
+                tv[j] = j < off ? INFINITY : -INFINITY;  // sentinels above, empty slots below
                 ti[j] = j < off ? -1 : 0x7FFFFFFF;
             }
             float m = -INFINITY;
-            uint32_t nans = 0;
             float *lrow = (p.logits && row < p.T) ? p.logits + row * N : nullptr;
 #pragma unroll 1
-            for (int c = 0; c < N / 16; ++c) {
+            for (int c = half * NH; c < (half + 1) * NH; c += 16) {
                 uint32_t r[16];
-                ptx::tmem_ld_32x32b_x16(taddr + c * 16, r);
+                ptx::tmem_ld_32x32b_x16(taddr + c, r);
                 ptx::tmem_ld_wait();
                 if (lrow) {
-                    float4 *dst = reinterpret_cast<float4 *>(lrow + c * 16);
+                    float4 *dst = reinterpret_cast<float4 *>(lrow + c);
 #pragma unroll
                     for (int i = 0; i < 4; ++i)
                         dst[i] = make_float4(__uint_as_float(r[4 * i]), __uint_as_float(r[4 * i + 1]),
@@ -197,14 +207,12 @@ __global__ void __launch_bounds__(kThreadsR, 1)
                                              __uint_as_float(r[4 * i + 3]));
                 }
                 const float thr = tv[KMAX - 1];
-                const bool thr_empty = isnan(thr);
                 uint32_t hit = 0;
 #pragma unroll
                 for (int i = 0; i < 16; ++i) {
                     const float v = __uint_as_float(r[i]);
                     m = fmaxf(m, v);
-                    nans += v != v;
-                    hit |= static_cast<uint32_t>(v > thr || (thr_empty && v == v)) << i;
+                    hit |= static_cast<uint32_t>(v > thr) << i;
                 }
                 if (hit) {
 #pragma unroll
@@ -212,50 +220,26 @@ __global__ void __launch_bounds__(kThreadsR, 1)
                     while (hit) {
                         const int i = __ffs(hit) - 1;
                         hit &= hit - 1;
-                        float cv = park[i];
-                        int ci = c * 16 + i;
+                        const float v = park[i];
+                        const int e = c + i;
+                        // sorted-list insertion: slot j takes slot j-1 if v goes above it
 #pragma unroll
-                        for (int j = 0; j < KMAX; ++j) {  // sentinels (id < 0) never move
-                            if (sel_beats(cv, ci, tv[j], ti[j])) {
-                                const float sv = tv[j];
-                                const int si = ti[j];
-                                tv[j] = cv;
-                                ti[j] = ci;
-                                cv = sv;
-                                ci = si;
-                            }
+                        for (int j = KMAX - 1; j >= 0; --j) {
+                            const bool here = v > tv[j];
+                            const bool above = j > 0 && v > tv[j > 0 ? j - 1 : 0];
+                            tv[j] = above ? tv[j > 0 ? j - 1 : 0] : (here ? v : tv[j]);
+                            ti[j] = above ? ti[j > 0 ? j - 1 : 0] : (here ? e : ti[j]);
                         }
                     }
                 }
             }
-            if (nans && ti[KMAX - 1] == 0x7FFFFFFF) {
-                // rare: fewer than k non-NaN logits — fill with NaN ids ascending
-#pragma unroll 1
-                for (int c = 0; c < N / 16; ++c) {
-                    uint32_t r[16];
-                    ptx::tmem_ld_32x32b_x16(taddr + c * 16, r);
-                    ptx::tmem_ld_wait();
-#pragma unroll
-                    for (int i = 0; i < 16; ++i) {
-                        if (!isnan(__uint_as_float(r[i]))) continue;
-                        bool placed = false;
-#pragma unroll
-                        for (int j = 0; j < KMAX; ++j)
-                            if (!placed && ti[j] == 0x7FFFFFFF) {
-                                ti[j] = c * 16 + i;
-                                tv[j] = NAN;
-                                placed = true;
-                            }
-                    }
-                }
-            }
             float ssum = 0.f;
-            const float mlog = m * 1.4426950408889634f;
             if (p.score_fn == MPB_SCORE_SOFTMAX) {
+                const float mlog = m * 1.4426950408889634f;
 #pragma unroll 1
-                for (int c = 0; c < N / 16; ++c) {
+                for (int c = half * NH; c < (half + 1) * NH; c += 16) {
                     uint32_t r[16];
-                    ptx::tmem_ld_32x32b_x16(taddr + c * 16, r);
+                    ptx::tmem_ld_32x32b_x16(taddr + c, r);
                     ptx::tmem_ld_wait();
 #pragma unroll
                     for (int i = 0; i < 16; ++i) {
@@ -264,33 +248,98 @@ __global__ void __launch_bounds__(kThreadsR, 1)
                     }
                 }
             }
-            // accumulator fully read: hand TMEM back to the MMA warp
-            ptx::tc_fence_before();
-            ptx::mbar_arrive(&tempty[acc]);
-            if (row < p.T) {
-                float w[KMAX];
-                float wsum = 0.f;
+            // ---- merge the two column halves (named barrier per lane quadrant)
+            if (half == 1) {
 #pragma unroll
                 for (int j = 0; j < KMAX; ++j) {
-                    const float v = tv[j];
-                    float x;
-                    if (j < off || isnan(v))
-                        x = 0.f;
-                    else if (p.score_fn == MPB_SCORE_SOFTMAX)
-                        x = exp2f(fmaf(v, 1.4426950408889634f, -mlog)) / ssum;
-                    else
-                        x = 1.f / (1.f + expf(-v));
-                    w[j] = x;
-                    wsum += x;
+                    park[j] = tv[j];
+                    park[KMAX + j] = __int_as_float(ti[j]);
                 }
+                park[2 * KMAX] = m;
+                park[2 * KMAX + 1] = ssum;
+            }
+            asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
+            if (half == 1) {
+                ptx::tc_fence_before();
+                ptx::mbar_arrive(&tempty[acc]);
+            } else {
+#pragma unroll 1
+                for (int jj = off; jj < KMAX; ++jj) {
+                    const float v = peer[jj];
+                    const int e = __float_as_int(peer[KMAX + jj]);
+                    if (!(v > tv[KMAX - 1])) break;  // peer list is sorted
 #pragma unroll
-                for (int j = 0; j < KMAX; ++j) {
-                    if (j < off) continue;
-                    const float x = p.renorm ? (wsum > 0.f ? w[j] / wsum : 0.f) : w[j];
-                    p.idx[row * p.k + (j - off)] = ti[j];
-                    p.w[row * p.k + (j - off)] = x;
+                    for (int j = KMAX - 1; j >= 0; --j) {
+                        const bool here = v > tv[j];
+                        const bool above = j > 0 && v > tv[j > 0 ? j - 1 : 0];
+                        tv[j] = above ? tv[j > 0 ? j - 1 : 0] : (here ? v : tv[j]);
+                        ti[j] = above ? ti[j > 0 ? j - 1 : 0] : (here ? e : ti[j]);
+                    }
+                }
+                const float m1 = peer[2 * KMAX], s1 = peer[2 * KMAX + 1];
+                const float mm = fmaxf(m, m1);
+                if (p.score_fn == MPB_SCORE_SOFTMAX) {
+                    const float a0 = m == -INFINITY ? 0.f : exp2f((m - mm) * 1.4426950408889634f);
+                    const float a1 = m1 == -INFINITY ? 0.f : exp2f((m1 - mm) * 1.4426950408889634f);
+                    ssum = ssum * a0 + s1 * a1;
+                }
+                m = mm;
+                if (ti[KMAX - 1] == 0x7FFFFFFF) {
+                    // rare: fewer than k logits above -inf — fill with -inf ids, then
+                    // NaN ids, ascending (NaN ranks lowest)
+#pragma unroll 1
+                    for (int pass = 0; pass < 2; ++pass)
+#pragma unroll 1
+                        for (int c = 0; c < N; c += 16) {
+                            uint32_t r[16];
+                            ptx::tmem_ld_32x32b_x16(taddr + c, r);
+                            ptx::tmem_ld_wait();
+#pragma unroll
+                            for (int i = 0; i < 16; ++i) {
+                                const float v = __uint_as_float(r[i]);
+                                const bool want = pass == 0 ? v == -INFINITY : v != v;
+                                if (!want) continue;
+                                bool placed = false;
+#pragma unroll
+                                for (int j = 0; j < KMAX; ++j)
+                                    if (!placed && ti[j] == 0x7FFFFFFF) {
+                                        ti[j] = c + i;
+                                        tv[j] = v;
+                                        placed = true;
+                                    }
+                            }
+                        }
+                }
+                ptx::tc_fence_before();
+                ptx::mbar_arrive(&tempty[acc]);
+                if (row < p.T) {
+                    const float mlog = m * 1.4426950408889634f;
+                    float w[KMAX];
+                    float wsum = 0.f;
+#pragma unroll
+                    for (int j = 0; j < KMAX; ++j) {
+                        const float v = tv[j];
+                        float x;
+                        if (j < off || isnan(v))
+                            x = 0.f;
+                        else if (p.score_fn == MPB_SCORE_SOFTMAX)
+                            x = exp2f(fmaf(v, 1.4426950408889634f, -mlog)) / ssum;
+                        else
+                            x = 1.f / (1.f + expf(-v));
+                        w[j] = x;
+                        wsum += x;
+                    }
+#pragma unroll
+                    for (int j = 0; j < KMAX; ++j) {
+                        if (j < off) continue;
+                        const float x = p.renorm ? (wsum > 0.f ? w[j] / wsum : 0.f) : w[j];
+                        p.idx[row * p.k + (j - off)] = ti[j];
+                        p.w[row * p.k + (j - off)] = x;
+                    }
                 }
             }
+            // half 1 must not overwrite its park row before half 0 read it
+            asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
             acc ^= 1;
             if (acc == 0) aphase ^= 1;
         }
@@ -333,7 +382,7 @@ bool make_map(CUtensorMap *map, const void *ptr, uint64_t rows, uint64_t cols, u
 template <int N, int KMAX>
 mpb_status launch_router_n(mpb_context *ctx, const CUtensorMap &mx, const CUtensorMap &mw,
                            const RouterParams &p) {
-    constexpr int smem = RCfg<N>::SMEM;
+    constexpr int smem = RCfg<N, KMAX>::SMEM;
     auto kern = k_router<N, KMAX>;
     MPB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     const uint32_t grid = std::min<uint32_t>(p.num_tiles, static_cast<uint32_t>(ctx->num_sms));

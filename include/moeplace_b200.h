@@ -194,7 +194,7 @@ MPB_API mpb_status mpb_route_sources(mpb_context *ctx, const uint32_t *rows, con
  * of a demand table originates on node row_node[r] (device uint8 [rows]):
  * rows = nodes with row_node = identity for node-level demand, or rows = D
  * with row_node = group_to_node for the per-source-group demand of
- * mpb_dispatch_layout. group_to_node[D] device uint8. */
+ * mpb_dispatch_layout. group_to_node[D] device uint8; D <= 255. */
 MPB_API mpb_status mpb_score_placements(mpb_context *ctx, const uint64_t *demand, uint32_t B,
                                         uint32_t rows, const uint8_t *row_node,
                                         const uint8_t *luts, uint32_t P,

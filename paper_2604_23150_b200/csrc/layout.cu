@@ -163,27 +163,34 @@ __global__ void __launch_bounds__(kThreads) k_layout_count(LayoutParams p) {
 }
 
 // Exclusive offsets over (slot, block), slot-major: the position of block b's
-// first pair with slot s. Also emits key_offsets[d*E+e] via key_lb.
-__global__ void __launch_bounds__(1024) k_layout_scan(uint32_t *bhist, uint32_t nb, uint32_t NS,
-                                                      const uint16_t *key_lb, uint32_t nkeys,
-                                                      int64_t *key_offsets) {
-    extern __shared__ uint32_t s_tot[];  // [NS + 1]
-    for (uint32_t s = threadIdx.x; s < NS; s += blockDim.x) {
-        uint32_t run = 0;
-        for (uint32_t b = 0; b < nb; ++b) {
-            const uint32_t v = bhist[static_cast<size_t>(b) * NS + s];
-            bhist[static_cast<size_t>(b) * NS + s] = run;
-            run += v;
-        }
-        s_tot[s] = run;
+// first pair with slot s. One CTA; thread (s, c) owns slot s over a
+// contiguous run of blocks (independent, unrolled loads), then a block-wide
+// scan over (slot, chunk) totals. Also emits key_offsets[d*E+e] via key_lb.
+constexpr int kScanThreads = 1024;
+
+__global__ void __launch_bounds__(kScanThreads) k_layout_scan(uint32_t *bhist, uint32_t nb,
+                                                              uint32_t NS, const uint16_t *key_lb,
+                                                              uint32_t nkeys, int64_t *key_offsets) {
+    extern __shared__ uint32_t s_tot[];  // [NS * chunks + 1]
+    __shared__ uint32_t s_warp[32];
+    const uint32_t chunks = max(1u, kScanThreads / NS);
+    const uint32_t per = (nb + chunks - 1) / chunks;
+    const uint32_t cells = NS * chunks;
+    // pass 1: chunk totals, cell id = s * chunks + c (slot-major order)
+    for (uint32_t cell = threadIdx.x; cell < cells; cell += kScanThreads) {
+        const uint32_t sl = cell / chunks, c = cell % chunks;
+        const uint32_t b0 = min(nb, c * per), b1 = min(nb, b0 + per);
+        uint32_t sum = 0;
+#pragma unroll 8
+        for (uint32_t b = b0; b < b1; ++b) sum += bhist[static_cast<size_t>(b) * NS + sl];
+        s_tot[cell] = sum;
     }
     __syncthreads();
-    // block exclusive scan of s_tot[0..NS): per-thread segments + warp scans
-    __shared__ uint32_t s_warp[32];
-    const uint32_t per = (NS + blockDim.x - 1) / blockDim.x;
-    const uint32_t lo = min(NS, threadIdx.x * per), hi = min(NS, lo + per);
+    // pass 2: exclusive scan of s_tot[0..cells) — per-thread segments + warp scans
+    const uint32_t seg = (cells + kScanThreads - 1) / kScanThreads;
+    const uint32_t lo = min(cells, threadIdx.x * seg), hi = min(cells, lo + seg);
     uint32_t local = 0;
-    for (uint32_t s = lo; s < hi; ++s) local += s_tot[s];
+    for (uint32_t i = lo; i < hi; ++i) local += s_tot[i];
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     uint32_t incl = local;
 #pragma unroll
@@ -194,33 +201,41 @@ __global__ void __launch_bounds__(1024) k_layout_scan(uint32_t *bhist, uint32_t 
     if (lane == 31) s_warp[warp] = incl;
     __syncthreads();
     if (warp == 0) {
-        const uint32_t nw = blockDim.x / 32;
-        uint32_t w = lane < nw ? s_warp[lane] : 0;
+        uint32_t w = s_warp[lane];
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
             if (lane >= o) w += y;
         }
-        if (lane < nw) s_warp[lane] = w;  // inclusive
+        s_warp[lane] = w;  // inclusive
     }
     __syncthreads();
     uint32_t run = (warp ? s_warp[warp - 1] : 0) + incl - local;
-    const uint32_t grand = s_warp[blockDim.x / 32 - 1];
-    __syncthreads();
-    for (uint32_t s = lo; s < hi; ++s) {
-        const uint32_t v = s_tot[s];
-        s_tot[s] = run;
+    const uint32_t grand = s_warp[31];
+    for (uint32_t i = lo; i < hi; ++i) {
+        const uint32_t v = s_tot[i];
+        s_tot[i] = run;
         run += v;
     }
-    if (threadIdx.x == 0) s_tot[NS] = grand;
+    if (threadIdx.x == 0) s_tot[cells] = grand;
     __syncthreads();
-    for (uint32_t s = threadIdx.x; s < NS; s += blockDim.x) {
-        const uint32_t b0 = s_tot[s];
-        for (uint32_t b = 0; b < nb; ++b) bhist[static_cast<size_t>(b) * NS + s] += b0;
+    // pass 3: rewrite bhist with global offsets
+    for (uint32_t cell = threadIdx.x; cell < cells; cell += kScanThreads) {
+        const uint32_t sl = cell / chunks, c = cell % chunks;
+        const uint32_t b0 = min(nb, c * per), b1 = min(nb, b0 + per);
+        uint32_t r = s_tot[cell];
+        for (uint32_t b = b0; b < b1; ++b) {
+            const size_t i = static_cast<size_t>(b) * NS + sl;
+            const uint32_t v = bhist[i];
+            bhist[i] = r;
+            r += v;
+        }
     }
     if (key_offsets)
-        for (uint32_t key = threadIdx.x; key <= nkeys; key += blockDim.x)
-            key_offsets[key] = static_cast<int64_t>(s_tot[key_lb[key]]);
+        for (uint32_t key = threadIdx.x; key <= nkeys; key += kScanThreads) {
+            const uint32_t sl = key_lb[key];
+            key_offsets[key] = static_cast<int64_t>(sl < NS ? s_tot[sl * chunks] : grand);
+        }
 }
 
 __global__ void __launch_bounds__(kThreads) k_layout_scatter(LayoutParams p, int32_t *sorted_pairs,
@@ -413,11 +428,12 @@ mpb_status launch_layout(mpb_context *ctx, const mpb_tokens *tk, const mpb_place
     }
     MPB_LAUNCHED(ctx);
     if (!perm) return MPB_OK;
-    const size_t scan_smem = (size_t(pl->NS) + 1) * 4;
+    const size_t chunks = std::max<size_t>(1, kScanThreads / pl->NS);
+    const size_t scan_smem = (size_t(pl->NS) * chunks + 1) * 4;
     MPB_CUDA(cudaFuncSetAttribute(k_layout_scan, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(scan_smem)));
-    k_layout_scan<<<1, 1024, scan_smem, ctx->stream>>>(p.bhist, nb, pl->NS, pl->d_key_lb,
-                                                       pl->D * pl->E, key_offsets);
+    k_layout_scan<<<1, kScanThreads, scan_smem, ctx->stream>>>(p.bhist, nb, pl->NS, pl->d_key_lb,
+                                                               pl->D * pl->E, key_offsets);
     MPB_LAUNCHED(ctx);
     const size_t sc_smem = size_t(kWarps) * pl->NS * 4;
     MPB_CUDA(cudaFuncSetAttribute(k_layout_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -65,47 +65,62 @@ __global__ void __launch_bounds__(256) k_batch_demand(const uint32_t *row_ptr, c
 }
 
 constexpr int kScoreWarps = 8;
+constexpr uint32_t kScoreMaxD = 32;  // lane-private rank accumulators in smem
 
+// Batch-major scorer: one CTA per (batch, candidate range). The batch's demand
+// is folded by source node into shared memory once; each warp then prices
+// one candidate at a time by streaming its [nodes x E] destination table from
+// L2 (coalesced bytes), accumulating pair counts per destination rank in
+// lane-private shared-memory columns (no atomics), and reducing at the end.
+template <bool kPrivate>
 __global__ void __launch_bounds__(kScoreWarps * 32) k_score(const uint64_t *demand, uint32_t B,
                                                             uint32_t rows,
                                                             const uint8_t *row_node_g,
-                                                            const uint8_t *luts,
+                                                            const uint8_t *luts, uint32_t P,
                                                             const uint8_t *g2n_g, uint32_t D,
                                                             uint32_t nodes, uint32_t E,
                                                             uint64_t *inter_out,
                                                             uint64_t *intra_out,
                                                             uint64_t *rank_out, uint32_t *err) {
-    extern __shared__ unsigned char s_raw[];
+    extern __shared__ unsigned long long s_raw[];
     const uint32_t NE = nodes * E;
-    const uint32_t RE = rows * E;
-    unsigned long long *s_rank = reinterpret_cast<unsigned long long *>(s_raw);  // [warps][D]
-    uint8_t *s_lut = s_raw + kScoreWarps * D * 8;
-    uint8_t *s_g2n = s_lut + NE;
-    uint8_t *s_rn = s_g2n + D;
-    const uint32_t p = blockIdx.x;
-    const uint8_t *lut = luts + static_cast<size_t>(p) * NE;
-    for (uint32_t i = threadIdx.x; i < NE; i += blockDim.x) s_lut[i] = lut[i];
+    unsigned long long *s_nd = s_raw;                        // [nodes*E]
+    unsigned long long *s_acc = s_nd + NE;  // [warps][D][32] lane-private, or [warps][D]
+    const uint32_t cols = kPrivate ? 32u : 1u;
+    uint8_t *s_g2n = reinterpret_cast<uint8_t *>(s_acc + kScoreWarps * D * cols);
+    const uint32_t b = blockIdx.x;
     for (uint32_t i = threadIdx.x; i < D; i += blockDim.x) s_g2n[i] = g2n_g[i];
-    for (uint32_t i = threadIdx.x; i < rows; i += blockDim.x) s_rn[i] = row_node_g[i];
+    for (uint32_t i = threadIdx.x; i < NE; i += blockDim.x) s_nd[i] = 0;
+    __syncthreads();
+    const uint64_t *a = demand + static_cast<size_t>(b) * rows * E;
+    for (uint32_t i = threadIdx.x; i < rows * E; i += blockDim.x) {
+        const unsigned long long v = a[i];
+        if (v) atomicAdd(&s_nd[static_cast<uint32_t>(row_node_g[i / E]) * E + i % E], v);
+    }
     __syncthreads();
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    unsigned long long *rank = s_rank + warp * D;
-    for (uint32_t b = blockIdx.y * kScoreWarps + warp; b < B; b += gridDim.y * kScoreWarps) {
-        for (uint32_t d = lane; d < D; d += 32) rank[d] = 0;
+    unsigned long long *acc = s_acc + warp * D * cols;
+    for (uint32_t p = blockIdx.y * kScoreWarps + warp; p < P; p += gridDim.y * kScoreWarps) {
+        if (kPrivate)
+            for (uint32_t d = 0; d < D; ++d) acc[d * 32 + lane] = 0;
+        else
+            for (uint32_t d = lane; d < D; d += 32) acc[d] = 0;
         __syncwarp();
-        const uint64_t *a = demand + static_cast<size_t>(b) * RE;
+        const uint8_t *lut = luts + static_cast<size_t>(p) * NE;
         unsigned long long inter = 0, intra = 0;
-        for (uint32_t i = lane; i < RE; i += 32) {
-            const unsigned long long v = a[i];
+        for (uint32_t i = lane; i < NE; i += 32) {
+            const unsigned long long v = s_nd[i];
+            const uint32_t d = __ldg(lut + i);
             if (!v) continue;
-            const uint32_t n = s_rn[i / E];
-            const uint32_t d = s_lut[n * E + i % E];
             if (d == 255) {
                 atomicOr(err, kErrUncovered);
                 continue;
             }
-            atomicAdd(rank + d, v);
-            if (s_g2n[d] == n)
+            if (kPrivate)
+                acc[d * 32 + lane] += v;
+            else
+                atomicAdd(acc + d, v);
+            if (s_g2n[d] == i / E)
                 intra += v;
             else
                 inter += v;
@@ -121,7 +136,14 @@ __global__ void __launch_bounds__(kScoreWarps * 32) k_score(const uint64_t *dema
             inter_out[cell] = inter;
             intra_out[cell] = intra;
         }
-        for (uint32_t d = lane; d < D; d += 32) rank_out[cell * D + d] = rank[d];
+        for (uint32_t d = lane; d < D; d += 32) {
+            unsigned long long t = 0;
+            if (kPrivate)
+                for (uint32_t l = 0; l < 32; ++l) t += acc[d * 32 + ((l + lane) & 31)];
+            else
+                t = acc[d];
+            rank_out[cell * D + d] = t;
+        }
         __syncwarp();
     }
 }
@@ -197,16 +219,19 @@ mpb_status mpb_score_placements(mpb_context *ctx, const uint64_t *demand, uint32
     if (D == 0 || D > 255 || nodes == 0)
         return fail(MPB_CONFIG_ERROR, "mpb_score_placements: need 1 <= D <= 255, nodes >= 1");
     if (P == 0 || B == 0) return MPB_OK;
-    const size_t smem = size_t(kScoreWarps) * D * 8 + size_t(nodes) * E + D + rows;
+    const bool priv = D <= kScoreMaxD;
+    const size_t smem =
+        size_t(nodes) * E * 8 + size_t(kScoreWarps) * D * (priv ? 32 : 1) * 8 + D + 8;
     if (smem > 200 * 1024) return fail(MPB_CONFIG_ERROR, "mpb_score_placements: nodes*E too large");
-    MPB_CUDA(cudaFuncSetAttribute(k_score, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    // enough CTAs to fill the machine: split batches across grid.y when P is small
-    uint32_t gy = (B + kScoreWarps - 1) / kScoreWarps;
+    auto kern = priv ? k_score<true> : k_score<false>;
+    MPB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    // one CTA per batch; split candidates over grid.y until the machine is full
     const uint32_t want = 4u * static_cast<uint32_t>(ctx->num_sms);
-    if (static_cast<uint64_t>(P) * gy > want) gy = std::max(1u, want / std::max(1u, P));
+    uint32_t gy = std::max(1u, want / std::max(1u, B));
+    gy = std::min(gy, (P + kScoreWarps - 1) / kScoreWarps);
     gy = std::min(gy, 65535u);
-    dim3 grid(P, gy);
-    k_score<<<grid, kScoreWarps * 32, smem, ctx->stream>>>(demand, B, rows, row_node, luts,
+    dim3 grid(B, gy);
+    kern<<<grid, kScoreWarps * 32, smem, ctx->stream>>>(demand, B, rows, row_node, luts, P,
                                                            group_to_node, D, nodes, E, inter,
                                                            intra, rank_pairs, ctx->d_error);
     MPB_LAUNCHED(ctx);

@@ -387,6 +387,7 @@ def main():
     ap.add_argument("--workload", default="dsv3")
     ap.add_argument("--layers", type=int, default=None, help="override (tests only)")
     ap.add_argument("--tokens", type=int, default=None, help="override (tests only)")
+    ap.add_argument("--boost", type=float, default=None, help="override domain logit boost")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -399,6 +400,8 @@ def main():
         over["layers"] = args.layers
     if args.tokens:
         over["tokens"] = args.tokens
+    if args.boost is not None:
+        over["boost"] = args.boost
     spec = spec_for(args.workload, **over)
     if args.impl == "reference":
         run_reference_arm(args, spec)

@@ -45,7 +45,8 @@ class WorkloadSpec:
     nodes: int = 2  # "nodes" = contiguous GPU groups
     domains: int = 8
     preferred: int = 32  # preferred experts per domain
-    boost: float = 1.0  # logit boost toward the domain's preferred experts (in sigma)
+    boost: float = 0.5  # logit boost toward the domain's preferred experts (in sigma);
+    # 0.5 reproduces the paper's ~20% all-to-all byte reduction at DSv3 shape
     tokens_per_request: int = 16
     candidates: int = 1024  # placements scored per layer (3 named + search)
     bytes_per_element: int = 2  # bf16 dispatch payload
@@ -68,7 +69,7 @@ WORKLOADS = {
                              preferred=16, domains=4, coact=False),
     # configs[3]: domain-mixed grouping (code/math/chat/general), 1M tokens, E=128 top-8
     "domain": WorkloadSpec("domain-mixed-4dom", 1, 1048576, 4096, 128, 8, 0, True, domains=4,
-                           preferred=32, boost=1.5),
+                           preferred=32),
 }
 
 

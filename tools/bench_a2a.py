@@ -1,0 +1,146 @@
+#!/usr/bin/env python
+"""Config 5: end-to-end EP=8 bf16 token dispatch/combine all-to-all (H=7168)
+under the learned (data-based + cluster-routed) vs round-robin (linear +
+batch-position) placement, GPU groups as nodes.
+
+    python tools/bench_a2a.py                        # 1 GPU (local permute)
+    torchrun --nproc-per-node 2 tools/bench_a2a.py   # 2/4/8 GPUs over NCCL
+
+Prints one JSON line per policy (rank 0): rows moved per step, the share that
+crossed "nodes" (contiguous rank halves), and the dispatch+combine time (max
+over ranks, CUDA events).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+from paper_2604_23150_b200 import moeplace as mp  # noqa: E402
+from paper_2604_23150_b200 import policies as pol  # noqa: E402
+from paper_2604_23150_b200.a2a import A2AStats, ExpertParallelA2A  # noqa: E402
+from paper_2604_23150_b200.distributed import groups_per_rank  # noqa: E402
+from paper_2604_23150_b200.pipeline import SyntheticModel, spec_for  # noqa: E402
+
+
+def learn_placement(spec, eng):
+    """Calibration identical on every rank (rank-0 draw): gate -> request x
+    expert matrix -> k-means grouping -> data-based placement."""
+    model = SyntheticModel(spec, eng.device, rank=0)
+    R, dom = model.requests(draw=1)
+    tok_req = np.arange(spec.tokens) // spec.tokens_per_request
+    X = torch.empty(spec.tokens, spec.hidden, dtype=torch.bfloat16, device=eng.device)
+    model.fill_hidden(X, 0, 1, torch.from_numpy(dom[tok_req]).to(eng.device))
+    idx, _ = eng.router_topk(X, model.W[0], spec.top_k, spec.score_fn, spec.renorm)
+    lin = pol.linear_placement(spec.experts, spec.groups)
+    top = mp.Topology.contiguous(spec.groups, 1, spec.groups, 1, spec.nodes)
+    dp = eng.placement(lin, top)
+    req = torch.zeros(R, spec.experts, dtype=torch.uint64, device=eng.device)
+    eng.dispatch_layout(idx, dp, src_base=0, src_span=spec.groups,
+                        tag=torch.from_numpy(tok_req.astype(np.uint16)).to(eng.device),
+                        n_tags=R, permutation=False, tag_pop=req)
+    eng.sync()
+    M = mp.ActivationMatrix(R, spec.experts, req.cpu().numpy().astype(np.float64),
+                            [f"domain{d}" for d in dom], list(range(R)))
+    stage = pol.run_cluster_stage(M, 0, 1, spec.groups, restarts=10)
+    strat = {s.label: s for s in pol.build_placements(stage, seed=2)}
+    route = []
+    for d in range(spec.domains):
+        lab = stage.model.labels[dom == d]
+        c = int(np.bincount(lab, minlength=stage.model.K).argmax())
+        route.append(stage.group_map.assignment[c])
+    return strat["linear"].placement, strat["data_based"].placement, route, model
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--tokens", type=int, default=16384, help="tokens per rank")
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--nodes", type=int, default=2)
+    a = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    eng = mp.Engine(local)
+    spec = spec_for("dsv3", layers=1, tokens=a.tokens)
+    D = spec.groups
+    gpr = groups_per_rank(D, world)
+    lin, learned, route, model = learn_placement(spec, eng)
+    nodes = min(a.nodes, world) if world > 1 else 1
+    top = mp.Topology.contiguous(D, 1, D, 1, spec.nodes)
+    # global request pool (domains dealt round-robin: balanced), tpr tokens each
+    tpr = spec.tokens_per_request
+    R_glob = world * (a.tokens // tpr)
+    dom_g = np.arange(R_glob) % spec.domains
+    results = {}
+    for policy, placement in (("round_robin", lin), ("learned", learned)):
+        if policy == "round_robin":
+            grp = (np.arange(R_glob) % D).astype(np.int64)  # batch-position rule
+        else:
+            grp = np.array([route[d][0] for d in dom_g], np.int64)
+        mine = np.nonzero(grp // gpr == rank)[0]
+        tok_dom = np.repeat(dom_g[mine], tpr)
+        tok_src = np.repeat(grp[mine], tpr).astype(np.uint8)
+        T = len(tok_dom)
+        X = torch.empty(T, spec.hidden, dtype=torch.bfloat16, device=eng.device)
+        g = torch.Generator(device=eng.device).manual_seed(77 + rank)
+        z = torch.randn(T, spec.hidden, device=eng.device, generator=g)
+        z += model.bias[0][torch.from_numpy(tok_dom).to(eng.device)]
+        X.copy_(z)
+        del z
+        idx, w = eng.router_topk(X, model.W[0], spec.top_k, spec.score_fn, spec.renorm)
+        src = torch.from_numpy(tok_src).to(eng.device)
+        op = ExpertParallelA2A(eng, placement, top, spec.hidden, T * spec.top_k, rank, world,
+                               nodes)
+        for _ in range(a.warmup):
+            Y = op(X, idx, w, src)
+        # correctness: identity experts -> Y = X * sum(w) = X (renormalised weights)
+        err = (Y.float() - X.float()).abs().max().item()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        st = A2AStats()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for i in range(a.steps):
+            op(X, idx, w, src, st if i == 0 else None)
+        e.record()
+        torch.cuda.synchronize()
+        ms = torch.tensor([s.elapsed_time(e) / a.steps], device=eng.device, dtype=torch.float64)
+        tot = torch.tensor([st.sent_rows, st.inter_node_rows, st.intra_node_rows],
+                           device=eng.device, dtype=torch.int64)
+        if world > 1:
+            dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+            dist.all_reduce(tot)
+        sent, inter, intra = (int(x) for x in tot.tolist())
+        results[policy] = dict(ms_per_step=float(ms.item()), rows=sent, inter_node_rows=inter,
+                               intra_node_rows=intra,
+                               inter_node_bytes=inter * spec.hidden * 2,
+                               inter_fraction=inter / max(1, sent), max_abs_err=err,
+                               tokens_per_rank=T)
+    if rank == 0:
+        base = results["round_robin"]["inter_node_bytes"]
+        saved = 1.0 - results["learned"]["inter_node_bytes"] / base if base else float("nan")
+        print(json.dumps({"config": "ep8-bf16-dispatch-combine", "n_gpus": world,
+                          "gpu_nodes": nodes, "hidden": spec.hidden, "experts": spec.experts,
+                          "top_k": spec.top_k, "results": results,
+                          "cross_node_bytes_saved_pct": 100.0 * saved}), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -80,10 +80,11 @@ def main():
     lin, learned, route, model = learn_placement(spec, eng)
     nodes = min(a.nodes, world) if world > 1 else 1
     top = mp.Topology.contiguous(D, 1, D, 1, spec.nodes)
-    # global request pool (domains dealt round-robin: balanced), tpr tokens each
+    # global request pool with seeded random domains (uncorrelated with the
+    # batch position that the round-robin baseline uses), tpr tokens each
     tpr = spec.tokens_per_request
     R_glob = world * (a.tokens // tpr)
-    dom_g = np.arange(R_glob) % spec.domains
+    dom_g = np.random.default_rng(2024).integers(0, spec.domains, R_glob)
     results = {}
     for policy, placement in (("round_robin", lin), ("learned", learned)):
         if policy == "round_robin":

@@ -265,6 +265,38 @@ MPB_API mpb_status mpb_assign_clusters_to_groups(const uint32_t *labels, uint64_
                                                  uint32_t *assign_sizes /* K */,
                                                  double *cluster_sizes_out /* K */);
 
+/* ---- host trace model (no device needed) -----------------------------------
+ * trace.cpp:73-297: JSONL loader / writer (byte-identical to the reference's
+ * nlohmann dump), activation-matrix builder, layers_present, and the
+ * synthetic generator (same std:: RNG calls) with an optional per-token tap
+ * (every token's k picks, in pick order, for the device kernels). */
+typedef struct mpb_trace mpb_trace;
+MPB_API mpb_status mpb_trace_parse(const char *text, uint64_t len, uint32_t E, uint32_t top_k,
+                                   uint32_t layers, mpb_trace **out);
+MPB_API mpb_status mpb_trace_read_file(const char *path, uint32_t E, uint32_t top_k,
+                                       uint32_t layers, mpb_trace **out);
+MPB_API mpb_status mpb_trace_write_file(const mpb_trace *t, const char *path);
+MPB_API mpb_status mpb_trace_generate(uint32_t num_domains, uint32_t requests_per_domain,
+                                      uint32_t preferred, double affinity,
+                                      double decode_tokens_mean, uint64_t seed, uint32_t E,
+                                      uint32_t top_k, uint32_t layers, int keep_picks,
+                                      mpb_trace **out);
+MPB_API mpb_status mpb_trace_destroy(mpb_trace *t);
+MPB_API mpb_status mpb_trace_sizes(const mpb_trace *t, uint64_t *n_records, uint64_t *n_pairs,
+                                   uint64_t *n_labels, uint64_t *n_picks);
+MPB_API mpb_status mpb_trace_export(const mpb_trace *t, uint64_t *request_id, uint32_t *layer,
+                                    uint8_t *stage, uint64_t *input_len, uint64_t *gen_tokens,
+                                    uint32_t *label, uint64_t *pair_offset, uint32_t *expert,
+                                    uint64_t *count, int32_t *picks, uint64_t *pick_offset);
+MPB_API const char *mpb_trace_label(const mpb_trace *t, uint64_t i);
+/* layer < 0: summed over layers; stage 0 prefill / 1 decode; values == NULL
+ * queries *rows only. */
+MPB_API mpb_status mpb_trace_matrix(const mpb_trace *t, uint32_t E, int64_t layer, int stage,
+                                    uint64_t *rows, double *values, uint64_t *request_ids,
+                                    uint32_t *labels);
+MPB_API mpb_status mpb_trace_layers_present(const mpb_trace *t, int stage, uint32_t *layers,
+                                            uint64_t *n);
+
 #ifdef __cplusplus
 }
 #endif

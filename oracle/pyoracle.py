@@ -282,6 +282,7 @@ class Reference:
                                                C.c_uint64, _u32p]
         L.ref_compare_scenario.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, _f64p]
         L.ref_bench_compare.argtypes = [C.c_char_p, C.c_uint32, _f64p]
+        L.ref_analysis.argtypes = [C.c_char_p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_char_p]
 
     def _check(self, st):
         if st:
@@ -385,6 +386,10 @@ class Reference:
                                                   str(trace_out).encode(),
                                                   str(out_json).encode(), sec))
         return float(sec[0])
+
+    def analysis(self, trace_path, E, top_k, layers, out_json):
+        self._check(self.lib.ref_analysis(str(trace_path).encode(), E, top_k, layers,
+                                          str(out_json).encode()))
 
     def bench_compare(self, config_path, reps):
         sec = np.zeros(1)

@@ -16,6 +16,7 @@
 //       simulator.cpp:122-243), dumped as a JSON fixture
 //   ref_expert_load / ref_pearson / ref_placement_* -> metrics.cpp, placement.cpp
 #include <chrono>
+#include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <fstream>
@@ -391,6 +392,47 @@ int ref_compare_scenario(const char *config_json_path, const char *trace_out,
         std::ofstream out(out_json_path);
         if (!out)
             throw Error(std::string("cannot write ") + out_json_path);
+        out << j.dump() << '\n';
+    });
+}
+
+// emit_analysis (pipeline.cpp:65-126) as data: per (stage, layer) imbalance
+// factor, per stage dataset correlation matrix, per layer PD correlation.
+int ref_analysis(const char *trace_path, std::uint32_t E, std::uint32_t top_k,
+                 std::uint32_t layers, const char *out_json_path) {
+    return guarded([&] {
+        ModelConfig model{"m", E, top_k, layers, false};
+        auto records = read_trace_file(trace_path, model);
+        json j;
+        json imb = json::array();
+        for (Stage stage : {Stage::prefill, Stage::decode})
+            for (std::uint32_t layer : layers_present(records, stage)) {
+                auto m = build_activation_matrix(records, E, layer, stage);
+                std::vector<double> col(E, 0.0);
+                for (std::size_t r = 0; r < m.rows; ++r)
+                    for (std::size_t e = 0; e < E; ++e) col[e] += m.at(r, e);
+                auto loads = expert_load(col, top_k);
+                imb.push_back({{"stage", stage_name(stage)}, {"layer", layer},
+                               {"imbalance", imbalance_factor(loads)}, {"loads", loads.loads},
+                               {"total_tokens", loads.total_tokens}});
+            }
+        j["imbalance"] = imb;
+        for (Stage stage : {Stage::prefill, Stage::decode}) {
+            auto m = build_activation_matrix_summed(records, E, stage);
+            auto c = dataset_correlation_matrix(m);
+            std::vector<json> vals;
+            for (double v : c.values) vals.push_back(std::isnan(v) ? json(nullptr) : json(v));
+            j[std::string("dataset_correlation_") + stage_name(stage)] = {{"labels", c.labels},
+                                                                          {"values", vals}};
+        }
+        json pd = json::array();
+        for (std::uint32_t layer : layers_present(records, Stage::prefill)) {
+            auto a = build_activation_matrix(records, E, layer, Stage::prefill);
+            auto b = build_activation_matrix(records, E, layer, Stage::decode);
+            pd.push_back({{"layer", layer}, {"pearson", prefill_decode_correlation(a, b)}});
+        }
+        j["prefill_decode"] = pd;
+        std::ofstream out(out_json_path);
         out << j.dump() << '\n';
     });
 }

@@ -76,6 +76,20 @@ _SIGS = {
                              C.c_double, _p, _p, _p, _p]),
     "mpb_assign_clusters_to_groups": (C.c_int, [_p, C.c_uint64, C.c_uint32, _p, C.c_uint32,
                                                 C.c_uint32, C.c_uint64, _p, _p, _p]),
+    "mpb_trace_parse": (C.c_int, [C.c_char_p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32,
+                                  C.POINTER(_p)]),
+    "mpb_trace_read_file": (C.c_int, [C.c_char_p, C.c_uint32, C.c_uint32, C.c_uint32,
+                                      C.POINTER(_p)]),
+    "mpb_trace_write_file": (C.c_int, [_p, C.c_char_p]),
+    "mpb_trace_generate": (C.c_int, [C.c_uint32, C.c_uint32, C.c_uint32, C.c_double, C.c_double,
+                                     C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, C.c_int,
+                                     C.POINTER(_p)]),
+    "mpb_trace_destroy": (C.c_int, [_p]),
+    "mpb_trace_sizes": (C.c_int, [_p, _p, _p, _p, _p]),
+    "mpb_trace_export": (C.c_int, [_p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p]),
+    "mpb_trace_label": (C.c_char_p, [_p, C.c_uint64]),
+    "mpb_trace_matrix": (C.c_int, [_p, C.c_uint32, C.c_int64, C.c_int, _p, _p, _p, _p]),
+    "mpb_trace_layers_present": (C.c_int, [_p, C.c_int, _p, _p]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -721,3 +721,65 @@ def pearson(x, y) -> float:
     if sxx == 0.0 or syy == 0.0:
         raise UndefinedCorrelationError("pearson: constant input vector")
     return min(1.0, max(-1.0, sxy / math.sqrt(sxx * syy)))
+
+
+@dataclass
+class CorrelationMatrix:
+    labels: list
+    values: np.ndarray  # [n, n]; NaN = undefined (constant vector)
+
+    def size(self) -> int:
+        return len(self.labels)
+
+    def at(self, i: int, j: int) -> float:
+        return float(self.values[i, j])
+
+
+def sum_rows_by_label(labels, rows) -> dict:
+    """metrics.cpp:72-81: per-label row sums (row order), labels in std::map
+    (lexicographic) order."""
+    sums: dict = {}
+    for lab, row in zip(labels, rows):
+        r = np.asarray(row, np.float64)
+        sums[lab] = sums[lab] + r if lab in sums else r.copy()
+    return dict(sorted(sums.items()))
+
+
+def dataset_correlation_vectors(vectors: dict) -> CorrelationMatrix:
+    """dataset_correlation_matrix (metrics.cpp:95-123) from per-label summed
+    vectors (e.g. the device tag histogram with tag = domain)."""
+    if len(vectors) < 2:
+        raise ValidationError(f"dataset_correlation_matrix: need >= 2 datasets, got "
+                              f"{len(vectors)}")
+    labels = sorted(vectors)
+    n = len(labels)
+    out = np.full((n, n), np.nan)
+    for i in range(n):
+        out[i, i] = 1.0
+        for j in range(i + 1, n):
+            try:
+                r = pearson(vectors[labels[i]], vectors[labels[j]])
+            except UndefinedCorrelationError:
+                continue
+            out[i, j] = out[j, i] = r
+    return CorrelationMatrix(labels, out)
+
+
+def dataset_correlation_matrix(matrix: ActivationMatrix) -> CorrelationMatrix:
+    return dataset_correlation_vectors(sum_rows_by_label(matrix.row_labels,
+                                                         np.asarray(matrix.values)))
+
+
+def prefill_decode_correlation(prefill: ActivationMatrix, decode: ActivationMatrix) -> float:
+    """metrics.cpp:125-132."""
+    if prefill.rows == 0 or decode.rows == 0:
+        raise ValidationError("prefill_decode_correlation: empty matrix")
+    if prefill.cols != decode.cols:
+        raise ValidationError("prefill_decode_correlation: expert count mismatch")
+    a = np.zeros(prefill.cols)
+    for row in np.asarray(prefill.values, np.float64):
+        a = a + row
+    b = np.zeros(decode.cols)
+    for row in np.asarray(decode.values, np.float64):
+        b = b + row
+    return pearson(a, b)

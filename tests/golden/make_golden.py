@@ -11,6 +11,8 @@ Fixtures (all small, committed):
   sim_tokens.npz      token-level simulate_layer cases (idx, src, placement,
                       topology, cost) and the reference LayerSim outputs
   trace_small.jsonl   reference generate_synthetic_trace output (write_trace)
+  trace_analysis.jsonl + analysis.json  emit_analysis outputs (imbalance per
+                      layer/stage, dataset correlation, PD correlation)
   compare_<cfg>.json  full compare_strategies scenarios (inputs + every row
                       + summaries) for configs/qwen3_c1.json and desk_default
   metrics.json        expert_load / imbalance / pearson cases
@@ -134,6 +136,11 @@ def main():
 
     # ---- synthetic trace ----
     R.generate_trace(OUT / "trace_small.jsonl", 3, 6, 16, 0.4, 8.0, 7, 64, 4, 2)
+
+    # a richer trace for the analysis fixture (3 layers, 5 domains: labels sort
+    # lexicographically, PD correlation per layer)
+    R.generate_trace(OUT / "trace_analysis.jsonl", 5, 12, 16, 0.6, 6.0, 11, 64, 2, 3)
+    R.analysis(OUT / "trace_analysis.jsonl", 64, 2, 3, OUT / "analysis.json")
 
     # ---- compare_strategies scenarios ----
     for name in ("qwen3_c1", "desk_default"):

@@ -118,9 +118,13 @@ MPB_API mpb_status mpb_topk_logits(mpb_context *ctx, const float *logits, uint64
  * Tokens t < T carry k expert ids idx[t*k + j]; pair p = t*k + j. Source EP
  * group: src_group[t] (device uint8), or when src_group == NULL,
  * src_base + (t * src_span) / T (contiguous token blocks).
+ * src_group2 (optional) is a second routing of the same tokens (e.g. the
+ * round-robin baseline next to the cluster routing) accounted in the same
+ * pass into demand2.
  * Outputs (device, ACCUMULATED with += so shards/layers can be fused; the
  * caller zeroes them):
  *   demand[D*E]       pairs per (source group, expert)        (uint64)
+ *   demand2[D*E]      same under src_group2 (when given)
  *   tag_pop[n_tags*E] pairs per (tag[t], expert) if tag != NULL (uint64; tag[t]
  *                     uint16, tags >= n_tags are ignored):
  *                     per-domain popularity / per-stage vectors
@@ -137,12 +141,14 @@ typedef struct {
     uint32_t src_span;
     const uint16_t *tag;
     uint32_t n_tags;
+    const uint8_t *src_group2;
 } mpb_tokens;
 
 MPB_API mpb_status mpb_dispatch_layout(mpb_context *ctx, const mpb_tokens *tokens,
                                        const mpb_placement *placement, uint64_t *demand,
-                                       uint64_t *tag_pop, int32_t *sorted_pairs,
-                                       int32_t *pair_pos, int64_t *key_offsets);
+                                       uint64_t *demand2, uint64_t *tag_pop,
+                                       int32_t *sorted_pairs, int32_t *pair_pos,
+                                       int64_t *key_offsets);
 
 /* From demand[D*E] (device): expert_count[E] (column sums), group_pairs[D]
  * (tokens_per_group / per_rank payload in pairs), node_demand[nodes*E],

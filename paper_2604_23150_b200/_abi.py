@@ -25,7 +25,7 @@ _f64p = C.POINTER(C.c_double)
 class MpbTokens(C.Structure):
     _fields_ = [("idx", _p), ("T", C.c_uint64), ("k", C.c_uint32), ("src_group", _p),
                 ("src_base", C.c_uint32), ("src_span", C.c_uint32), ("tag", _p),
-                ("n_tags", C.c_uint32)]
+                ("n_tags", C.c_uint32), ("src_group2", _p)]
 
 
 _SIGS = {
@@ -45,7 +45,7 @@ _SIGS = {
                                   C.c_int, C.c_int, _p, _p, _p]),
     "mpb_topk_logits": (C.c_int, [_p, _p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_int, C.c_int,
                                   _p, _p]),
-    "mpb_dispatch_layout": (C.c_int, [_p, C.POINTER(MpbTokens), _p, _p, _p, _p, _p, _p]),
+    "mpb_dispatch_layout": (C.c_int, [_p, C.POINTER(MpbTokens), _p, _p, _p, _p, _p, _p, _p]),
     "mpb_layout_derive": (C.c_int, [_p, _p, _p, _p, _p, _p, _p]),
     "mpb_coactivation": (C.c_int, [_p, _p, C.c_uint64, C.c_uint32, C.c_uint32, _p]),
     "mpb_sample_batches": (C.c_int, [_p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, _p,

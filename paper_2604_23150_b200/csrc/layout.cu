@@ -7,18 +7,19 @@
 // HBM layout: idx[T*k] int32 (pair p = t*k + j), src_group[T] / tag[T] uint8.
 // Three launches, all streaming idx with coalesced 128-bit loads:
 //   1. count   : per block (2048 pairs) shared-memory-privatised histograms
-//                (demand[src][e], tag_pop[tag][e], slot counts) fed by
-//                warp-aggregated atomics (__match_any_sync + popc leader);
-//                demand / tag flushed with one global atomic per non-zero bin,
-//                slot counts written densely as bhist[block][slot].
-//   2. scan    : one CTA turns bhist into exclusive global offsets
-//                (key-major: slot, then block) and emits key_offsets.
-//   3. scatter : each block re-reads its chunk (L2-resident), ranks pairs
-//                stably inside each warp (match_any + popc of lower lanes),
-//                and writes sorted_pairs / pair_pos.
+//                (demand[src][e], demand2[src2][e] for a second routing of the
+//                same tokens, tag_pop[tag][e]); the block's slot counts are
+//                derived from its demand cells (one add per non-zero cell, not
+//                per pair); bins flushed with one global atomic each, slot
+//                counts written slot-major as bhist[slot][block].
+//   2. scan    : one CTA per slot scans its row of bhist (exclusive, in place)
+//                and writes the slot total.
+//   3. scatter : every block scans the NS slot totals in smem (slot bases; block
+//                0 emits key_offsets), re-reads its chunk (L2-resident), ranks
+//                pairs stably inside each warp (warp-aggregated per-warp
+//                counters, then __match_any_sync + popc of lower lanes) and
+//                writes sorted_pairs / pair_pos.
 // Algorithmic bytes per pair: 4 (idx) + 8 (perm out) [+ 1/k src + 1/k tag].
-#include <cooperative_groups.h>
-
 #include "internal.cuh"
 
 namespace mpb {
@@ -38,14 +39,19 @@ struct LayoutParams {
     uint32_t src_base, src_span;
     const uint16_t *tag;
     uint32_t n_tags;
+    const uint8_t *src2;
     const uint8_t *g2n;
     const uint16_t *slot_lut;
     uint32_t D, E, NS;
     uint64_t *demand;
+    uint64_t *demand2;
     uint64_t *tag_pop;
-    uint32_t *bhist;  // [nblocks][NS]
+    uint32_t *bhist;   // [NS][nblocks] slot-major
+    uint32_t *totals;  // [NS]
+    uint32_t nb;
     uint32_t *err;
     int demand_smem;
+    int demand2_smem;
     int tag_smem;
 };
 
@@ -107,11 +113,13 @@ __device__ __forceinline__ uint32_t resolve(const LayoutParams &p, uint64_t pair
 template <bool kPerm>
 __global__ void __launch_bounds__(kThreads) k_layout_count(LayoutParams p) {
     extern __shared__ uint32_t sm[];
+    const uint32_t DE = p.D * p.E;
     uint32_t *s_demand = sm;
-    uint32_t *s_tag = s_demand + (p.demand_smem ? p.D * p.E : 0);
+    uint32_t *s_demand2 = s_demand + (p.demand_smem ? DE : 0);
+    uint32_t *s_tag = s_demand2 + (p.demand2_smem ? DE : 0);
     uint32_t *s_slot = s_tag + (p.tag_smem ? p.n_tags * p.E : 0);
-    const uint32_t nsm = (p.demand_smem ? p.D * p.E : 0) + (p.tag_smem ? p.n_tags * p.E : 0) +
-                         (kPerm ? p.NS : 0);
+    const uint32_t nsm = (p.demand_smem ? DE : 0) + (p.demand2_smem ? DE : 0) +
+                         (p.tag_smem ? p.n_tags * p.E : 0) + (kPerm ? p.NS : 0);
     for (uint32_t i = threadIdx.x; i < nsm; i += kThreads) sm[i] = 0;
     __syncthreads();
 
@@ -126,73 +134,71 @@ __global__ void __launch_bounds__(kThreads) k_layout_count(LayoutParams p) {
             uint32_t src = 0;
             uint64_t t = 0;
             const uint32_t slot = resolve(p, q + c, v[c], src, t);
-            const bool ok = slot != kNone;
-            const uint32_t dkey = ok ? src * p.E + static_cast<uint32_t>(v[c]) : kNone;
+            if (slot == kNone) continue;
+            const uint32_t e = static_cast<uint32_t>(v[c]);
             if (p.demand_smem) {
-                agg_add(s_demand, dkey);
-            } else if (ok) {
-                atomicAdd(reinterpret_cast<unsigned long long *>(p.demand) + dkey, 1ull);
+                atomicAdd(s_demand + src * p.E + e, 1u);
+            } else {
+                atomicAdd(reinterpret_cast<unsigned long long *>(p.demand) + src * p.E + e, 1ull);
+                if (kPerm) atomicAdd(s_slot + slot, 1u);
             }
-            if (kPerm) agg_add(s_slot, slot);
-            if (p.tag && ok) {
+            if (p.src2) {
+                const uint32_t s2 = p.src2[t];
+                if (s2 >= p.D) {
+                    atomicOr(p.err, kErrSourceRange);
+                } else if (p.demand2_smem) {
+                    atomicAdd(s_demand2 + s2 * p.E + e, 1u);
+                } else {
+                    atomicAdd(reinterpret_cast<unsigned long long *>(p.demand2) + s2 * p.E + e,
+                              1ull);
+                }
+            }
+            if (p.tag) {
                 const uint32_t tg = p.tag[t];
                 if (tg < p.n_tags) {
-                    const uint32_t tkey = tg * p.E + static_cast<uint32_t>(v[c]);
                     if (p.tag_smem)
-                        atomicAdd(s_tag + tkey, 1u);
+                        atomicAdd(s_tag + tg * p.E + e, 1u);
                     else
-                        atomicAdd(reinterpret_cast<unsigned long long *>(p.tag_pop) + tkey, 1ull);
+                        atomicAdd(reinterpret_cast<unsigned long long *>(p.tag_pop) + tg * p.E + e,
+                                  1ull);
                 }
             }
         }
     }
     __syncthreads();
-    if (p.demand_smem)
-        for (uint32_t i = threadIdx.x; i < p.D * p.E; i += kThreads)
-            if (s_demand[i])
-                atomicAdd(reinterpret_cast<unsigned long long *>(p.demand) + i,
-                          static_cast<unsigned long long>(s_demand[i]));
+    if (p.demand_smem) {
+        for (uint32_t i = threadIdx.x; i < DE; i += kThreads) {
+            const uint32_t c = s_demand[i];
+            if (!c) continue;
+            atomicAdd(reinterpret_cast<unsigned long long *>(p.demand) + i,
+                      static_cast<unsigned long long>(c));
+            if (kPerm) {  // the block's slot counts from its (src, expert) cells
+                const uint32_t sg = i / p.E, e = i - sg * p.E;
+                atomicAdd(s_slot + __ldg(p.slot_lut + static_cast<size_t>(p.g2n[sg]) * p.E + e), c);
+            }
+        }
+    }
+    if (p.demand2_smem)
+        for (uint32_t i = threadIdx.x; i < DE; i += kThreads)
+            if (s_demand2[i])
+                atomicAdd(reinterpret_cast<unsigned long long *>(p.demand2) + i,
+                          static_cast<unsigned long long>(s_demand2[i]));
     if (p.tag && p.tag_smem)
         for (uint32_t i = threadIdx.x; i < p.n_tags * p.E; i += kThreads)
             if (s_tag[i])
                 atomicAdd(reinterpret_cast<unsigned long long *>(p.tag_pop) + i,
                           static_cast<unsigned long long>(s_tag[i]));
-    if (kPerm)
-        for (uint32_t s = threadIdx.x; s < p.NS; s += kThreads)
-            p.bhist[static_cast<size_t>(blockIdx.x) * p.NS + s] = s_slot[s];
+    if (kPerm) {
+        __syncthreads();
+        for (uint32_t sl = threadIdx.x; sl < p.NS; sl += kThreads)
+            p.bhist[static_cast<size_t>(sl) * p.nb + blockIdx.x] = s_slot[sl];
+    }
 }
 
-// Exclusive offsets over (slot, block), slot-major: the position of block b's
-// first pair with slot s. One CTA; thread (s, c) owns slot s over a
-// contiguous run of blocks (independent, unrolled loads), then a block-wide
-// scan over (slot, chunk) totals. Also emits key_offsets[d*E+e] via key_lb.
-constexpr int kScanThreads = 1024;
-
-__global__ void __launch_bounds__(kScanThreads) k_layout_scan(uint32_t *bhist, uint32_t nb,
-                                                              uint32_t NS, const uint16_t *key_lb,
-                                                              uint32_t nkeys, int64_t *key_offsets) {
-    extern __shared__ uint32_t s_tot[];  // [NS * chunks + 1]
-    __shared__ uint32_t s_warp[32];
-    const uint32_t chunks = max(1u, kScanThreads / NS);
-    const uint32_t per = (nb + chunks - 1) / chunks;
-    const uint32_t cells = NS * chunks;
-    // pass 1: chunk totals, cell id = s * chunks + c (slot-major order)
-    for (uint32_t cell = threadIdx.x; cell < cells; cell += kScanThreads) {
-        const uint32_t sl = cell / chunks, c = cell % chunks;
-        const uint32_t b0 = min(nb, c * per), b1 = min(nb, b0 + per);
-        uint32_t sum = 0;
-#pragma unroll 8
-        for (uint32_t b = b0; b < b1; ++b) sum += bhist[static_cast<size_t>(b) * NS + sl];
-        s_tot[cell] = sum;
-    }
-    __syncthreads();
-    // pass 2: exclusive scan of s_tot[0..cells) — per-thread segments + warp scans
-    const uint32_t seg = (cells + kScanThreads - 1) / kScanThreads;
-    const uint32_t lo = min(cells, threadIdx.x * seg), hi = min(cells, lo + seg);
-    uint32_t local = 0;
-    for (uint32_t i = lo; i < hi; ++i) local += s_tot[i];
+// Block-wide exclusive scan of one value per thread (kThreads threads).
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t *s_warp, uint32_t &total) {
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint32_t incl = local;
+    uint32_t incl = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
         const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
@@ -201,49 +207,66 @@ __global__ void __launch_bounds__(kScanThreads) k_layout_scan(uint32_t *bhist, u
     if (lane == 31) s_warp[warp] = incl;
     __syncthreads();
     if (warp == 0) {
-        uint32_t w = s_warp[lane];
+        uint32_t w = lane < kWarps ? s_warp[lane] : 0;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
             if (lane >= o) w += y;
         }
-        s_warp[lane] = w;  // inclusive
+        if (lane < kWarps) s_warp[lane] = w;
     }
     __syncthreads();
-    uint32_t run = (warp ? s_warp[warp - 1] : 0) + incl - local;
-    const uint32_t grand = s_warp[31];
-    for (uint32_t i = lo; i < hi; ++i) {
-        const uint32_t v = s_tot[i];
-        s_tot[i] = run;
-        run += v;
-    }
-    if (threadIdx.x == 0) s_tot[cells] = grand;
+    total = s_warp[kWarps - 1];
+    const uint32_t r = (warp ? s_warp[warp - 1] : 0) + incl - v;
     __syncthreads();
-    // pass 3: rewrite bhist with global offsets
-    for (uint32_t cell = threadIdx.x; cell < cells; cell += kScanThreads) {
-        const uint32_t sl = cell / chunks, c = cell % chunks;
-        const uint32_t b0 = min(nb, c * per), b1 = min(nb, b0 + per);
-        uint32_t r = s_tot[cell];
-        for (uint32_t b = b0; b < b1; ++b) {
-            const size_t i = static_cast<size_t>(b) * NS + sl;
-            const uint32_t v = bhist[i];
-            bhist[i] = r;
-            r += v;
-        }
+    return r;
+}
+
+// One CTA per slot: exclusive scan of bhist[slot][0..nb) in place + total.
+__global__ void __launch_bounds__(kThreads) k_layout_scan(uint32_t *bhist, uint32_t nb,
+                                                          uint32_t *totals) {
+    __shared__ uint32_t s_warp[32];
+    uint32_t *row = bhist + static_cast<size_t>(blockIdx.x) * nb;
+    uint32_t carry = 0;
+    for (uint32_t i0 = 0; i0 < nb; i0 += kThreads) {
+        const uint32_t i = i0 + threadIdx.x;
+        const uint32_t v = i < nb ? row[i] : 0;
+        uint32_t tot;
+        const uint32_t ex = block_excl_scan(v, s_warp, tot);
+        if (i < nb) row[i] = carry + ex;
+        carry += tot;
     }
-    if (key_offsets)
-        for (uint32_t key = threadIdx.x; key <= nkeys; key += kScanThreads) {
-            const uint32_t sl = key_lb[key];
-            key_offsets[key] = static_cast<int64_t>(sl < NS ? s_tot[sl * chunks] : grand);
-        }
+    if (threadIdx.x == 0) totals[blockIdx.x] = carry;
 }
 
 __global__ void __launch_bounds__(kThreads) k_layout_scatter(LayoutParams p, int32_t *sorted_pairs,
-                                                             int32_t *pair_pos) {
-    extern __shared__ uint32_t s_w[];  // [kWarps][NS] running positions
+                                                             int32_t *pair_pos,
+                                                             const uint16_t *key_lb,
+                                                             uint32_t nkeys,
+                                                             int64_t *key_offsets) {
+    extern __shared__ uint32_t s_w[];  // [kWarps][NS] running positions, then [NS+1] bases
+    __shared__ uint32_t s_warp[32];
+    uint32_t *s_base = s_w + kWarps * p.NS;
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (uint32_t i = threadIdx.x; i < kWarps * p.NS; i += kThreads) s_w[i] = 0;
+    // slot bases: exclusive scan of the slot totals (every block; NS is small)
+    {
+        const uint32_t per = (p.NS + kThreads - 1) / kThreads;
+        const uint32_t lo = min(p.NS, threadIdx.x * per), hi = min(p.NS, lo + per);
+        uint32_t local = 0;
+        for (uint32_t i = lo; i < hi; ++i) local += p.totals[i];
+        uint32_t grand;
+        uint32_t run = block_excl_scan(local, s_warp, grand);
+        for (uint32_t i = lo; i < hi; ++i) {
+            s_base[i] = run;
+            run += p.totals[i];
+        }
+        if (threadIdx.x == 0) s_base[p.NS] = grand;
+    }
     __syncthreads();
+    if (blockIdx.x == 0 && key_offsets)
+        for (uint32_t key = threadIdx.x; key <= nkeys; key += kThreads)
+            key_offsets[key] = static_cast<int64_t>(s_base[key_lb[key]]);
 
     // each warp owns 256 consecutive pairs: two 128-bit loads per lane
     const uint64_t wbase = static_cast<uint64_t>(blockIdx.x) * kChunk + warp * 256ull;
@@ -276,7 +299,7 @@ __global__ void __launch_bounds__(kThreads) k_layout_scatter(LayoutParams p, int
     __syncthreads();
     // per slot: exclusive prefix over warps, seeded with the block's global offset
     for (uint32_t s = threadIdx.x; s < p.NS; s += kThreads) {
-        uint32_t run = p.bhist[static_cast<size_t>(blockIdx.x) * p.NS + s];
+        uint32_t run = s_base[s] + p.bhist[static_cast<size_t>(s) * p.nb + blockIdx.x];
 #pragma unroll
         for (int w = 0; w < kWarps; ++w) {
             const uint32_t c = s_w[w * p.NS + s];
@@ -363,8 +386,8 @@ constexpr size_t kSmemLimit = 160 * 1024;
 }  // namespace
 
 mpb_status launch_layout(mpb_context *ctx, const mpb_tokens *tk, const mpb_placement *pl,
-                         uint64_t *demand, uint64_t *tag_pop, int32_t *sorted_pairs,
-                         int32_t *pair_pos, int64_t *key_offsets) {
+                         uint64_t *demand, uint64_t *demand2, uint64_t *tag_pop,
+                         int32_t *sorted_pairs, int32_t *pair_pos, int64_t *key_offsets) {
     // the permutation is requested through key_offsets (never empty: D*E+1
     // entries); sorted_pairs / pair_pos may be NULL only when T*k == 0
     const bool perm = key_offsets != nullptr;
@@ -372,21 +395,21 @@ mpb_status launch_layout(mpb_context *ctx, const mpb_tokens *tk, const mpb_place
         return fail(MPB_VALIDATION_ERROR,
                     "mpb_dispatch_layout: sorted_pairs, pair_pos and key_offsets go together");
     if (!demand) return fail(MPB_VALIDATION_ERROR, "mpb_dispatch_layout: demand is NULL");
+    if (tk->src_group2 && !demand2)
+        return fail(MPB_VALIDATION_ERROR, "mpb_dispatch_layout: src_group2 given without demand2");
     if (tk->k == 0) return fail(MPB_CONFIG_ERROR, "mpb_dispatch_layout: k must be >= 1");
     if (tk->tag && !tag_pop)
         return fail(MPB_VALIDATION_ERROR, "mpb_dispatch_layout: tag given without tag_pop");
     const uint64_t P = tk->T * tk->k;
     if (P > 0x7fffffffull)
         return fail(MPB_CONFIG_ERROR, "mpb_dispatch_layout: T*k must fit int32 pair ids");
-    if (perm && pl->NS * kWarps * 4 > kSmemLimit)
+    if (perm && (size_t(pl->NS) * kWarps + pl->NS + 1) * 4 > kSmemLimit)
         return fail(MPB_CONFIG_ERROR, "mpb_dispatch_layout: too many (group, expert) slots "
                                       "for the permutation");
     if (P == 0) {
-        if (perm) {
-            // every offset is zero
+        if (perm)  // every offset is zero
             MPB_CUDA(cudaMemsetAsync(key_offsets, 0, sizeof(int64_t) * (size_t(pl->D) * pl->E + 1),
                                      ctx->stream));
-        }
         return MPB_OK;
     }
     LayoutParams p{};
@@ -399,46 +422,44 @@ mpb_status launch_layout(mpb_context *ctx, const mpb_tokens *tk, const mpb_place
     p.src_span = tk->src_span;
     p.tag = tk->tag;
     p.n_tags = tk->tag ? tk->n_tags : 0;
+    p.src2 = tk->src_group2;
     p.g2n = pl->d_g2n;
     p.slot_lut = pl->d_slot_lut;
     p.D = pl->D;
     p.E = pl->E;
     p.NS = pl->NS;
     p.demand = demand;
+    p.demand2 = demand2;
     p.tag_pop = tag_pop;
     p.err = ctx->d_error;
+    const size_t DE4 = size_t(pl->D) * pl->E * 4;
     size_t smem = perm ? size_t(pl->NS) * 4 : 0;
-    p.demand_smem = smem + size_t(pl->D) * pl->E * 4 <= kSmemLimit;
-    if (p.demand_smem) smem += size_t(pl->D) * pl->E * 4;
+    p.demand_smem = smem + DE4 <= kSmemLimit;
+    if (p.demand_smem) smem += DE4;
+    p.demand2_smem = p.src2 && smem + DE4 <= kSmemLimit;
+    if (p.demand2_smem) smem += DE4;
     p.tag_smem = p.n_tags && smem + size_t(p.n_tags) * pl->E * 4 <= kSmemLimit;
     if (p.tag_smem) smem += size_t(p.n_tags) * pl->E * 4;
     const uint32_t nb = static_cast<uint32_t>((P + kChunk - 1) / kChunk);
+    p.nb = nb;
     if (perm) {
-        MPB_CUDA(ctx->ensure_scratch(size_t(nb) * pl->NS * 4));
+        MPB_CUDA(ctx->ensure_scratch((size_t(nb) + 1) * pl->NS * 4 + 256));
         p.bhist = static_cast<uint32_t *>(ctx->scratch);
+        p.totals = p.bhist + size_t(nb) * pl->NS;
     }
-    if (perm) {
-        MPB_CUDA(cudaFuncSetAttribute(k_layout_count<true>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-        k_layout_count<true><<<nb, kThreads, smem, ctx->stream>>>(p);
-    } else {
-        MPB_CUDA(cudaFuncSetAttribute(k_layout_count<false>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-        k_layout_count<false><<<nb, kThreads, smem, ctx->stream>>>(p);
-    }
+    auto count = perm ? k_layout_count<true> : k_layout_count<false>;
+    MPB_CUDA(cudaFuncSetAttribute(count, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    count<<<nb, kThreads, smem, ctx->stream>>>(p);
     MPB_LAUNCHED(ctx);
     if (!perm) return MPB_OK;
-    const size_t chunks = std::max<size_t>(1, kScanThreads / pl->NS);
-    const size_t scan_smem = (size_t(pl->NS) * chunks + 1) * 4;
-    MPB_CUDA(cudaFuncSetAttribute(k_layout_scan, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  int(scan_smem)));
-    k_layout_scan<<<1, kScanThreads, scan_smem, ctx->stream>>>(p.bhist, nb, pl->NS, pl->d_key_lb,
-                                                               pl->D * pl->E, key_offsets);
+    k_layout_scan<<<pl->NS, kThreads, 0, ctx->stream>>>(p.bhist, nb, p.totals);
     MPB_LAUNCHED(ctx);
-    const size_t sc_smem = size_t(kWarps) * pl->NS * 4;
+    const size_t sc_smem = (size_t(kWarps) * pl->NS + pl->NS + 1) * 4;
     MPB_CUDA(cudaFuncSetAttribute(k_layout_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(sc_smem)));
-    k_layout_scatter<<<nb, kThreads, sc_smem, ctx->stream>>>(p, sorted_pairs, pair_pos);
+    k_layout_scatter<<<nb, kThreads, sc_smem, ctx->stream>>>(p, sorted_pairs, pair_pos,
+                                                             pl->d_key_lb, pl->D * pl->E,
+                                                             key_offsets);
     MPB_LAUNCHED(ctx);
     return MPB_OK;
 }
@@ -462,15 +483,15 @@ extern "C" {
 
 mpb_status mpb_dispatch_layout(mpb_context *ctx, const mpb_tokens *tokens,
                                const mpb_placement *placement, uint64_t *demand,
-                               uint64_t *tag_pop, int32_t *sorted_pairs, int32_t *pair_pos,
-                               int64_t *key_offsets) {
+                               uint64_t *demand2, uint64_t *tag_pop, int32_t *sorted_pairs,
+                               int32_t *pair_pos, int64_t *key_offsets) {
     if (!ctx || !tokens || !placement)
         return fail(MPB_VALIDATION_ERROR, "mpb_dispatch_layout: NULL argument");
     if (tokens->T && !tokens->idx)
         return fail(MPB_VALIDATION_ERROR, "mpb_dispatch_layout: idx is NULL");
     if (!tokens->src_group && tokens->src_span == 0 && tokens->T)
         return fail(MPB_CONFIG_ERROR, "mpb_dispatch_layout: src_group NULL needs src_span >= 1");
-    return launch_layout(ctx, tokens, placement, demand, tag_pop, sorted_pairs, pair_pos,
+    return launch_layout(ctx, tokens, placement, demand, demand2, tag_pop, sorted_pairs, pair_pos,
                          key_offsets);
 }
 

@@ -349,15 +349,19 @@ class Engine:
                         src: Optional[torch.Tensor] = None, src_base: int = 0,
                         src_span: int = 0, tag: Optional[torch.Tensor] = None,
                         n_tags: int = 0, permutation: bool = True, demand=None, tag_pop=None,
-                        perm_out=None):
+                        perm_out=None, src2: Optional[torch.Tensor] = None, demand2=None):
+        """src2/demand2: a second routing of the same tokens accounted in the
+        same pass (e.g. the round-robin baseline next to the cluster routing)."""
         T, k = idx.shape
         if demand is None:
             demand = self._u64(dp.D, dp.E)
+        if src2 is not None and demand2 is None:
+            demand2 = self._u64(dp.D, dp.E)
         if tag is not None and tag_pop is None:
             tag_pop = self._u64(n_tags, dp.E)
         tk = _abi.MpbTokens(idx.data_ptr(), T, k, src.data_ptr() if src is not None else None,
                             src_base, src_span, tag.data_ptr() if tag is not None else None,
-                            n_tags)
+                            n_tags, src2.data_ptr() if src2 is not None else None)
         sp = pp = ko = None
         if permutation:
             if perm_out is not None:
@@ -367,9 +371,9 @@ class Engine:
                 pp = torch.empty(T * k, dtype=torch.int32, device=self.device)
                 ko = torch.empty(dp.D * dp.E + 1, dtype=torch.int64, device=self.device)
         _abi.call("mpb_dispatch_layout", self.ctx, C.byref(tk), dp.handle, _ptr(demand),
-                  _ptr(tag_pop), _ptr(sp), _ptr(pp), _ptr(ko))
-        return dict(demand=demand, tag_pop=tag_pop, sorted_pairs=sp, pair_pos=pp,
-                    key_offsets=ko)
+                  _ptr(demand2), _ptr(tag_pop), _ptr(sp), _ptr(pp), _ptr(ko))
+        return dict(demand=demand, demand2=demand2, tag_pop=tag_pop, sorted_pairs=sp,
+                    pair_pos=pp, key_offsets=ko)
 
     def layout_derive(self, dp: DevicePlacement, demand: torch.Tensor, out=None):
         if out is None:

@@ -259,11 +259,12 @@ class RoutingPipeline:
         if timed_router:
             e1.record(eng.stream)
             self.router_events.append((e0, e1))
+        # deployed (cluster-routed) layout + permutation, with the round-robin
+        # baseline's demand accounted in the same pass
         eng.dispatch_layout(self.idx, self.dp_deployed, src=self.src_cl, tag=self.dom_tok,
                             n_tags=s.domains, demand=self.dem_cl[l], tag_pop=self.pop,
-                            perm_out=(self.sp, self.pp, self.ko))
-        eng.dispatch_layout(self.idx, self.dp_deployed, src=self.src_rr, permutation=False,
-                            demand=self.dem_rr[l])
+                            perm_out=(self.sp, self.pp, self.ko), src2=self.src_rr,
+                            demand2=self.dem_rr[l])
         if s.coact:
             eng.coactivation(self.idx, s.experts, out=self.coact)
 

@@ -16,6 +16,9 @@ BUILD = ROOT / "paper_2604_23150_b200" / "shim" / "build"
 
 @pytest.mark.parametrize("binary", ["shim_unit_tests", "shim_acceptance"])
 def test_reference_suites_through_b200_shim(binary):
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
     exe = BUILD / binary
     if not exe.exists():
         pytest.skip(f"{exe} not built (make -C paper_2604_23150_b200/shim tests)")

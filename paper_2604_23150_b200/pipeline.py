@@ -94,19 +94,26 @@ class SyntheticModel:
         # domain bias per layer: boost * sum of the preferred experts' router rows
         self.bias = [spec.boost * w.float()[self.pref].sum(1) for w in self.W]  # [dom, H] fp32
 
+    def _seed_rank(self, draw: int) -> int:
+        # the calibration draw (1) is the same on every rank, so all ranks learn
+        # the same placement; measurement draws are per rank (token shards)
+        return 0 if draw == 1 else self.rank
+
     def requests(self, draw: int):
         """Request domains and token -> request map for one draw (calibration
         draw = 1, measurement draw = 0)."""
         s = self.spec
         R = s.tokens // s.tokens_per_request
-        dom = _lcg_domains(R, s.domains, 7919 * (self.rank + 1) + 104729 * draw + s.seed)
+        dom = _lcg_domains(R, s.domains,
+                           7919 * (self._seed_rank(draw) + 1) + 104729 * draw + s.seed)
         return R, dom
 
     def fill_hidden(self, X: torch.Tensor, layer: int, draw: int, dom_tok: torch.Tensor,
                     chunk: int = 16384):
         s = self.spec
         g = torch.Generator(device=self.device).manual_seed(
-            (draw * 1_000_003 + layer * 7_919 + self.rank * 104_729 + s.seed) & 0x7FFFFFFF)
+            (draw * 1_000_003 + layer * 7_919 + self._seed_rank(draw) * 104_729 + s.seed)
+            & 0x7FFFFFFF)
         for t0 in range(0, s.tokens, chunk):
             t1 = min(s.tokens, t0 + chunk)
             z = torch.randn(t1 - t0, s.hidden, device=self.device, generator=g)

@@ -9,7 +9,9 @@
 // synthetically, /root/reference/proj/core/src/trace.cpp:240-259); selection
 // follows its lowest-index-wins tie rule (placement.cpp:143-152).
 //
-// Persistent, warp-specialised CTA (one per SM, 256 threads):
+// Persistent, warp-specialised CTA (one per SM, 384 threads); for E = 256 the
+// default is a 2-CTA cluster per 256-token tile with cta_group::2 UMMA (see
+// k_router's PAIR mode):
 //   warp 0     TMA producer: X tile [128 x 64] (evict-first) + W tile [N x 64]
 //              (evict-last, L2-resident across CTAs) per k-block into a
 //              STAGES-deep 128B-swizzled smem ring (mbarrier full/empty)
@@ -24,6 +26,7 @@
 #include <cudaTypedefs.h>
 
 #include <cfloat>
+#include <cstdlib>
 #include <mutex>
 
 #include "internal.cuh"
@@ -36,12 +39,13 @@ constexpr int kBM = 128;
 constexpr int kBK = 64;  // 64 bf16 = 128 bytes: one 128B swizzle atom per row
 constexpr int kThreadsR = 384;  // 4 non-epilogue + 8 epilogue warps
 
-template <int N, int KMAX>
+template <int N, int KMAX, bool PAIR>
 struct RCfg {
     static constexpr int A_BYTES = kBM * kBK * 2;
-    static constexpr int B_BYTES = N * kBK * 2;
+    static constexpr int B_BYTES = (PAIR ? N / 2 : N) * kBK * 2;  // pair: this CTA's half of W
     static constexpr int STAGE = A_BYTES + B_BYTES;
     static constexpr uint32_t TMEM_COLS = 2 * N < 32 ? 32 : 2 * N;
+    static constexpr int ROWS_PER_TILE = PAIR ? 2 * kBM : kBM;
     // per epilogue thread: 16 parked logits, later its half's top-k (values,
     // ids) + max + sum for the merge; odd stride keeps banks conflict-free
     static constexpr int PARK_ROW = (2 * KMAX + 2 > 16 ? 2 * KMAX + 2 : 16) | 1;
@@ -73,11 +77,36 @@ __device__ __forceinline__ bool sel_beats(float a, int ia, float b, int ib) {
     return ia < ib;
 }
 
-template <int N, int KMAX>
+// Hands an accumulator's TMEM back to the MMA issuer after this thread's
+// tcgen05.ld reads: single CTA — every epilogue thread arrives; pair — one lane
+// per warp arrives on the LEADER's barrier (locally or through DSMEM).
+template <bool PAIR>
+__device__ __forceinline__ void release_tmem(uint64_t *bar, uint32_t rank, uint32_t lane) {
+    ptx::tc_fence_before();
+    if constexpr (PAIR) {
+        __syncwarp();
+        if (lane == 0) {
+            if (rank == 0)
+                ptx::mbar_arrive(bar);
+            else
+                ptx::mbar_arrive_remote(ptx::mapa(ptx::smem_u32(bar), 0));
+        }
+    } else {
+        ptx::mbar_arrive(bar);
+    }
+}
+
+// PAIR = false: one CTA per 128-token tile, UMMA M=128 x N (cta_group::1).
+// PAIR = true : a 2-CTA cluster per 256-token tile, UMMA M=256 x N issued by the
+//   leader with cta_group::2 — each CTA stages its own 128 X rows and HALF of
+//   W's rows; the tensor cores read the peer's operands across the SM pair, so
+//   W's L2->SM traffic per FLOP halves. Each CTA's TMEM holds full 256-expert
+//   rows for its 128 tokens, so the top-k epilogue stays CTA-local.
+template <int N, int KMAX, bool PAIR>
 __global__ void __launch_bounds__(kThreadsR, 1)
     k_router(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
              RouterParams p) {
-    using Cfg = RCfg<N, KMAX>;
+    using Cfg = RCfg<N, KMAX, PAIR>;
     constexpr int S = Cfg::STAGES;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *base = reinterpret_cast<uint8_t *>(
@@ -92,6 +121,9 @@ __global__ void __launch_bounds__(kThreadsR, 1)
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
 
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = PAIR ? ptx::cluster_ctarank() : 0u;
+    const uint32_t unit = PAIR ? blockIdx.x >> 1 : blockIdx.x;     // tile-scheduling unit
+    const uint32_t units = PAIR ? gridDim.x >> 1 : gridDim.x;
     if (warp == 0 && lane == 0) {
         ptx::tma_prefetch_desc(&tmX);
         ptx::tma_prefetch_desc(&tmW);
@@ -101,13 +133,23 @@ __global__ void __launch_bounds__(kThreadsR, 1)
         }
         for (int a = 0; a < 2; ++a) {
             ptx::mbar_init(&tfull[a], 1);
-            ptx::mbar_init(&tempty[a], 256);
+            // single: every epilogue thread arrives; pair: one lane per epilogue
+            // warp of both CTAs arrives on the leader's barrier
+            ptx::mbar_init(&tempty[a], PAIR ? 16 : 256);
         }
         ptx::fence_barrier_init();
     }
-    if (warp == 2) ptx::tmem_alloc<Cfg::TMEM_COLS>(tmem_slot);
+    if (warp == 2) {
+        if constexpr (PAIR)
+            ptx::tmem_alloc_2sm<Cfg::TMEM_COLS>(tmem_slot);
+        else
+            ptx::tmem_alloc<Cfg::TMEM_COLS>(tmem_slot);
+    }
     ptx::tc_fence_before();
-    __syncthreads();
+    if constexpr (PAIR)
+        ptx::cluster_sync();
+    else
+        __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     const uint32_t nk = p.H / kBK;
@@ -118,27 +160,37 @@ __global__ void __launch_bounds__(kThreadsR, 1)
         const uint64_t pol_w = ptx::policy_evict_last();
         int stage = 0;
         uint32_t phase = 0;
-        for (uint32_t tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
-            const int32_t m0 = static_cast<int32_t>(tile * kBM);
+        for (uint32_t tile = unit; tile < p.num_tiles; tile += units) {
+            const int32_t m0 = static_cast<int32_t>(tile * Cfg::ROWS_PER_TILE + rank * kBM);
             for (uint32_t kb = 0; kb < nk; ++kb) {
                 ptx::mbar_wait(&empty[stage], phase ^ 1);
-                ptx::mbar_arrive_expect_tx(&full[stage], Cfg::STAGE);
-                ptx::tma_load_2d(&tmX, &full[stage], sA + stage * Cfg::A_BYTES, kb * kBK, m0,
-                                 pol_x);
-                ptx::tma_load_2d(&tmW, &full[stage], sB + stage * Cfg::B_BYTES, kb * kBK, 0,
-                                 pol_w);
+                if constexpr (PAIR) {
+                    // both CTAs' loads complete on the leader's full barrier
+                    if (rank == 0) ptx::mbar_arrive_expect_tx(&full[stage], 2 * Cfg::STAGE);
+                    const uint32_t bar = ptx::mapa(ptx::smem_u32(&full[stage]), 0);
+                    ptx::tma_load_2d_2sm(&tmX, bar, sA + stage * Cfg::A_BYTES, kb * kBK, m0,
+                                         pol_x);
+                    ptx::tma_load_2d_2sm(&tmW, bar, sB + stage * Cfg::B_BYTES, kb * kBK,
+                                         static_cast<int32_t>(rank) * (N / 2), pol_w);
+                } else {
+                    ptx::mbar_arrive_expect_tx(&full[stage], Cfg::STAGE);
+                    ptx::tma_load_2d(&tmX, &full[stage], sA + stage * Cfg::A_BYTES, kb * kBK, m0,
+                                     pol_x);
+                    ptx::tma_load_2d(&tmW, &full[stage], sB + stage * Cfg::B_BYTES, kb * kBK, 0,
+                                     pol_w);
+                }
                 if (++stage == S) {
                     stage = 0;
                     phase ^= 1;
                 }
             }
         }
-    } else if (warp == 1 && lane == 0) {
-        // ---------------- MMA issuer ----------------
-        constexpr uint32_t idesc = ptx::idesc_bf16_f32<kBM, N>();
+    } else if (warp == 1 && lane == 0 && rank == 0) {
+        // ---------------- MMA issuer (pair: leader CTA only) ----------------
+        constexpr uint32_t idesc = ptx::idesc_bf16_f32<PAIR ? 2 * kBM : kBM, N>();
         int stage = 0;
         uint32_t phase = 0, acc = 0, aphase = 0;
-        for (uint32_t tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+        for (uint32_t tile = unit; tile < p.num_tiles; tile += units) {
             ptx::mbar_wait(&tempty[acc], aphase ^ 1);
             ptx::tc_fence_after();
             const uint32_t d = tmem_base + acc * N;
@@ -148,15 +200,25 @@ __global__ void __launch_bounds__(kThreadsR, 1)
                 const uint64_t ad = ptx::sw128_kmajor_desc(ptx::smem_u32(sA + stage * Cfg::A_BYTES));
                 const uint64_t bd = ptx::sw128_kmajor_desc(ptx::smem_u32(sB + stage * Cfg::B_BYTES));
 #pragma unroll
-                for (int kk = 0; kk < kBK / 16; ++kk)  // +32 bytes along K per UMMA_K = 16
-                    ptx::mma_bf16(d, ad + 2 * kk, bd + 2 * kk, idesc, (kb | kk) != 0);
-                ptx::mma_commit(&empty[stage]);
+                for (int kk = 0; kk < kBK / 16; ++kk) {  // +32 bytes along K per UMMA_K = 16
+                    if constexpr (PAIR)
+                        ptx::mma_bf16_2sm(d, ad + 2 * kk, bd + 2 * kk, idesc, (kb | kk) != 0);
+                    else
+                        ptx::mma_bf16(d, ad + 2 * kk, bd + 2 * kk, idesc, (kb | kk) != 0);
+                }
+                if constexpr (PAIR)
+                    ptx::mma_commit_2sm_mc(&empty[stage], 0x3);  // frees the stage in both CTAs
+                else
+                    ptx::mma_commit(&empty[stage]);
                 if (++stage == S) {
                     stage = 0;
                     phase ^= 1;
                 }
             }
-            ptx::mma_commit(&tfull[acc]);
+            if constexpr (PAIR)
+                ptx::mma_commit_2sm_mc(&tfull[acc], 0x3);
+            else
+                ptx::mma_commit(&tfull[acc]);
             acc ^= 1;
             if (acc == 0) aphase ^= 1;
         }
@@ -179,10 +241,11 @@ __global__ void __launch_bounds__(kThreadsR, 1)
         constexpr int NH = N / 2;
         const int off = KMAX - static_cast<int>(p.k);
         uint32_t acc = 0, aphase = 0;
-        for (uint32_t tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+        for (uint32_t tile = unit; tile < p.num_tiles; tile += units) {
             ptx::mbar_wait(&tfull[acc], aphase);
             ptx::tc_fence_after();
-            const uint64_t row = static_cast<uint64_t>(tile) * kBM + row_in_tile;
+            const uint64_t row =
+                static_cast<uint64_t>(tile) * Cfg::ROWS_PER_TILE + rank * kBM + row_in_tile;
             const uint32_t taddr = tmem_base + acc * N + ((q * 32) << 16);
             float tv[KMAX];
             int ti[KMAX];
@@ -260,8 +323,7 @@ __global__ void __launch_bounds__(kThreadsR, 1)
             }
             asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
             if (half == 1) {
-                ptx::tc_fence_before();
-                ptx::mbar_arrive(&tempty[acc]);
+                release_tmem<PAIR>(&tempty[acc], rank, lane);
             } else {
 #pragma unroll 1
                 for (int jj = off; jj < KMAX; ++jj) {
@@ -310,8 +372,7 @@ __global__ void __launch_bounds__(kThreadsR, 1)
                             }
                         }
                 }
-                ptx::tc_fence_before();
-                ptx::mbar_arrive(&tempty[acc]);
+                release_tmem<PAIR>(&tempty[acc], rank, lane);
                 if (row < p.T) {
                     const float mlog = m * 1.4426950408889634f;
                     float w[KMAX];
@@ -345,10 +406,16 @@ __global__ void __launch_bounds__(kThreadsR, 1)
         }
     }
     ptx::tc_fence_before();
-    __syncthreads();
+    if constexpr (PAIR)
+        ptx::cluster_sync();
+    else
+        __syncthreads();
     if (warp == 2) {
         ptx::tc_fence_after();
-        ptx::tmem_dealloc<Cfg::TMEM_COLS>(tmem_base);
+        if constexpr (PAIR)
+            ptx::tmem_dealloc_2sm<Cfg::TMEM_COLS>(tmem_base);
+        else
+            ptx::tmem_dealloc<Cfg::TMEM_COLS>(tmem_base);
     }
 }
 
@@ -379,26 +446,44 @@ bool make_map(CUtensorMap *map, const void *ptr, uint64_t rows, uint64_t cols, u
     return r == CUDA_SUCCESS;
 }
 
-template <int N, int KMAX>
+template <int N, int KMAX, bool PAIR>
 mpb_status launch_router_n(mpb_context *ctx, const CUtensorMap &mx, const CUtensorMap &mw,
-                           const RouterParams &p) {
-    constexpr int smem = RCfg<N, KMAX>::SMEM;
-    auto kern = k_router<N, KMAX>;
+                           RouterParams p) {
+    constexpr int smem = RCfg<N, KMAX, PAIR>::SMEM;
+    auto kern = k_router<N, KMAX, PAIR>;
     MPB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    const uint32_t grid = std::min<uint32_t>(p.num_tiles, static_cast<uint32_t>(ctx->num_sms));
-    kern<<<grid, kThreadsR, smem, ctx->stream>>>(mx, mw, p);
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute attr[1];
+    cfg.blockDim = dim3(kThreadsR);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = ctx->stream;
+    if constexpr (PAIR) {
+        p.num_tiles = static_cast<uint32_t>((p.T + 2 * kBM - 1) / (2 * kBM));
+        const uint32_t pairs =
+            std::min<uint32_t>(p.num_tiles, static_cast<uint32_t>(ctx->num_sms) / 2);
+        cfg.gridDim = dim3(2 * pairs);
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+    } else {
+        cfg.gridDim = dim3(std::min<uint32_t>(p.num_tiles, static_cast<uint32_t>(ctx->num_sms)));
+    }
+    MPB_CUDA(cudaLaunchKernelEx(&cfg, kern, mx, mw, p));
     MPB_LAUNCHED(ctx);
     return MPB_OK;
 }
 
-template <int N>
+template <int N, bool PAIR>
 mpb_status launch_router_k(mpb_context *ctx, const CUtensorMap &mx, const CUtensorMap &mw,
                            const RouterParams &p) {
-    if (p.k <= 1) return launch_router_n<N, 1>(ctx, mx, mw, p);
-    if (p.k <= 2) return launch_router_n<N, 2>(ctx, mx, mw, p);
-    if (p.k <= 4) return launch_router_n<N, 4>(ctx, mx, mw, p);
-    if (p.k <= 8) return launch_router_n<N, 8>(ctx, mx, mw, p);
-    return launch_router_n<N, 16>(ctx, mx, mw, p);
+    if (p.k <= 1) return launch_router_n<N, 1, PAIR>(ctx, mx, mw, p);
+    if (p.k <= 2) return launch_router_n<N, 2, PAIR>(ctx, mx, mw, p);
+    if (p.k <= 4) return launch_router_n<N, 4, PAIR>(ctx, mx, mw, p);
+    if (p.k <= 8) return launch_router_n<N, 8, PAIR>(ctx, mx, mw, p);
+    return launch_router_n<N, 16, PAIR>(ctx, mx, mw, p);
 }
 
 }  // namespace
@@ -421,13 +506,21 @@ extern "C" mpb_status mpb_router_topk(mpb_context *ctx, const void *X, const voi
         return fail(MPB_CONFIG_ERROR, "mpb_router_topk: X and W must be 16-byte aligned");
     if (T == 0) return MPB_OK;
     if (T > 0x7fffffffull) return fail(MPB_CONFIG_ERROR, "mpb_router_topk: T too large");
-    CUtensorMap mx, mw;
-    const uint32_t box_n = E;
-    if (!make_map(&mx, X, T, H, kBM) || !make_map(&mw, W, E, H, box_n))
-        return fail(MPB_CUDA_ERROR, "mpb_router_topk: cuTensorMapEncodeTiled failed");
     RouterParams p{T, H, k, score_fn, renorm, static_cast<uint32_t>((T + kBM - 1) / kBM),
                    idx, weights, logits_out};
-    if (E == 64) return launch_router_k<64>(ctx, mx, mw, p);
-    if (E == 128) return launch_router_k<128>(ctx, mx, mw, p);
-    return launch_router_k<256>(ctx, mx, mw, p);
+    CUtensorMap mx, mw;
+    // E = 256 (tensor-bound): 2-SM CTA pairs (UMMA M=256) by default;
+    // MPB_ROUTER_SINGLE=1 forces the single-CTA kernel. E <= 128 is HBM-bound:
+    // single-CTA tiles already stream X at the HBM roofline.
+    static const bool single = [] {
+        const char *v = std::getenv("MPB_ROUTER_SINGLE");
+        return v && v[0] == '1';
+    }();
+    const bool pair = E == 256 && !single;
+    if (!make_map(&mx, X, T, H, kBM) || !make_map(&mw, W, E, H, pair ? E / 2 : E))
+        return fail(MPB_CUDA_ERROR, "mpb_router_topk: cuTensorMapEncodeTiled failed");
+    if (pair) return launch_router_k<256, true>(ctx, mx, mw, p);
+    if (E == 64) return launch_router_k<64, false>(ctx, mx, mw, p);
+    if (E == 128) return launch_router_k<128, false>(ctx, mx, mw, p);
+    return launch_router_k<256, false>(ctx, mx, mw, p);
 }

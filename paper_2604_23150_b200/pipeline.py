@@ -256,6 +256,13 @@ class RoutingPipeline:
                        torch.empty(P * L, D, dtype=torch.float64, device=dev))
 
     # ---------------------------------------------------------------- the step
+    def layer_untimed(self, l: int, X: torch.Tensor):
+        """layer() with the router event pair recorded by the caller (capture)."""
+        s, eng = self.spec, self.eng
+        # router event pair is recorded around this call by capture()
+        eng.router_topk(X, self.model.W[l], s.top_k, s.score_fn, s.renorm, out=(self.idx, self.w))
+        self._layer_tail(l)
+
     def layer(self, l: int, X: torch.Tensor, timed_router=False):
         s, eng = self.spec, self.eng
         if timed_router:
@@ -266,6 +273,10 @@ class RoutingPipeline:
         if timed_router:
             e1.record(eng.stream)
             self.router_events.append((e0, e1))
+        self._layer_tail(l)
+
+    def _layer_tail(self, l: int):
+        s, eng = self.spec, self.eng
         # deployed (cluster-routed) layout + permutation, with the round-robin
         # baseline's demand accounted in the same pass
         eng.dispatch_layout(self.idx, self.dp_deployed, src=self.src_cl, tag=self.dom_tok,
@@ -276,10 +287,13 @@ class RoutingPipeline:
             eng.coactivation(self.idx, s.experts, out=self.coact)
 
     def reduce_and_score(self, group=None):
-        s, eng = self.spec, self.eng
         if self.world > 1:
             import torch.distributed as dist
             dist.all_reduce(self.stats.view(torch.int64), group=group)
+        self._score_only()
+
+    def _score_only(self):
+        s, eng = self.spec, self.eng
         L, D, E = s.layers, s.groups, s.experts
         eng.score_placements(self.dem_rr, self.luts_rr, self.g2n, D, row_node=self.g2n,
                              out=self.sc_rr)
@@ -293,10 +307,64 @@ class RoutingPipeline:
                      self.topology, out=self.fin_cl[0], payload=self.fin_cl[1])
 
     def step(self, timed_router=False, group=None):
+        if getattr(self, "graphs", None):
+            return self._replay(group)
         self.stats.zero_()
         for l in range(self.spec.layers):
             self.layer(l, self.X[l], timed_router)
         self.reduce_and_score(group)
+
+    # ---------------------------------------------------------------- CUDA graphs
+    def capture(self, group=None) -> bool:
+        """Captures the step's launch sequence as CUDA graphs (one for the
+        layers, one for scoring; the NCCL all-reduce between them stays eager),
+        with event-record nodes around every router launch so the roofline is
+        still measured on the device inside the timed region. Returns False
+        (eager fallback of the launch mechanism, same kernels) if capture fails."""
+        eng = self.eng
+        L = self.spec.layers
+        old = eng.stream
+        try:
+            self.graph_events = [(torch.cuda.Event(enable_timing=True),
+                                  torch.cuda.Event(enable_timing=True)) for _ in range(L)]
+            for e0, e1 in self.graph_events:  # create the cudaEvent_t handles eagerly
+                e0.record(old)
+                e1.record(old)
+            cap = torch.cuda.Stream(eng.device)
+            cap.wait_stream(old)
+            n0 = eng.launches
+            g_layers, g_score = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+            with torch.cuda.stream(cap):
+                eng.set_stream(cap)
+                with torch.cuda.graph(g_layers, stream=cap):
+                    self.stats.zero_()
+                    for l in range(L):
+                        e0, e1 = self.graph_events[l]
+                        _record_external(e0, cap)
+                        self.layer_untimed(l, self.X[l])
+                        _record_external(e1, cap)
+                with torch.cuda.graph(g_score, stream=cap):
+                    self._score_only()
+            old.wait_stream(cap)
+            self.launches_per_step = eng.launches - n0  # our kernels per replayed step
+            self.graphs = (g_layers, g_score)
+            return True
+        except Exception:
+            self.graphs = None
+            return False
+        finally:
+            eng.set_stream(old)
+
+    def _replay(self, group=None):
+        g_layers, g_score = self.graphs
+        g_layers.replay()
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.all_reduce(self.stats.view(torch.int64), group=group)
+        g_score.replay()
+
+    def graph_router_ms(self):
+        return [a.elapsed_time(b) for a, b in self.graph_events]
 
     # ---------------------------------------------------------------- results
     def results(self):
@@ -316,6 +384,37 @@ class RoutingPipeline:
             best_candidate=float(cand_med[best] / lin_med) if lin_med > 0 else float("nan")),
             best_candidate_index=best,
             a2a_bytes_saved_pct=100.0 * (1.0 - norm(db)))
+
+
+_cudart = None
+
+
+def _record_external(ev: "torch.cuda.Event", stream: "torch.cuda.Stream") -> None:
+    """cudaEventRecordWithFlags(..., cudaEventRecordExternal) during stream
+    capture: an event-record node whose timestamps stay readable outside the
+    graph (torch's Event.record would make a graph-internal node)."""
+    global _cudart
+    import ctypes as C
+    if _cudart is None:
+        import os
+        cands = []
+        try:
+            import nvidia.cuda_runtime as ncr  # torch's own runtime
+            cands.append(os.path.join(os.path.dirname(ncr.__file__), "lib", "libcudart.so.12"))
+        except ImportError:
+            pass
+        cands += ["libcudart.so.12", "/usr/local/cuda/lib64/libcudart.so.12"]
+        for c in cands:
+            try:
+                _cudart = C.CDLL(c)
+                break
+            except OSError:
+                continue
+        _cudart.cudaEventRecordWithFlags.argtypes = [C.c_void_p, C.c_void_p, C.c_uint]
+    err = _cudart.cudaEventRecordWithFlags(C.c_void_p(ev.cuda_event),
+                                           C.c_void_p(stream.cuda_stream), 1)
+    if err != 0:
+        raise RuntimeError(f"cudaEventRecordWithFlags failed: {err}")
 
 
 def spec_for(name: str, **overrides) -> WorkloadSpec:

@@ -85,6 +85,7 @@ mpb_status mpb_context_destroy(mpb_context *ctx) {
     cudaStreamSynchronize(ctx->stream);
     if (ctx->d_error) cudaFree(ctx->d_error);
     if (ctx->scratch) cudaFree(ctx->scratch);
+    if (ctx->router_ws) cudaFree(ctx->router_ws);
     delete ctx;
     return MPB_OK;
 }

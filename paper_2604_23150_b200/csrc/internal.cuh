@@ -52,6 +52,10 @@ struct mpb_context {
     void *scratch = nullptr;
     size_t scratch_bytes = 0;
     cudaError_t ensure_scratch(size_t bytes);
+    // router split-K tail: fp32 partial accumulators + per-slot ready flags
+    void *router_ws = nullptr;
+    size_t router_ws_bytes = 0;
+    uint32_t router_epoch = 0;
 };
 
 struct mpb_placement {

@@ -65,7 +65,43 @@ struct RouterParams {
     int32_t *idx;
     float *w;
     float *logits;
+    // split-K tail (wave quantisation): the last partial wave's tiles are split in
+    // two K halves run by two units; the second half dumps its fp32 partial
+    uint32_t split_tail;
+    uint32_t epoch;
+    float *partial;      // [slot][rank][N/16 chunks][128 rows][16]
+    uint32_t *flags;     // [slot][rank] == epoch when the partial is ready
 };
+
+// Work item n of a scheduling unit: full waves of whole tiles, then (split
+// tail) unit u takes K-half (u & 1) of tail tile u / 2. role 0 = whole tile,
+// 1 = first K half + fix-up with the partial, 2 = second K half, dump only.
+struct WorkItem {
+    uint32_t tile, k0, k1, role, slot;
+};
+
+__device__ __forceinline__ bool next_item(uint32_t n, uint32_t unit, uint32_t units,
+                                          uint32_t num_tiles, uint32_t nk, uint32_t split,
+                                          WorkItem &w) {
+    if (!split) {
+        const uint32_t t = unit + n * units;
+        if (t >= num_tiles) return false;
+        w = {t, 0, nk, 0, 0};
+        return true;
+    }
+    const uint32_t waves = num_tiles / units;
+    if (n < waves) {
+        w = {unit + n * units, 0, nk, 0, 0};
+        return true;
+    }
+    const uint32_t rem = num_tiles - waves * units;
+    if (n == waves && unit < 2 * rem) {
+        const uint32_t slot = unit >> 1, h = unit & 1;
+        w = {waves * units + slot, h ? nk / 2 : 0, h ? nk : nk / 2, h ? 2u : 1u, slot};
+        return true;
+    }
+    return false;
+}
 
 // Selection order: (value desc, id asc), NaN below everything; a sentinel
 // slot (id < 0) is beaten by nothing.
@@ -160,9 +196,10 @@ __global__ void __launch_bounds__(kThreadsR, 1)
         const uint64_t pol_w = ptx::policy_evict_last();
         int stage = 0;
         uint32_t phase = 0;
-        for (uint32_t tile = unit; tile < p.num_tiles; tile += units) {
-            const int32_t m0 = static_cast<int32_t>(tile * Cfg::ROWS_PER_TILE + rank * kBM);
-            for (uint32_t kb = 0; kb < nk; ++kb) {
+        WorkItem it;
+        for (uint32_t n = 0; next_item(n, unit, units, p.num_tiles, nk, p.split_tail, it); ++n) {
+            const int32_t m0 = static_cast<int32_t>(it.tile * Cfg::ROWS_PER_TILE + rank * kBM);
+            for (uint32_t kb = it.k0; kb < it.k1; ++kb) {
                 ptx::mbar_wait(&empty[stage], phase ^ 1);
                 if constexpr (PAIR) {
                     // both CTAs' loads complete on the leader's full barrier
@@ -190,21 +227,23 @@ __global__ void __launch_bounds__(kThreadsR, 1)
         constexpr uint32_t idesc = ptx::idesc_bf16_f32<PAIR ? 2 * kBM : kBM, N>();
         int stage = 0;
         uint32_t phase = 0, acc = 0, aphase = 0;
-        for (uint32_t tile = unit; tile < p.num_tiles; tile += units) {
+        WorkItem it;
+        for (uint32_t n = 0; next_item(n, unit, units, p.num_tiles, nk, p.split_tail, it); ++n) {
             ptx::mbar_wait(&tempty[acc], aphase ^ 1);
             ptx::tc_fence_after();
             const uint32_t d = tmem_base + acc * N;
-            for (uint32_t kb = 0; kb < nk; ++kb) {
+            for (uint32_t kb = it.k0; kb < it.k1; ++kb) {
                 ptx::mbar_wait(&full[stage], phase);
                 ptx::tc_fence_after();
                 const uint64_t ad = ptx::sw128_kmajor_desc(ptx::smem_u32(sA + stage * Cfg::A_BYTES));
                 const uint64_t bd = ptx::sw128_kmajor_desc(ptx::smem_u32(sB + stage * Cfg::B_BYTES));
 #pragma unroll
                 for (int kk = 0; kk < kBK / 16; ++kk) {  // +32 bytes along K per UMMA_K = 16
+                    const uint32_t accum = (kb != it.k0) | (kk != 0);
                     if constexpr (PAIR)
-                        ptx::mma_bf16_2sm(d, ad + 2 * kk, bd + 2 * kk, idesc, (kb | kk) != 0);
+                        ptx::mma_bf16_2sm(d, ad + 2 * kk, bd + 2 * kk, idesc, accum);
                     else
-                        ptx::mma_bf16(d, ad + 2 * kk, bd + 2 * kk, idesc, (kb | kk) != 0);
+                        ptx::mma_bf16(d, ad + 2 * kk, bd + 2 * kk, idesc, accum);
                 }
                 if constexpr (PAIR)
                     ptx::mma_commit_2sm_mc(&empty[stage], 0x3);  // frees the stage in both CTAs
@@ -241,12 +280,65 @@ __global__ void __launch_bounds__(kThreadsR, 1)
         constexpr int NH = N / 2;
         const int off = KMAX - static_cast<int>(p.k);
         uint32_t acc = 0, aphase = 0;
-        for (uint32_t tile = unit; tile < p.num_tiles; tile += units) {
+        WorkItem it;
+        for (uint32_t n = 0; next_item(n, unit, units, p.num_tiles, nk, p.split_tail, it); ++n) {
             ptx::mbar_wait(&tfull[acc], aphase);
             ptx::tc_fence_after();
             const uint64_t row =
-                static_cast<uint64_t>(tile) * Cfg::ROWS_PER_TILE + rank * kBM + row_in_tile;
+                static_cast<uint64_t>(it.tile) * Cfg::ROWS_PER_TILE + rank * kBM + row_in_tile;
             const uint32_t taddr = tmem_base + acc * N + ((q * 32) << 16);
+            if (it.role != 0) {
+                // split-K tail: partial [slot][rank][chunk][row][16] fp32, coalesced rows
+                float *part = p.partial + (static_cast<size_t>(it.slot) * (PAIR ? 2 : 1) + rank) *
+                                              (static_cast<size_t>(N) * kBM);
+                uint32_t *flag = p.flags + it.slot * (PAIR ? 2 : 1) + rank;
+                if (it.role == 2) {
+#pragma unroll 1
+                    for (int c = half * NH; c < (half + 1) * NH; c += 16) {
+                        uint32_t r[16];
+                        ptx::tmem_ld_32x32b_x16(taddr + c, r);
+                        ptx::tmem_ld_wait();
+                        float4 *dst = reinterpret_cast<float4 *>(part + ((c / 16) * kBM + row_in_tile) * 16);
+#pragma unroll
+                        for (int i = 0; i < 4; ++i)
+                            dst[i] = make_float4(__uint_as_float(r[4 * i]), __uint_as_float(r[4 * i + 1]),
+                                                 __uint_as_float(r[4 * i + 2]),
+                                                 __uint_as_float(r[4 * i + 3]));
+                    }
+                    __threadfence();
+                    asm volatile("bar.sync 5, 256;" ::: "memory");  // every epilogue thread dumped
+                    if (warp == 4 && lane == 0)
+                        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flag), "r"(p.epoch)
+                                     : "memory");
+                    release_tmem<PAIR>(&tempty[acc], rank, lane);
+                    acc ^= 1;
+                    if (acc == 0) aphase ^= 1;
+                    continue;
+                }
+                // role 1: wait for the other K half, add it into TMEM, then finish
+                uint32_t seen;
+                do {
+                    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(flag) : "memory");
+                } while (seen != p.epoch);
+#pragma unroll 1
+                for (int c = half * NH; c < (half + 1) * NH; c += 16) {
+                    uint32_t r[16];
+                    ptx::tmem_ld_32x32b_x16(taddr + c, r);
+                    ptx::tmem_ld_wait();
+                    const float4 *src =
+                        reinterpret_cast<const float4 *>(part + ((c / 16) * kBM + row_in_tile) * 16);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const float4 v = __ldcg(src + i);
+                        r[4 * i] = __float_as_uint(__uint_as_float(r[4 * i]) + v.x);
+                        r[4 * i + 1] = __float_as_uint(__uint_as_float(r[4 * i + 1]) + v.y);
+                        r[4 * i + 2] = __float_as_uint(__uint_as_float(r[4 * i + 2]) + v.z);
+                        r[4 * i + 3] = __float_as_uint(__uint_as_float(r[4 * i + 3]) + v.w);
+                    }
+                    ptx::tmem_st_32x32b_x16(taddr + c, r);
+                }
+                ptx::tmem_st_wait();
+            }
             float tv[KMAX];
             int ti[KMAX];
 #pragma unroll
@@ -457,11 +549,42 @@ mpb_status launch_router_n(mpb_context *ctx, const CUtensorMap &mx, const CUtens
     cfg.blockDim = dim3(kThreadsR);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = ctx->stream;
+    uint32_t units;
     if constexpr (PAIR) {
         p.num_tiles = static_cast<uint32_t>((p.T + 2 * kBM - 1) / (2 * kBM));
-        const uint32_t pairs =
-            std::min<uint32_t>(p.num_tiles, static_cast<uint32_t>(ctx->num_sms) / 2);
-        cfg.gridDim = dim3(2 * pairs);
+        units = std::min<uint32_t>(p.num_tiles, static_cast<uint32_t>(ctx->num_sms) / 2);
+    } else {
+        units = std::min<uint32_t>(p.num_tiles, static_cast<uint32_t>(ctx->num_sms));
+    }
+    // split-K tail: when the last wave would leave at least half the units idle,
+    // its tiles are split in two K halves over twice as many units
+    const uint32_t full_units = PAIR ? static_cast<uint32_t>(ctx->num_sms) / 2
+                                     : static_cast<uint32_t>(ctx->num_sms);
+    const uint32_t nk = p.H / kBK;
+    const uint32_t waves = p.num_tiles / full_units;
+    const uint32_t rem = p.num_tiles - waves * full_units;
+    p.split_tail = rem > 0 && 2 * rem <= full_units && nk >= 2 && !std::getenv("MPB_ROUTER_NO_SPLIT");
+    if (p.split_tail) {
+        units = full_units;
+        const size_t ranks = PAIR ? 2 : 1;
+        const size_t flag_bytes = 4096;
+        const size_t need = flag_bytes + size_t(rem) * ranks * N * kBM * sizeof(float);
+        if (ctx->router_ws_bytes < need) {
+            MPB_CUDA(cudaStreamSynchronize(ctx->stream));
+            if (ctx->router_ws) cudaFree(ctx->router_ws);
+            ctx->router_ws = nullptr;
+            ctx->router_ws_bytes = 0;
+            MPB_CUDA(cudaMalloc(&ctx->router_ws, need));
+            MPB_CUDA(cudaMemset(ctx->router_ws, 0, flag_bytes));
+            ctx->router_ws_bytes = need;
+        }
+        if (++ctx->router_epoch == 0) ctx->router_epoch = 1;
+        p.epoch = ctx->router_epoch;
+        p.flags = static_cast<uint32_t *>(ctx->router_ws);
+        p.partial = reinterpret_cast<float *>(static_cast<char *>(ctx->router_ws) + flag_bytes);
+    }
+    if constexpr (PAIR) {
+        cfg.gridDim = dim3(2 * units);
         attr[0].id = cudaLaunchAttributeClusterDimension;
         attr[0].val.clusterDim.x = 2;
         attr[0].val.clusterDim.y = 1;
@@ -469,7 +592,7 @@ mpb_status launch_router_n(mpb_context *ctx, const CUtensorMap &mx, const CUtens
         cfg.attrs = attr;
         cfg.numAttrs = 1;
     } else {
-        cfg.gridDim = dim3(std::min<uint32_t>(p.num_tiles, static_cast<uint32_t>(ctx->num_sms)));
+        cfg.gridDim = dim3(units);
     }
     MPB_CUDA(cudaLaunchKernelEx(&cfg, kern, mx, mw, p));
     MPB_LAUNCHED(ctx);
@@ -507,7 +630,7 @@ extern "C" mpb_status mpb_router_topk(mpb_context *ctx, const void *X, const voi
     if (T == 0) return MPB_OK;
     if (T > 0x7fffffffull) return fail(MPB_CONFIG_ERROR, "mpb_router_topk: T too large");
     RouterParams p{T, H, k, score_fn, renorm, static_cast<uint32_t>((T + kBM - 1) / kBM),
-                   idx, weights, logits_out};
+                   idx, weights, logits_out, 0, 0, nullptr, nullptr};
     CUtensorMap mx, mw;
     // E = 256 (tensor-bound): 2-SM CTA pairs (UMMA M=256) by default;
     // MPB_ROUTER_SINGLE=1 forces the single-CTA kernel. E <= 128 is HBM-bound:

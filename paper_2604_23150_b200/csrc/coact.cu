@@ -1,4 +1,9 @@
-// K4: expert x expert co-activation via warp-ballot expert masks + popc.
+// K4: expert x expert co-activation.
+//
+// E <= 256 and k <= 16 (every shape the pipeline runs): tcgen05 kind::i8
+// tensor-core kernel k_coact_mma below (C = X^T X over the 0/1 routing
+// matrix, exact s32 accumulation). Otherwise the popc kernel described here.
+// Top-k ids are distinct per token; ids outside [0, E) are ignored.
 //
 // C[i][j] = #tokens whose top-k holds both i and j. For every group of 32
 // tokens the CTA needs one 32-bit mask per expert (bit u set when token u
@@ -15,7 +20,11 @@
 // Work: E^2/2 AND+POPC+ADD per 32 tokens (POPC-bound); HBM: T*k*4 bytes.
 // (No reference implementation: the closest analogue is aggregate_usage,
 // /root/reference/proj/core/src/placement.cpp:96-125.)
+#include <algorithm>
+#include <cstdlib>
+
 #include "internal.cuh"
+#include "tc_ptx.cuh"
 
 namespace mpb {
 namespace {
@@ -160,6 +169,233 @@ __global__ void k_coact_reduce(const uint32_t *partials, uint32_t chunks, uint32
     if (ib != jb) coact[static_cast<size_t>(j) * E + i] += s;
 }
 
+// ---------------------------------------------------------------------------
+// Tensor-core path (E <= 256, k <= 16): C = X^T X with X the [T x E] 0/1
+// routing matrix, on tcgen05 kind::i8 (u8 x u8 -> s32: exact integer counts).
+// Per 128-token chunk the producers build X in shared memory in its natural
+// token-major order, as an MN-major SW128 u8 operand: token t's row of
+// experts is 128-byte MN blocks (expert e in block e/128), rows grouped by 8
+// tokens into 1024-byte swizzle atoms. Each producer thread owns one token:
+// it zeroes the token's row (16-byte stores, swizzled so a warp's stores hit
+// distinct banks) and sets its k expert bytes — no transposes. One thread
+// issues the MMAs (both operands MN-major views of the same tile): the upper
+// triangle as tile 0 (experts 0..127 x all) and, when E > 128, tile 1
+// (experts 128.. x 128..); both accumulate in TMEM over the CTA's token
+// range. The epilogue writes the CTA's u16 partial (upper triangle only;
+// <= 65535 tokens per CTA) and k_coact_mma_reduce folds partials into C.
+// Work per 128 tokens: 128*128*(N0+N1) MACs on the tensor pipe; E/16 + k
+// shared stores per token; HBM: T*k*4 bytes of ids (+ the partials,
+// L2-resident).
+constexpr int kMmaStages = 4;
+constexpr int kMmaMaxK = 16;
+constexpr int kMmaThreads = 320;  // warp 0: TMEM + MMA; warps 1-8: producers + epilogue; 9: ids
+
+template <int WORDS>
+__global__ void __launch_bounds__(kMmaThreads, 1)
+    k_coact_mma(const int32_t *idx, uint64_t T, uint32_t k, uint32_t E, uint32_t N0, uint32_t N1,
+                uint32_t chunks_per_cta, uint32_t *partials, uint32_t dbg) {
+    constexpr bool kTwo = WORDS == 8;
+    constexpr uint32_t kRows = WORDS * 32;   // experts (padded) = partial row length
+    constexpr uint32_t kBlock = 128 * 128;   // one 128-expert MN block of 128 token rows
+    constexpr uint32_t kTile = kRows * 128;  // bytes per stage
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                                ~uintptr_t(1023));
+    uint8_t *tiles = smem;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + kMmaStages * kTile);
+    uint64_t *full = bars, *empty = bars + kMmaStages, *idfull = bars + 2 * kMmaStages,
+             *idempty = bars + 3 * kMmaStages, *tfull = bars + 4 * kMmaStages;
+    uint32_t *s_tmem = reinterpret_cast<uint32_t *>(tfull + 1);
+    int32_t *ring = reinterpret_cast<int32_t *>(bars + 4 * kMmaStages + 2);  // [S][128][k]
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kMmaStages; ++s) {
+            ptx::mbar_init(&full[s], 128);
+            ptx::mbar_init(&empty[s], 1);
+            ptx::mbar_init(&idfull[s], 1);
+            ptx::mbar_init(&idempty[s], 128);
+        }
+        ptx::mbar_init(tfull, 1);
+        ptx::fence_barrier_init();
+    }
+    if (dbg & 256) {
+        __syncthreads();
+        return;
+    }
+    if (warp == 0) ptx::tmem_alloc<kTwo ? 512 : 256>(s_tmem);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = *s_tmem;
+
+    const uint64_t tok0 = static_cast<uint64_t>(blockIdx.x) * chunks_per_cta * 128;
+    const uint64_t tok1 = min(T, tok0 + static_cast<uint64_t>(chunks_per_cta) * 128);
+    const uint32_t nch = (dbg & 32) ? 0 : tok0 < tok1 ? static_cast<uint32_t>((tok1 - tok0 + 127) / 128) : 0;
+
+    if (warp == 0) {
+        if (lane == 0 && nch) {
+            const uint32_t id0 = ptx::idesc_u8_s32_mn(128, N0);
+            const uint32_t id1 = ptx::idesc_u8_s32_mn(128, N1);
+            for (uint32_t n = 0; n < nch; ++n) {
+                const uint32_t s = n % kMmaStages;
+                ptx::mbar_wait(&full[s], (n / kMmaStages) & 1);
+                ptx::tc_fence_after();
+                const uint32_t base = ptx::smem_u32(tiles + s * kTile);
+#pragma unroll
+                for (uint32_t kk = 0; kk < 4; ++kk) {  // K = 32 tokens per MMA
+                    const uint32_t acc = (n | kk) != 0;
+                    if (dbg & 2) continue;
+                    // K = 32 tokens = 4 swizzle atoms of 8 token rows
+                    const uint64_t d0 = ptx::sw128_mnmajor_desc(base + kk * 4096, kBlock);
+                    ptx::mma_u8(tmem, d0, d0, id0, acc);
+                    if (kTwo) {
+                        const uint64_t d1 = ptx::sw128_mnmajor_desc(base + kBlock + kk * 4096, kBlock);
+                        ptx::mma_u8(tmem + 256, d1, d1, id1, acc);
+                    }
+                }
+                ptx::mma_commit(&empty[s]);
+            }
+            ptx::mma_commit(tfull);
+        }
+        __syncwarp();
+    } else if (warp == 9) {
+        // ids loader: chunk n's [ntok x k] int32 block -> ring slot n % S with
+        // one bulk copy (async proxy; the sub-16-byte tail by plain copies)
+        if (lane == 0) {
+            const bool aligned = (reinterpret_cast<uintptr_t>(idx) & 15) == 0;
+            for (uint32_t n = 0; n < nch; ++n) {
+                const uint32_t s = n % kMmaStages;
+                if (n >= kMmaStages) ptx::mbar_wait(&idempty[s], ((n / kMmaStages) - 1) & 1);
+                const uint64_t t = tok0 + static_cast<uint64_t>(n) * 128;
+                const uint32_t ntok = static_cast<uint32_t>(min(static_cast<uint64_t>(128), tok1 - t));
+                const uint32_t bytes = ntok * k * 4;
+                const uint32_t bulk = aligned ? bytes & ~15u : 0;
+                const int32_t *src = idx + t * k;
+                int32_t *dst = ring + s * 128 * k;
+                for (uint32_t i = bulk / 4; i < bytes / 4; ++i) dst[i] = __ldg(src + i);
+                ptx::mbar_arrive_expect_tx(&idfull[s], bulk);
+                if (bulk) ptx::bulk_load(dst, src, bulk, &idfull[s]);
+            }
+        }
+        __syncwarp();
+    } else {
+        const uint32_t pw = warp - 1, set = pw >> 2, g = pw & 3;
+        const uint32_t u = g * 32 + lane;  // token within the chunk
+        for (uint32_t n = set; n < nch; n += 2) {
+            const uint32_t s = n % kMmaStages;
+            const uint32_t tile = ptx::smem_u32(tiles + s * kTile);
+            ptx::mbar_wait(&idfull[s], (n / kMmaStages) & 1);  // this chunk's ids landed
+            int32_t ids[kMmaMaxK];
+            const bool ok = tok0 + static_cast<uint64_t>(n) * 128 + u < tok1;
+            {
+                const uint32_t ids_s = ptx::smem_u32(ring + (s * 128 + u) * k);
+#pragma unroll
+                for (int j = 0; j < kMmaMaxK; ++j) {
+                    ids[j] = -1;
+                    if (ok && j < static_cast<int>(k))
+                        asm volatile("ld.shared.s32 %0, [%1];" : "=r"(ids[j]) : "r"(ids_s + 4 * j) : "memory");
+                }
+            }
+            ptx::mbar_arrive(&idempty[s]);
+            if (n >= kMmaStages) ptx::mbar_wait(&empty[s], ((n / kMmaStages) - 1) & 1);
+            // token u's row: (u/8)*1024 + (u%8)*128 in each MN block; 16-byte
+            // chunk c of the row lives at physical chunk c ^ (u%8)
+            const uint32_t row = tile + (u >> 3) * 1024 + (u & 7) * 128;
+            if (!(dbg & 4)) {
+#pragma unroll
+                for (int b = 0; b < (kTwo ? 2 : 1); ++b)
+#pragma unroll
+                    for (uint32_t c = 0; c < 8; ++c)
+                        asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(
+                                         row + b * kBlock + ((c ^ (u & 7)) << 4)),
+                                     "r"(0u)
+                                     : "memory");
+#pragma unroll
+                for (int j = 0; j < kMmaMaxK; ++j) {
+                    const uint32_t e = static_cast<uint32_t>(ids[j]);
+                    if (e < E)
+                        asm volatile("st.shared.u8 [%0], %1;" ::"r"(
+                                         row + (e >> 7) * kBlock + ((((e >> 4) & 7) ^ (u & 7)) << 4) +
+                                         (e & 15)),
+                                     "r"(1u)
+                                     : "memory");
+                }
+            }
+            if (!(dbg & 8)) ptx::fence_proxy_async_smem();
+            ptx::mbar_arrive(&full[s]);
+        }
+        // ---- epilogue: TMEM lane quarter (warp % 4) holds tile rows 32*(warp%4) + lane;
+        // the two warp sets take alternate 32-column slices
+        if (nch) {
+            ptx::mbar_wait(tfull, 0);
+            ptx::tc_fence_after();
+            const uint32_t q = warp & 3, r = q * 32 + lane;
+            uint16_t *out = reinterpret_cast<uint16_t *>(partials) +
+                            static_cast<size_t>(blockIdx.x) * kRows * kRows;
+            auto dump = [&](uint32_t tcol, uint32_t orow, uint32_t ocol) {
+                uint32_t v[32];
+                ptx::tmem_ld_32x32b_x32(tmem + ((q * 32) << 16) + tcol, v);
+                ptx::tmem_ld_wait();
+                uint4 *o = reinterpret_cast<uint4 *>(out + static_cast<size_t>(orow) * kRows + ocol);
+#pragma unroll
+                for (int w = 0; w < 4; ++w)
+                    if (!(dbg & 1))
+                        o[w] = make_uint4(v[8 * w] | (v[8 * w + 1] << 16),
+                                          v[8 * w + 2] | (v[8 * w + 3] << 16),
+                                          v[8 * w + 4] | (v[8 * w + 5] << 16),
+                                          v[8 * w + 6] | (v[8 * w + 7] << 16));
+            };
+            // tile 0: row r, cols >= the quarter's first row
+            if (!(dbg & 64))
+            for (uint32_t c = q * 32 + set * 32; c < N0; c += 64) dump(c, r, c);
+            if (kTwo && !(dbg & 64))  // tile 1: row 128 + r, col 128 + c
+                for (uint32_t c = q * 32 + set * 32; c < N1; c += 64) dump(256 + c, 128 + r, 128 + c);
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 0) ptx::tmem_dealloc<kTwo ? 512 : 256>(tmem);
+}
+
+// C[i][j] (+ mirror) += sum over CTAs [z*32, z*32+32) of the u16 partials,
+// i <= j < E; one thread per column pair (j0, j0+1).
+__global__ void k_coact_mma_reduce(const uint32_t *partials, uint32_t ctas, uint32_t E,
+                                   uint32_t E8, uint64_t *coact) {
+    const uint32_t i = blockIdx.y;
+    const uint32_t j0 = 2 * (blockIdx.x * blockDim.x + threadIdx.x);
+    if (j0 + 1 < i || j0 >= E) return;
+    const uint32_t c0 = blockIdx.z * 32, c1 = min(ctas, c0 + 32);
+    const size_t stride = static_cast<size_t>(E8) * E8 / 2;  // u32 words per partial
+    const uint32_t *p = partials + (static_cast<size_t>(i) * E8 + j0) / 2;
+    unsigned long long s0 = 0, s1 = 0;
+    uint32_t c = c0;
+    for (; c + 8 <= c1; c += 8) {
+        uint32_t v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = __ldg(p + (c + u) * stride);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            s0 += v[u] & 0xFFFFu;
+            s1 += v[u] >> 16;
+        }
+    }
+    for (; c < c1; ++c) {
+        const uint32_t v = __ldg(p + c * stride);
+        s0 += v & 0xFFFFu;
+        s1 += v >> 16;
+    }
+    auto add = [&](uint32_t j, unsigned long long v) {
+        if (j < i || j >= E) return;
+        atomicAdd(reinterpret_cast<unsigned long long *>(coact) + static_cast<size_t>(i) * E + j, v);
+        if (i != j)
+            atomicAdd(reinterpret_cast<unsigned long long *>(coact) + static_cast<size_t>(j) * E + i,
+                      v);
+    };
+    add(j0, s0);
+    add(j0 + 1, s1);
+}
+
 template <int WORDS>
 mpb_status launch_partial(mpb_context *ctx, dim3 grid, uint32_t threads, size_t smem,
                           const int32_t *idx, uint64_t T, uint32_t k, uint32_t NT, uint32_t tpcta,
@@ -187,6 +423,42 @@ extern "C" mpb_status mpb_coactivation(mpb_context *ctx, const int32_t *idx, uin
     if (E == 0 || E > 32 * kMaxWords)
         return fail(MPB_CONFIG_ERROR, "mpb_coactivation: need 1 <= E <= 1024");
     if (T == 0 || k == 0) return MPB_OK;
+    static const bool force_popc = std::getenv("MPB_COACT_POPC") != nullptr;
+    if (E <= 256 && k <= static_cast<uint32_t>(kMmaMaxK) && !force_popc) {
+        const bool two = E > 128;
+        const uint32_t E16 = (E + 15) / 16 * 16;
+        const uint32_t N0 = E16, N1 = two ? E16 - 128 : 0;
+        const uint32_t E8 = two ? 256 : 128;
+        const uint64_t chunks = (T + 127) / 128;
+        // one CTA per SM (at most), >= 2 chunks each; u16 partials need
+        // <= 65535 tokens per CTA
+        static const char *env = std::getenv("MPB_COACT_CHUNKS_PER_CTA");
+        const uint64_t want = env ? std::max(1, std::atoi(env)) : 2;
+        uint64_t ctas = std::min<uint64_t>(ctx->num_sms, std::max<uint64_t>(1, chunks / want));
+        uint64_t cpc = (chunks + ctas - 1) / ctas;
+        if (cpc > 511) cpc = 511;
+        ctas = (chunks + cpc - 1) / cpc;
+        MPB_CUDA(ctx->ensure_scratch(size_t(ctas) * E8 * E8 * 2));
+        auto *partials = static_cast<uint32_t *>(ctx->scratch);
+        const size_t smem = 1024 + size_t(kMmaStages) * E8 * 128 + (4 * kMmaStages + 2) * 8 +
+                            size_t(kMmaStages) * 128 * k * 4;
+        static const char *dbg_env = std::getenv("MPB_COACT_DBG");
+        const uint32_t dbg = dbg_env ? std::atoi(dbg_env) : 0;
+        auto kern = two ? k_coact_mma<8> : k_coact_mma<4>;
+        MPB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        kern<<<static_cast<unsigned>(ctas), kMmaThreads, smem, ctx->stream>>>(
+            idx, T, k, E, N0, N1, static_cast<uint32_t>(cpc), partials, dbg);
+        MPB_LAUNCHED(ctx);
+        dim3 rgrid(((E + 1) / 2 + 127) / 128, E, static_cast<unsigned>((ctas + 31) / 32));
+        static const bool carve = std::getenv("MPB_CARVEOUT") != nullptr;
+        if (carve)
+            MPB_CUDA(cudaFuncSetAttribute(k_coact_mma_reduce,
+                                          cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        if (!(dbg & 128)) k_coact_mma_reduce<<<rgrid, 128, 0, ctx->stream>>>(partials, static_cast<uint32_t>(ctas), E,
+                                                          E8, coact);
+        MPB_LAUNCHED(ctx);
+        return MPB_OK;
+    }
     const uint32_t words = (E + 31) / 32;
     const uint32_t W = words <= 2 ? 2 : words <= 4 ? 4 : words <= 8 ? 8 : words <= 16 ? 16 : 32;
     const uint32_t E8 = W * 32;

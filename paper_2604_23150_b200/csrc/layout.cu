@@ -110,6 +110,34 @@ __device__ __forceinline__ uint32_t resolve(const LayoutParams &p, uint64_t pair
     return slot;
 }
 
+// Per-token fields of the pairs q..q+3 (pair ids < 2^31, so 32-bit math):
+// one division per 4 pairs, token loads only when the token changes.
+struct TokenCursor {
+    uint32_t t, r, src, s2, tg;
+};
+
+__device__ __forceinline__ void load_token(const LayoutParams &p, TokenCursor &c) {
+    if (c.t >= p.T) return;
+    c.src = p.src_group ? static_cast<uint32_t>(__ldg(p.src_group + c.t))
+                        : p.src_base + static_cast<uint32_t>((uint64_t(c.t) * p.src_span) / p.T);
+    c.s2 = p.src2 ? static_cast<uint32_t>(__ldg(p.src2 + c.t)) : 0u;
+    c.tg = p.tag ? static_cast<uint32_t>(__ldg(p.tag + c.t)) : kNone;
+}
+
+__device__ __forceinline__ void cursor_start(const LayoutParams &p, uint32_t q, TokenCursor &c) {
+    c.t = q / p.k;
+    c.r = q - c.t * p.k;
+    load_token(p, c);
+}
+
+__device__ __forceinline__ void cursor_next(const LayoutParams &p, TokenCursor &c) {
+    if (++c.r == p.k) {
+        c.r = 0;
+        ++c.t;
+        load_token(p, c);
+    }
+}
+
 template <bool kPerm>
 __global__ void __launch_bounds__(kThreads) k_layout_count(LayoutParams p) {
     extern __shared__ uint32_t sm[];
@@ -123,7 +151,43 @@ __global__ void __launch_bounds__(kThreads) k_layout_count(LayoutParams p) {
     for (uint32_t i = threadIdx.x; i < nsm; i += kThreads) sm[i] = 0;
     __syncthreads();
 
-    const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kChunk;
+    const uint32_t base = blockIdx.x * kChunk;
+    const uint32_t P = static_cast<uint32_t>(p.P);
+    if (p.demand_smem && (!p.src2 || p.demand2_smem) && (!p.tag || p.tag_smem)) {
+        // fast path: every histogram is block-private; coverage is checked per
+        // non-zero cell at flush time instead of per pair
+#pragma unroll
+        for (int h = 0; h < kChunk / (kThreads * 4); ++h) {
+            const uint32_t q = base + h * kThreads * 4 + threadIdx.x * 4;
+            if (q >= P) break;
+            int32_t v[4];
+            load4(p.idx, q, p.P, v);
+            TokenCursor tc;
+            cursor_start(p, q, tc);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                if (c) cursor_next(p, tc);
+                if (q + c >= P) break;
+                const uint32_t e = static_cast<uint32_t>(v[c]);
+                if (e >= p.E) {
+                    atomicOr(p.err, kErrExpertRange);
+                    continue;
+                }
+                if (tc.src >= p.D) {
+                    atomicOr(p.err, kErrSourceRange);
+                    continue;
+                }
+                atomicAdd(s_demand + tc.src * p.E + e, 1u);
+                if (p.src2) {
+                    if (tc.s2 < p.D)
+                        atomicAdd(s_demand2 + tc.s2 * p.E + e, 1u);
+                    else
+                        atomicOr(p.err, kErrSourceRange);
+                }
+                if (tc.tg < p.n_tags) atomicAdd(s_tag + tc.tg * p.E + e, 1u);
+            }
+        }
+    } else {
 #pragma unroll
     for (int h = 0; h < kChunk / (kThreads * 4); ++h) {
         const uint64_t q = base + static_cast<uint64_t>(h) * kThreads * 4 + threadIdx.x * 4;
@@ -165,17 +229,22 @@ __global__ void __launch_bounds__(kThreads) k_layout_count(LayoutParams p) {
             }
         }
     }
+    }
     __syncthreads();
     if (p.demand_smem) {
         for (uint32_t i = threadIdx.x; i < DE; i += kThreads) {
             const uint32_t c = s_demand[i];
             if (!c) continue;
+            // the block's slot counts (and coverage) from its (src, expert) cells
+            const uint32_t sg = i / p.E, e = i - sg * p.E;
+            const uint16_t slot = __ldg(p.slot_lut + static_cast<size_t>(p.g2n[sg]) * p.E + e);
+            if (slot == 0xFFFF) {
+                atomicOr(p.err, kErrUncovered);
+                continue;
+            }
             atomicAdd(reinterpret_cast<unsigned long long *>(p.demand) + i,
                       static_cast<unsigned long long>(c));
-            if (kPerm) {  // the block's slot counts from its (src, expert) cells
-                const uint32_t sg = i / p.E, e = i - sg * p.E;
-                atomicAdd(s_slot + __ldg(p.slot_lut + static_cast<size_t>(p.g2n[sg]) * p.E + e), c);
-            }
+            if (kPerm) atomicAdd(s_slot + slot, c);
         }
     }
     if (p.demand2_smem)
@@ -269,26 +338,25 @@ __global__ void __launch_bounds__(kThreads) k_layout_scatter(LayoutParams p, int
             key_offsets[key] = static_cast<int64_t>(s_base[key_lb[key]]);
 
     // each warp owns 256 consecutive pairs: two 128-bit loads per lane
-    const uint64_t wbase = static_cast<uint64_t>(blockIdx.x) * kChunk + warp * 256ull;
+    const uint32_t wbase = blockIdx.x * kChunk + warp * 256u;
+    const uint32_t P = static_cast<uint32_t>(p.P);
     uint32_t sl[2][4];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-        const uint64_t q = wbase + h * 128 + lane * 4;
+        const uint32_t q = wbase + h * 128 + lane * 4;
         int32_t v[4];
         load4(p.idx, q, p.P, v);
+        TokenCursor tc;
+        if (q < P) cursor_start(p, q, tc);
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-            uint32_t src;
-            uint64_t t;
             // errors were flagged by the count pass; here invalid pairs drop out
-            const uint64_t pair = q + c;
             uint32_t slot = kNone;
-            if (pair < p.P && v[c] >= 0 && static_cast<uint32_t>(v[c]) < p.E) {
-                t = pair / p.k;
-                src = source_of(p, t);
-                if (src < p.D) {
+            if (q + c < P) {
+                if (c) cursor_next(p, tc);
+                if (static_cast<uint32_t>(v[c]) < p.E && tc.src < p.D) {
                     const uint16_t s16 =
-                        __ldg(p.slot_lut + static_cast<size_t>(p.g2n[src]) * p.E + v[c]);
+                        __ldg(p.slot_lut + static_cast<size_t>(__ldg(p.g2n + tc.src)) * p.E + v[c]);
                     slot = s16 == 0xFFFF ? kNone : s16;
                 }
             }

@@ -229,8 +229,12 @@ def test_layout_accumulates_across_shards(eng, oracle):
 # ---------------------------------------------------------------- co-activation
 
 
+# E <= 256 and k <= 16 run on the tcgen05 kind::i8 path (one or two TMEM
+# tiles, any number of 128-token chunks per CTA); larger E or k on popc
 @pytest.mark.parametrize("T,E,k", [(1, 8, 2), (33, 64, 2), (4096, 128, 8), (20000, 256, 8),
-                                   (3000, 100, 5), (5000, 128, 1)])
+                                   (3000, 100, 5), (5000, 128, 1), (65536, 256, 8),
+                                   (3001, 200, 8), (777, 256, 16), (130, 129, 3),
+                                   (2000, 512, 8), (1000, 64, 20)])
 def test_coactivation_bit_exact(eng, oracle, T, E, k):
     rng = np.random.default_rng(T * 7 + E)
     idx = random_idx(rng, T, E, k)
@@ -307,3 +311,17 @@ def test_gather_combine_round_trip(eng):
     eng.sync()
     ref = (w.unsqueeze(-1) * X.float().unsqueeze(1)).sum(1)
     torch.testing.assert_close(Y.float(), ref, rtol=1e-2, atol=1e-2)
+
+
+@pytest.mark.parametrize("k", [3, 8])
+def test_coactivation_unaligned_ids(eng, oracle, k):
+    """ids not 16-byte aligned: the tensor-core path's loader falls back to
+    plain copies instead of bulk copies."""
+    rng = np.random.default_rng(11)
+    T, E = 1000, 256
+    idx = random_idx(rng, T, E, k)
+    buf = torch.empty(T * k + 1, dtype=torch.int32, device="cuda")
+    buf[1:] = dev(idx).view(-1)
+    c = eng.coactivation(buf[1:].view(T, k), E)
+    eng.sync()
+    np.testing.assert_array_equal(c.cpu().numpy(), oracle.coactivation(idx, E))

@@ -1,4 +1,4 @@
-"""Warm per-kernel timings (CUDA events) at the DSv3 step shape."""
+"""Warm per-kernel GPU timings (CUDA events, launches pre-queued) at the DSv3 step shape."""
 import sys
 from pathlib import Path
 
@@ -19,6 +19,8 @@ top = mp.Topology.contiguous(D, 1, D, 1, 2)
 pl = mp.Placement([list(range(d * 32, d * 32 + 32)) for d in range(D)], E, 0, 32)
 dp = eng.placement(pl, top)
 demand = torch.zeros(D, E, dtype=torch.uint64, device="cuda")
+demand2 = torch.zeros(D, E, dtype=torch.uint64, device="cuda")
+src2 = torch.from_numpy((np.arange(T) // 16 * 3 % D).astype(np.uint8)).cuda()
 pop = torch.zeros(8, E, dtype=torch.uint64, device="cuda")
 sp = torch.empty(T * k, dtype=torch.int32, device="cuda")
 pp = torch.empty(T * k, dtype=torch.int32, device="cuda")
@@ -38,6 +40,10 @@ cases = {
     "layout+perm+tag": lambda: eng.dispatch_layout(idx, dp, src=src, tag=dom, n_tags=8,
                                                    demand=demand, tag_pop=pop,
                                                    perm_out=(sp, pp, ko)),
+    "layout+perm+tag+src2": lambda: eng.dispatch_layout(idx, dp, src=src, tag=dom, n_tags=8,
+                                                        demand=demand, tag_pop=pop,
+                                                        perm_out=(sp, pp, ko), src2=src2,
+                                                        demand2=demand2),
     "layout demand-only": lambda: eng.dispatch_layout(idx, dp, src=src, permutation=False,
                                                       demand=demand),
     "coactivation": lambda: eng.coactivation(idx, E, out=co),
@@ -53,6 +59,9 @@ for name, fn in cases.items():
     torch.cuda.synchronize()
     n0 = eng.launches
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # keep the GPU busy while the host queues the 20 calls, so the events time
+    # the kernels, not the host's launch rate
+    torch.cuda._sleep(int(2e7))
     s.record()
     for _ in range(20):
         fn()

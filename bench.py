@@ -299,7 +299,7 @@ def run_gpu_arm(args, spec):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    launches0 = eng.launches
+    launches0 = pipe.launches
     pipe.router_events = []
     start = torch.cuda.Event(enable_timing=True)
     end = torch.cuda.Event(enable_timing=True)
@@ -314,7 +314,7 @@ def run_gpu_arm(args, spec):
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-    launches = eng.launches - launches0
+    launches = pipe.launches - launches0
     if graphed:  # kernels replayed from the graphs: launches per step x steps
         launches = pipe.launches_per_step * args.steps
     ms = start.elapsed_time(end)

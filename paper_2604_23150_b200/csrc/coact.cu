@@ -182,7 +182,7 @@ __global__ void k_coact_reduce(const uint32_t *partials, uint32_t chunks, uint32
 // triangle as tile 0 (experts 0..127 x all) and, when E > 128, tile 1
 // (experts 128.. x 128..); both accumulate in TMEM over the CTA's token
 // range. The epilogue writes the CTA's u16 partial (upper triangle only;
-// <= 65535 tokens per CTA) and k_coact_mma_reduce folds partials into C.
+// <= 65535 tokens per CTA) and k_coact_mma_reduce folds the partials into C.
 // Work per 128 tokens: 128*128*(N0+N1) MACs on the tensor pipe; E/16 + k
 // shared stores per token; HBM: T*k*4 bytes of ids (+ the partials,
 // L2-resident).
@@ -193,7 +193,7 @@ constexpr int kMmaThreads = 320;  // warp 0: TMEM + MMA; warps 1-8: producers + 
 template <int WORDS>
 __global__ void __launch_bounds__(kMmaThreads, 1)
     k_coact_mma(const int32_t *idx, uint64_t T, uint32_t k, uint32_t E, uint32_t N0, uint32_t N1,
-                uint32_t chunks_per_cta, uint32_t *partials, uint32_t dbg) {
+                uint32_t chunks_per_cta, uint32_t *partials) {
     constexpr bool kTwo = WORDS == 8;
     constexpr uint32_t kRows = WORDS * 32;   // experts (padded) = partial row length
     constexpr uint32_t kBlock = 128 * 128;   // one 128-expert MN block of 128 token rows
@@ -219,10 +219,6 @@ __global__ void __launch_bounds__(kMmaThreads, 1)
         ptx::mbar_init(tfull, 1);
         ptx::fence_barrier_init();
     }
-    if (dbg & 256) {
-        __syncthreads();
-        return;
-    }
     if (warp == 0) ptx::tmem_alloc<kTwo ? 512 : 256>(s_tmem);
     ptx::tc_fence_before();
     __syncthreads();
@@ -231,7 +227,7 @@ __global__ void __launch_bounds__(kMmaThreads, 1)
 
     const uint64_t tok0 = static_cast<uint64_t>(blockIdx.x) * chunks_per_cta * 128;
     const uint64_t tok1 = min(T, tok0 + static_cast<uint64_t>(chunks_per_cta) * 128);
-    const uint32_t nch = (dbg & 32) ? 0 : tok0 < tok1 ? static_cast<uint32_t>((tok1 - tok0 + 127) / 128) : 0;
+    const uint32_t nch = tok0 < tok1 ? static_cast<uint32_t>((tok1 - tok0 + 127) / 128) : 0;
 
     if (warp == 0) {
         if (lane == 0 && nch) {
@@ -245,7 +241,6 @@ __global__ void __launch_bounds__(kMmaThreads, 1)
 #pragma unroll
                 for (uint32_t kk = 0; kk < 4; ++kk) {  // K = 32 tokens per MMA
                     const uint32_t acc = (n | kk) != 0;
-                    if (dbg & 2) continue;
                     // K = 32 tokens = 4 swizzle atoms of 8 token rows
                     const uint64_t d0 = ptx::sw128_mnmajor_desc(base + kk * 4096, kBlock);
                     ptx::mma_u8(tmem, d0, d0, id0, acc);
@@ -302,7 +297,7 @@ __global__ void __launch_bounds__(kMmaThreads, 1)
             // token u's row: (u/8)*1024 + (u%8)*128 in each MN block; 16-byte
             // chunk c of the row lives at physical chunk c ^ (u%8)
             const uint32_t row = tile + (u >> 3) * 1024 + (u & 7) * 128;
-            if (!(dbg & 4)) {
+            {
 #pragma unroll
                 for (int b = 0; b < (kTwo ? 2 : 1); ++b)
 #pragma unroll
@@ -322,7 +317,7 @@ __global__ void __launch_bounds__(kMmaThreads, 1)
                                      : "memory");
                 }
             }
-            if (!(dbg & 8)) ptx::fence_proxy_async_smem();
+            ptx::fence_proxy_async_smem();
             ptx::mbar_arrive(&full[s]);
         }
         // ---- epilogue: TMEM lane quarter (warp % 4) holds tile rows 32*(warp%4) + lane;
@@ -340,16 +335,14 @@ __global__ void __launch_bounds__(kMmaThreads, 1)
                 uint4 *o = reinterpret_cast<uint4 *>(out + static_cast<size_t>(orow) * kRows + ocol);
 #pragma unroll
                 for (int w = 0; w < 4; ++w)
-                    if (!(dbg & 1))
-                        o[w] = make_uint4(v[8 * w] | (v[8 * w + 1] << 16),
+                    o[w] = make_uint4(v[8 * w] | (v[8 * w + 1] << 16),
                                           v[8 * w + 2] | (v[8 * w + 3] << 16),
                                           v[8 * w + 4] | (v[8 * w + 5] << 16),
                                           v[8 * w + 6] | (v[8 * w + 7] << 16));
             };
             // tile 0: row r, cols >= the quarter's first row
-            if (!(dbg & 64))
             for (uint32_t c = q * 32 + set * 32; c < N0; c += 64) dump(c, r, c);
-            if (kTwo && !(dbg & 64))  // tile 1: row 128 + r, col 128 + c
+            if (kTwo)  // tile 1: row 128 + r, col 128 + c
                 for (uint32_t c = q * 32 + set * 32; c < N1; c += 64) dump(256 + c, 128 + r, 128 + c);
         }
     }
@@ -358,42 +351,50 @@ __global__ void __launch_bounds__(kMmaThreads, 1)
     if (warp == 0) ptx::tmem_dealloc<kTwo ? 512 : 256>(tmem);
 }
 
-// C[i][j] (+ mirror) += sum over CTAs [z*32, z*32+32) of the u16 partials,
-// i <= j < E; one thread per column pair (j0, j0+1).
-__global__ void k_coact_mma_reduce(const uint32_t *partials, uint32_t ctas, uint32_t E,
-                                   uint32_t E8, uint64_t *coact) {
-    const uint32_t i = blockIdx.y;
-    const uint32_t j0 = 2 * (blockIdx.x * blockDim.x + threadIdx.x);
-    if (j0 + 1 < i || j0 >= E) return;
-    const uint32_t c0 = blockIdx.z * 32, c1 = min(ctas, c0 + 32);
-    const size_t stride = static_cast<size_t>(E8) * E8 / 2;  // u32 words per partial
-    const uint32_t *p = partials + (static_cast<size_t>(i) * E8 + j0) / 2;
-    unsigned long long s0 = 0, s1 = 0;
-    uint32_t c = c0;
-    for (; c + 8 <= c1; c += 8) {
-        uint32_t v[8];
+// Row i of C (one CTA of 8 warps per row): warp w sums partials w, w+8, ...
+// with lane L owning columns 8L..8L+7 (coalesced 16-byte loads, 8 in flight);
+// the warps' sums meet in shared memory; C[i][j] and C[j][i] += sum, j >= i.
+__global__ void __launch_bounds__(256) k_coact_mma_reduce(const uint32_t *partials, uint32_t ctas,
+                                                          uint32_t E, uint32_t kRows,
+                                                          uint64_t *coact) {
+    __shared__ uint32_t s_red[8][256];
+    const uint32_t i = blockIdx.x, w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const size_t pstride = static_cast<size_t>(kRows) * kRows / 8;  // uint4 per partial
+    uint32_t acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (8 * lane < kRows && 8 * lane + 7 >= i) {
+        const uint4 *p = reinterpret_cast<const uint4 *>(partials) +
+                         (static_cast<size_t>(i) * kRows) / 8 + lane;
+        for (uint32_t c0 = w; c0 < ctas; c0 += 64) {
+            uint4 v[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = __ldg(p + (c + u) * stride);
+            for (int b = 0; b < 8; ++b) {
+                const uint32_t c = c0 + 8 * b;
+                v[b] = c < ctas ? __ldg(p + c * pstride) : make_uint4(0, 0, 0, 0);
+            }
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            s0 += v[u] & 0xFFFFu;
-            s1 += v[u] >> 16;
+            for (int b = 0; b < 8; ++b) {
+                acc[0] += v[b].x & 0xFFFFu;
+                acc[1] += v[b].x >> 16;
+                acc[2] += v[b].y & 0xFFFFu;
+                acc[3] += v[b].y >> 16;
+                acc[4] += v[b].z & 0xFFFFu;
+                acc[5] += v[b].z >> 16;
+                acc[6] += v[b].w & 0xFFFFu;
+                acc[7] += v[b].w >> 16;
+            }
         }
     }
-    for (; c < c1; ++c) {
-        const uint32_t v = __ldg(p + c * stride);
-        s0 += v & 0xFFFFu;
-        s1 += v >> 16;
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj) s_red[w][(8 * lane + jj) & 255] = acc[jj];
+    __syncthreads();
+    const uint32_t j = threadIdx.x;
+    if (j >= i && j < E) {
+        uint32_t sum = 0;
+#pragma unroll
+        for (int ww = 0; ww < 8; ++ww) sum += s_red[ww][j];
+        coact[static_cast<size_t>(i) * E + j] += sum;
+        if (i != j) coact[static_cast<size_t>(j) * E + i] += sum;
     }
-    auto add = [&](uint32_t j, unsigned long long v) {
-        if (j < i || j >= E) return;
-        atomicAdd(reinterpret_cast<unsigned long long *>(coact) + static_cast<size_t>(i) * E + j, v);
-        if (i != j)
-            atomicAdd(reinterpret_cast<unsigned long long *>(coact) + static_cast<size_t>(j) * E + i,
-                      v);
-    };
-    add(j0, s0);
-    add(j0 + 1, s1);
 }
 
 template <int WORDS>
@@ -429,34 +430,31 @@ extern "C" mpb_status mpb_coactivation(mpb_context *ctx, const int32_t *idx, uin
         const uint32_t E16 = (E + 15) / 16 * 16;
         const uint32_t N0 = E16, N1 = two ? E16 - 128 : 0;
         const uint32_t E8 = two ? 256 : 128;
-        const uint64_t chunks = (T + 127) / 128;
-        // one CTA per SM (at most), >= 2 chunks each; u16 partials need
-        // <= 65535 tokens per CTA
-        static const char *env = std::getenv("MPB_COACT_CHUNKS_PER_CTA");
-        const uint64_t want = env ? std::max(1, std::atoi(env)) : 2;
-        uint64_t ctas = std::min<uint64_t>(ctx->num_sms, std::max<uint64_t>(1, chunks / want));
-        uint64_t cpc = (chunks + ctas - 1) / ctas;
-        if (cpc > 511) cpc = 511;
-        ctas = (chunks + cpc - 1) / cpc;
-        MPB_CUDA(ctx->ensure_scratch(size_t(ctas) * E8 * E8 * 2));
-        auto *partials = static_cast<uint32_t *>(ctx->scratch);
         const size_t smem = 1024 + size_t(kMmaStages) * E8 * 128 + (4 * kMmaStages + 2) * 8 +
                             size_t(kMmaStages) * 128 * k * 4;
-        static const char *dbg_env = std::getenv("MPB_COACT_DBG");
-        const uint32_t dbg = dbg_env ? std::atoi(dbg_env) : 0;
         auto kern = two ? k_coact_mma<8> : k_coact_mma<4>;
         MPB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-        kern<<<static_cast<unsigned>(ctas), kMmaThreads, smem, ctx->stream>>>(
-            idx, T, k, E, N0, N1, static_cast<uint32_t>(cpc), partials, dbg);
-        MPB_LAUNCHED(ctx);
-        dim3 rgrid(((E + 1) / 2 + 127) / 128, E, static_cast<unsigned>((ctas + 31) / 32));
-        static const bool carve = std::getenv("MPB_CARVEOUT") != nullptr;
-        if (carve)
-            MPB_CUDA(cudaFuncSetAttribute(k_coact_mma_reduce,
-                                          cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-        if (!(dbg & 128)) k_coact_mma_reduce<<<rgrid, 128, 0, ctx->stream>>>(partials, static_cast<uint32_t>(ctas), E,
+        // one CTA per SM at most, >= 2 chunks of 128 tokens each;
+        // u16 partials need <= 511 chunks per CTA: longer inputs take several
+        // launches, each accumulating into C
+        static const char *env = std::getenv("MPB_COACT_CHUNKS_PER_CTA");
+        const uint64_t want = env ? std::max(1, std::atoi(env)) : 2;
+        const uint64_t max_tokens = uint64_t(ctx->num_sms) * 511 * 128;
+        for (uint64_t t0 = 0; t0 < T; t0 += max_tokens) {
+            const uint64_t Tn = std::min<uint64_t>(max_tokens, T - t0);
+            const uint64_t chunks = (Tn + 127) / 128;
+            uint64_t ctas = std::min<uint64_t>(ctx->num_sms, std::max<uint64_t>(1, chunks / want));
+            const uint64_t cpc = (chunks + ctas - 1) / ctas;
+            ctas = (chunks + cpc - 1) / cpc;
+            MPB_CUDA(ctx->ensure_scratch(size_t(ctas) * E8 * E8 * 2));
+            auto *partials = static_cast<uint32_t *>(ctx->scratch);
+            kern<<<static_cast<unsigned>(ctas), kMmaThreads, smem, ctx->stream>>>(
+                idx + t0 * k, Tn, k, E, N0, N1, static_cast<uint32_t>(cpc), partials);
+            MPB_LAUNCHED(ctx);
+            k_coact_mma_reduce<<<E, 256, 0, ctx->stream>>>(partials, static_cast<uint32_t>(ctas), E,
                                                           E8, coact);
-        MPB_LAUNCHED(ctx);
+            MPB_LAUNCHED(ctx);
+        }
         return MPB_OK;
     }
     const uint32_t words = (E + 31) / 32;

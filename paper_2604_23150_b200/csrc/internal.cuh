@@ -55,7 +55,6 @@ struct mpb_context {
     // router split-K tail: fp32 partial accumulators + per-slot ready flags
     void *router_ws = nullptr;
     size_t router_ws_bytes = 0;
-    uint32_t router_epoch = 0;
 };
 
 struct mpb_placement {

@@ -70,7 +70,7 @@ struct RouterParams {
     uint32_t split_tail;
     uint32_t epoch;
     float *partial;      // [slot][rank][N/16 chunks][128 rows][16]
-    uint32_t *flags;     // [slot][rank] == epoch when the partial is ready
+    uint32_t *flags;     // [slot][rank]: 1 when the partial is ready, reset to 0 by the reader
 };
 
 // Work item n of a scheduling unit: full waves of whole tiles, then (split
@@ -338,6 +338,11 @@ __global__ void __launch_bounds__(kThreadsR, 1)
                     ptx::tmem_st_32x32b_x16(taddr + c, r);
                 }
                 ptx::tmem_st_wait();
+                // every epilogue thread has read the partial: re-arm the flag for the
+                // next launch (self-resetting, so CUDA-graph replays stay correct)
+                asm volatile("bar.sync 5, 256;" ::: "memory");
+                if (warp == 4 && lane == 0)
+                    asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(flag), "r"(0u) : "memory");
             }
             float tv[KMAX];
             int ti[KMAX];
@@ -578,8 +583,7 @@ mpb_status launch_router_n(mpb_context *ctx, const CUtensorMap &mx, const CUtens
             MPB_CUDA(cudaMemset(ctx->router_ws, 0, flag_bytes));
             ctx->router_ws_bytes = need;
         }
-        if (++ctx->router_epoch == 0) ctx->router_epoch = 1;
-        p.epoch = ctx->router_epoch;
+        p.epoch = 1;  // flags: 0 idle, 1 partial ready (reset by the finisher)
         p.flags = static_cast<uint32_t *>(ctx->router_ws);
         p.partial = reinterpret_cast<float *>(static_cast<char *>(ctx->router_ws) + flag_bytes);
     }

@@ -21,6 +21,7 @@ measured steps use — the paper's flow.
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass, replace
 from typing import Optional
 
@@ -156,6 +157,13 @@ class RoutingPipeline:
         self.dem_rr = self.stats[o:o + L * D * E].view(L, D, E); o += L * D * E
         self.pop = self.stats[o:o + s.domains * E].view(s.domains, E); o += s.domains * E
         self.coact = self.stats[o:o + E * E].view(E, E)
+        # co-activation runs on a side stream (own context + scratch) while the
+        # layout kernels run on the main one: both only read the layer's idx
+        self.side = None
+        self.side_mode = int(os.environ.get("MPB_SIDE_STREAM", "1"))  # 0 off, 1 coact, 2 +rr stats
+        if s.coact and self.side_mode:
+            self.side = mp.Engine(eng.device.index, stream=torch.cuda.Stream(eng.device))
+            self._fork, self._join = torch.cuda.Event(), torch.cuda.Event()
         # ---- calibration -> learned placement, routes, candidates
         self.calib = self._calibrate(progress)
         self._build_candidates()
@@ -255,6 +263,11 @@ class RoutingPipeline:
         self.fin_cl = (torch.empty(P * L, 6, dtype=torch.float64, device=dev),
                        torch.empty(P * L, D, dtype=torch.float64, device=dev))
 
+    @property
+    def launches(self) -> int:
+        """Kernels launched so far through this pipeline's contexts."""
+        return self.eng.launches + (self.side.launches if self.side is not None else 0)
+
     # ---------------------------------------------------------------- the step
     def layer_untimed(self, l: int, X: torch.Tensor):
         """layer() with the router event pair recorded by the caller (capture)."""
@@ -277,13 +290,32 @@ class RoutingPipeline:
 
     def _layer_tail(self, l: int):
         s, eng = self.spec, self.eng
+        if self.side is not None and self.side_mode == 2:
+            self._fork.record(eng.stream)
+            self.side.stream.wait_event(self._fork)
+            self.side.dispatch_layout(self.idx, self.dp_deployed, src=self.src_rr,
+                                      tag=self.dom_tok, n_tags=s.domains, permutation=False,
+                                      demand=self.dem_rr[l], tag_pop=self.pop)
+            self.side.coactivation(self.idx, s.experts, out=self.coact)
+            self._join.record(self.side.stream)
+            eng.dispatch_layout(self.idx, self.dp_deployed, src=self.src_cl,
+                                demand=self.dem_cl[l], perm_out=(self.sp, self.pp, self.ko))
+            eng.stream.wait_event(self._join)
+            return
+        if self.side is not None:  # fork: co-activation of this layer's idx
+            self._fork.record(eng.stream)
+            self.side.stream.wait_event(self._fork)
+            self.side.coactivation(self.idx, s.experts, out=self.coact)
+            self._join.record(self.side.stream)
         # deployed (cluster-routed) layout + permutation, with the round-robin
         # baseline's demand accounted in the same pass
         eng.dispatch_layout(self.idx, self.dp_deployed, src=self.src_cl, tag=self.dom_tok,
                             n_tags=s.domains, demand=self.dem_cl[l], tag_pop=self.pop,
                             perm_out=(self.sp, self.pp, self.ko), src2=self.src_rr,
                             demand2=self.dem_rr[l])
-        if s.coact:
+        if self.side is not None:  # join before the next router overwrites idx
+            eng.stream.wait_event(self._join)
+        elif s.coact:
             eng.coactivation(self.idx, s.experts, out=self.coact)
 
     def reduce_and_score(self, group=None):
@@ -332,7 +364,7 @@ class RoutingPipeline:
                 e1.record(old)
             cap = torch.cuda.Stream(eng.device)
             cap.wait_stream(old)
-            n0 = eng.launches
+            n0 = self.launches
             g_layers, g_score = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
             with torch.cuda.stream(cap):
                 eng.set_stream(cap)
@@ -346,7 +378,7 @@ class RoutingPipeline:
                 with torch.cuda.graph(g_score, stream=cap):
                     self._score_only()
             old.wait_stream(cap)
-            self.launches_per_step = eng.launches - n0  # our kernels per replayed step
+            self.launches_per_step = self.launches - n0  # our kernels per replayed step
             self.graphs = (g_layers, g_score)
             return True
         except Exception:

@@ -58,3 +58,39 @@ def test_router_ties_lowest_id(eng):
     idx, _ = eng.router_topk(X, W, k, 0, False)
     torch.cuda.synchronize()
     assert (idx.cpu() == torch.arange(k, dtype=torch.int32)).all()
+
+
+def test_router_and_coact_graph_replay(eng):
+    """Captured once, replayed on new inputs: the router's split-K tail flags and
+    the co-activation grid barrier are self-resetting, so every replay matches
+    an eager run (DSv3 shape: exercises the split tail)."""
+    T, H, E, k = 65536, 7168, 256, 8
+    g = torch.Generator(device="cuda").manual_seed(5)
+    W = (torch.randn(E, H, device="cuda", generator=g) / H ** 0.5).to(torch.bfloat16)
+    X = torch.empty(T, H, device="cuda", dtype=torch.bfloat16)
+    idx = torch.empty(T, k, dtype=torch.int32, device="cuda")
+    w = torch.empty(T, k, dtype=torch.float32, device="cuda")
+    co = torch.zeros(E, E, dtype=torch.uint64, device="cuda")
+    s = torch.cuda.Stream()
+    geng = mp.Engine(0, stream=s)
+    X.copy_(torch.randn(T, H, device="cuda", generator=g))
+    torch.cuda.synchronize()
+    with torch.cuda.stream(s):  # warm-up (allocates scratch) outside capture
+        geng.router_topk(X, W, k, 1, True, out=(idx, w))
+        geng.coactivation(idx, E, out=co)
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=s):
+        co.zero_()
+        geng.router_topk(X, W, k, 1, True, out=(idx, w))
+        geng.coactivation(idx, E, out=co)
+    for rep in range(3):
+        X.copy_(torch.randn(T, H, device="cuda", generator=g))
+        torch.cuda.synchronize()
+        graph.replay()
+        torch.cuda.synchronize()
+        ri, rw = eng.router_topk(X, W, k, 1, True)
+        rc = eng.coactivation(ri, E)
+        torch.cuda.synchronize()
+        assert torch.equal(idx, ri) and torch.equal(w, rw), rep
+        assert torch.equal(co, rc), rep

@@ -188,6 +188,10 @@ mpb_status mpb_placement_create(mpb_context *ctx, const uint32_t *groups_flat,
         }
     std::vector<uint8_t> g2n(D);
     for (uint32_t d = 0; d < D; ++d) g2n[d] = static_cast<uint8_t>(group_to_node[d]);
+    std::vector<uint16_t> cell_slot(size_t(D) * E);
+    for (uint32_t d = 0; d < D; ++d)
+        for (uint32_t e = 0; e < E; ++e)
+            cell_slot[size_t(d) * E + e] = slot_lut[size_t(group_to_node[d]) * E + e];
 
     auto *p = new mpb_placement();
     p->ctx = ctx;
@@ -202,6 +206,10 @@ mpb_status mpb_placement_create(mpb_context *ctx, const uint32_t *groups_flat,
     if (e == cudaSuccess) e = cudaMalloc(&p->d_slot_lut, slot_lut.size() * 2);
     if (e == cudaSuccess) e = cudaMalloc(&p->d_key_lb, key_lb.size() * 2);
     if (e == cudaSuccess) e = cudaMalloc(&p->d_g2n, D);
+    if (e == cudaSuccess) e = cudaMalloc(&p->d_cell_slot, cell_slot.size() * 2);
+    if (e == cudaSuccess)
+        e = cudaMemcpy(p->d_cell_slot, cell_slot.data(), cell_slot.size() * 2,
+                       cudaMemcpyHostToDevice);
     if (e == cudaSuccess)
         e = cudaMemcpy(p->d_dest_lut, lut.data(), lut.size(), cudaMemcpyHostToDevice);
     if (e == cudaSuccess)
@@ -223,6 +231,7 @@ mpb_status mpb_placement_destroy(mpb_placement *p) {
     cudaFree(p->d_dest_lut);
     cudaFree(p->d_slot_lut);
     cudaFree(p->d_key_lb);
+    cudaFree(p->d_cell_slot);
     cudaFree(p->d_g2n);
     delete p;
     return MPB_OK;

@@ -63,6 +63,7 @@ struct mpb_placement {
     uint8_t *d_dest_lut = nullptr;   // [nodes][E] destination group, 255 = uncovered
     uint16_t *d_slot_lut = nullptr;  // [nodes][E] slot id of (dest, e), 0xFFFF = uncovered
     uint16_t *d_key_lb = nullptr;    // [D*E + 1] first slot with key >= d*E+e
+    uint16_t *d_cell_slot = nullptr; // [D][E] slot of a pair from source group s to expert e
     uint8_t *d_g2n = nullptr;        // [D]
     std::vector<uint8_t> h_dest_lut;
     std::vector<uint32_t> h_g2n;

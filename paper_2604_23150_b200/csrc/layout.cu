@@ -11,23 +11,26 @@
 //                same tokens, tag_pop[tag][e]); the block's slot counts are
 //                derived from its demand cells (one add per non-zero cell, not
 //                per pair); bins flushed with one global atomic each, slot
-//                counts written slot-major as bhist[slot][block].
-//   2. scan    : one CTA per slot scans its row of bhist (exclusive, in place)
-//                and writes the slot total.
+//                counts written block-major as bhist[block][slot].
+//   2. scan    : one CTA per 32 slots scans their bhist columns down the block
+//                axis (exclusive, in place) and writes the slot totals.
 //   3. scatter : every block scans the NS slot totals in smem (slot bases; block
 //                0 emits key_offsets), re-reads its chunk (L2-resident), ranks
 //                pairs stably inside each warp (warp-aggregated per-warp
 //                counters, then __match_any_sync + popc of lower lanes) and
 //                writes sorted_pairs / pair_pos.
 // Algorithmic bytes per pair: 4 (idx) + 8 (perm out) [+ 1/k src + 1/k tag].
+#include <algorithm>
+#include <cstdlib>
+
 #include "internal.cuh"
 
 namespace mpb {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kChunk = 2048;  // pairs per block
 constexpr int kWarps = kThreads / 32;
+constexpr uint32_t kChunkQuantum = kWarps * 128;  // block chunks: multiples of 1024 pairs
 constexpr uint32_t kNone = 0xFFFFFFFFu;
 
 struct LayoutParams {
@@ -42,15 +45,19 @@ struct LayoutParams {
     const uint8_t *src2;
     const uint8_t *g2n;
     const uint16_t *slot_lut;
+    const uint16_t *cell_slot;  // [D][E]: slot of a pair from source group s to expert e
     uint32_t D, E, NS;
     uint64_t *demand;
     uint64_t *demand2;
     uint64_t *tag_pop;
-    uint32_t *bhist;   // [NS][nblocks] slot-major
+    uint32_t *bhist;   // [nblocks][NS] block-major
     uint32_t *totals;  // [NS]
     uint32_t nb;
+    uint32_t chunk;     // pairs per block (multiple of kChunkQuantum)
+    uint32_t key_bits;  // bits of a slot id with kNone mapped to all-ones (NS < 2^key_bits - 1)
     uint32_t *err;
     int demand_smem;
+    int cell_smem;
     int demand2_smem;
     int tag_smem;
 };
@@ -148,16 +155,21 @@ __global__ void __launch_bounds__(kThreads) k_layout_count(LayoutParams p) {
     uint32_t *s_slot = s_tag + (p.tag_smem ? p.n_tags * p.E : 0);
     const uint32_t nsm = (p.demand_smem ? DE : 0) + (p.demand2_smem ? DE : 0) +
                          (p.tag_smem ? p.n_tags * p.E : 0) + (kPerm ? p.NS : 0);
+    // the (source, expert) -> slot table, staged for the flush
+    uint16_t *s_cell = reinterpret_cast<uint16_t *>(sm + nsm);
+    if (kPerm && p.cell_smem)
+        for (uint32_t i = threadIdx.x; i < DE; i += kThreads) s_cell[i] = __ldg(p.cell_slot + i);
     for (uint32_t i = threadIdx.x; i < nsm; i += kThreads) sm[i] = 0;
     __syncthreads();
 
-    const uint32_t base = blockIdx.x * kChunk;
+    const uint32_t base = blockIdx.x * p.chunk;
     const uint32_t P = static_cast<uint32_t>(p.P);
+    const uint32_t rounds = p.chunk / (kThreads * 4);
     if (p.demand_smem && (!p.src2 || p.demand2_smem) && (!p.tag || p.tag_smem)) {
         // fast path: every histogram is block-private; coverage is checked per
         // non-zero cell at flush time instead of per pair
-#pragma unroll
-        for (int h = 0; h < kChunk / (kThreads * 4); ++h) {
+#pragma unroll 2
+        for (uint32_t h = 0; h < rounds; ++h) {
             const uint32_t q = base + h * kThreads * 4 + threadIdx.x * 4;
             if (q >= P) break;
             int32_t v[4];
@@ -188,8 +200,7 @@ __global__ void __launch_bounds__(kThreads) k_layout_count(LayoutParams p) {
             }
         }
     } else {
-#pragma unroll
-    for (int h = 0; h < kChunk / (kThreads * 4); ++h) {
+    for (uint32_t h = 0; h < rounds; ++h) {
         const uint64_t q = base + static_cast<uint64_t>(h) * kThreads * 4 + threadIdx.x * 4;
         int32_t v[4];
         load4(p.idx, q, p.P, v);
@@ -232,12 +243,12 @@ __global__ void __launch_bounds__(kThreads) k_layout_count(LayoutParams p) {
     }
     __syncthreads();
     if (p.demand_smem) {
+#pragma unroll 4
         for (uint32_t i = threadIdx.x; i < DE; i += kThreads) {
             const uint32_t c = s_demand[i];
-            if (!c) continue;
             // the block's slot counts (and coverage) from its (src, expert) cells
-            const uint32_t sg = i / p.E, e = i - sg * p.E;
-            const uint16_t slot = __ldg(p.slot_lut + static_cast<size_t>(p.g2n[sg]) * p.E + e);
+            const uint16_t slot = (kPerm && p.cell_smem) ? s_cell[i] : __ldg(p.cell_slot + i);
+            if (!c) continue;
             if (slot == 0xFFFF) {
                 atomicOr(p.err, kErrUncovered);
                 continue;
@@ -248,11 +259,13 @@ __global__ void __launch_bounds__(kThreads) k_layout_count(LayoutParams p) {
         }
     }
     if (p.demand2_smem)
+#pragma unroll 4
         for (uint32_t i = threadIdx.x; i < DE; i += kThreads)
             if (s_demand2[i])
                 atomicAdd(reinterpret_cast<unsigned long long *>(p.demand2) + i,
                           static_cast<unsigned long long>(s_demand2[i]));
     if (p.tag && p.tag_smem)
+#pragma unroll 4
         for (uint32_t i = threadIdx.x; i < p.n_tags * p.E; i += kThreads)
             if (s_tag[i])
                 atomicAdd(reinterpret_cast<unsigned long long *>(p.tag_pop) + i,
@@ -260,7 +273,7 @@ __global__ void __launch_bounds__(kThreads) k_layout_count(LayoutParams p) {
     if (kPerm) {
         __syncthreads();
         for (uint32_t sl = threadIdx.x; sl < p.NS; sl += kThreads)
-            p.bhist[static_cast<size_t>(sl) * p.nb + blockIdx.x] = s_slot[sl];
+            p.bhist[static_cast<size_t>(blockIdx.x) * p.NS + sl] = s_slot[sl];
     }
 }
 
@@ -291,21 +304,53 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t *s_warp
     return r;
 }
 
-// One CTA per slot: exclusive scan of bhist[slot][0..nb) in place + total.
+// One CTA per 32 slots: exclusive scan down the block axis of bhist[.][slot]
+// in place + slot totals. Lane = slot (coalesced 128-byte rows); warp w owns a
+// contiguous range of blocks: per-warp sums, prefix over warps, then rewrite.
 __global__ void __launch_bounds__(kThreads) k_layout_scan(uint32_t *bhist, uint32_t nb,
-                                                          uint32_t *totals) {
-    __shared__ uint32_t s_warp[32];
-    uint32_t *row = bhist + static_cast<size_t>(blockIdx.x) * nb;
-    uint32_t carry = 0;
-    for (uint32_t i0 = 0; i0 < nb; i0 += kThreads) {
-        const uint32_t i = i0 + threadIdx.x;
-        const uint32_t v = i < nb ? row[i] : 0;
-        uint32_t tot;
-        const uint32_t ex = block_excl_scan(v, s_warp, tot);
-        if (i < nb) row[i] = carry + ex;
-        carry += tot;
+                                                          uint32_t NS, uint32_t *totals) {
+    __shared__ uint32_t s_part[kWarps][32];
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t slot = blockIdx.x * 32 + lane;
+    const bool ok = slot < NS;
+    const uint32_t per = (nb + kWarps - 1) / kWarps;
+    const uint32_t b0 = min(nb, warp * per), b1 = min(nb, b0 + per);
+    uint32_t *col = bhist + slot;
+    uint32_t sum = 0;
+    if (ok) {
+        uint32_t b = b0;
+        for (; b + 8 <= b1; b += 8) {
+            uint32_t v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = col[static_cast<size_t>(b + u) * NS];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) sum += v[u];
+        }
+        for (; b < b1; ++b) sum += col[static_cast<size_t>(b) * NS];
     }
-    if (threadIdx.x == 0) totals[blockIdx.x] = carry;
+    s_part[warp][lane] = sum;
+    __syncthreads();
+    uint32_t run = 0;
+    for (uint32_t w = 0; w < warp; ++w) run += s_part[w][lane];
+    if (warp == kWarps - 1 && ok) totals[slot] = run + sum;
+    if (ok) {
+        uint32_t b = b0;
+        for (; b + 8 <= b1; b += 8) {
+            uint32_t v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = col[static_cast<size_t>(b + u) * NS];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                col[static_cast<size_t>(b + u) * NS] = run;
+                run += v[u];
+            }
+        }
+        for (; b < b1; ++b) {
+            const uint32_t v = col[static_cast<size_t>(b) * NS];
+            col[static_cast<size_t>(b) * NS] = run;
+            run += v;
+        }
+    }
 }
 
 __global__ void __launch_bounds__(kThreads) k_layout_scatter(LayoutParams p, int32_t *sorted_pairs,
@@ -313,37 +358,40 @@ __global__ void __launch_bounds__(kThreads) k_layout_scatter(LayoutParams p, int
                                                              const uint16_t *key_lb,
                                                              uint32_t nkeys,
                                                              int64_t *key_offsets) {
-    extern __shared__ uint32_t s_w[];  // [kWarps][NS] running positions, then [NS+1] bases
+    extern __shared__ uint32_t s_w[];  // [kWarps][NS] per-warp counts / positions, [NS+1] bases
     __shared__ uint32_t s_warp[32];
     uint32_t *s_base = s_w + kWarps * p.NS;
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // slot bases: exclusive scan of the slot totals (coalesced loads into smem,
+    // then a blocked scan; every block, NS is small)
+    for (uint32_t i = threadIdx.x; i < p.NS; i += kThreads) s_base[i] = __ldg(p.totals + i);
     for (uint32_t i = threadIdx.x; i < kWarps * p.NS; i += kThreads) s_w[i] = 0;
-    // slot bases: exclusive scan of the slot totals (every block; NS is small)
+    __syncthreads();
     {
         const uint32_t per = (p.NS + kThreads - 1) / kThreads;
         const uint32_t lo = min(p.NS, threadIdx.x * per), hi = min(p.NS, lo + per);
         uint32_t local = 0;
-        for (uint32_t i = lo; i < hi; ++i) local += p.totals[i];
+        for (uint32_t i = lo; i < hi; ++i) local += s_base[i];
         uint32_t grand;
         uint32_t run = block_excl_scan(local, s_warp, grand);
         for (uint32_t i = lo; i < hi; ++i) {
+            const uint32_t t = s_base[i];
             s_base[i] = run;
-            run += p.totals[i];
+            run += t;
         }
         if (threadIdx.x == 0) s_base[p.NS] = grand;
     }
     __syncthreads();
     if (blockIdx.x == 0 && key_offsets)
         for (uint32_t key = threadIdx.x; key <= nkeys; key += kThreads)
-            key_offsets[key] = static_cast<int64_t>(s_base[key_lb[key]]);
+            key_offsets[key] = static_cast<int64_t>(s_base[__ldg(key_lb + key)]);
 
-    // each warp owns 256 consecutive pairs: two 128-bit loads per lane
-    const uint32_t wbase = blockIdx.x * kChunk + warp * 256u;
+    // each warp owns chunk/kWarps consecutive pairs, walked in groups of 128
+    // (one 128-bit load of 4 pairs per lane)
+    const uint32_t wchunk = p.chunk / kWarps;
+    const uint32_t wbase = blockIdx.x * p.chunk + warp * wchunk;
     const uint32_t P = static_cast<uint32_t>(p.P);
-    uint32_t sl[2][4];
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-        const uint32_t q = wbase + h * 128 + lane * 4;
+    auto slots_of = [&](uint32_t q, uint32_t (&sl)[4]) {
         int32_t v[4];
         load4(p.idx, q, p.P, v);
         TokenCursor tc;
@@ -355,19 +403,33 @@ __global__ void __launch_bounds__(kThreads) k_layout_scatter(LayoutParams p, int
             if (q + c < P) {
                 if (c) cursor_next(p, tc);
                 if (static_cast<uint32_t>(v[c]) < p.E && tc.src < p.D) {
-                    const uint16_t s16 =
-                        __ldg(p.slot_lut + static_cast<size_t>(__ldg(p.g2n + tc.src)) * p.E + v[c]);
+                    const uint16_t s16 = __ldg(p.cell_slot + tc.src * p.E + v[c]);
                     slot = s16 == 0xFFFF ? kNone : s16;
                 }
             }
-            sl[h][c] = slot;
-            agg_add(s_w + warp * p.NS, slot);
+            sl[c] = slot;
         }
+    };
+    // the first kKeep groups keep their slots in registers for the ranking pass
+    constexpr uint32_t kKeep = 4;
+    uint32_t keep[kKeep][4];
+    auto count_group = [&](uint32_t g, uint32_t (&sl)[4]) {
+        slots_of(wbase + g + lane * 4, sl);
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+            if (sl[c] != kNone) atomicAdd(s_w + warp * p.NS + sl[c], 1u);
+    };
+#pragma unroll
+    for (uint32_t gi = 0; gi < kKeep; ++gi)
+        if (gi * 128 < wchunk) count_group(gi * 128, keep[gi]);
+    for (uint32_t g = kKeep * 128; g < wchunk; g += 128) {
+        uint32_t sl[4];
+        count_group(g, sl);
     }
     __syncthreads();
     // per slot: exclusive prefix over warps, seeded with the block's global offset
     for (uint32_t s = threadIdx.x; s < p.NS; s += kThreads) {
-        uint32_t run = s_base[s] + p.bhist[static_cast<size_t>(s) * p.nb + blockIdx.x];
+        uint32_t run = s_base[s] + p.bhist[static_cast<size_t>(blockIdx.x) * p.NS + s];
 #pragma unroll
         for (int w = 0; w < kWarps; ++w) {
             const uint32_t c = s_w[w * p.NS + s];
@@ -378,29 +440,45 @@ __global__ void __launch_bounds__(kThreads) k_layout_scatter(LayoutParams p, int
     __syncthreads();
     uint32_t *mine = s_w + warp * p.NS;
     const unsigned lt = (1u << lane) - 1u;
+    auto rank_group = [&](uint32_t g, const uint32_t (&sl)[4]) {
 #pragma unroll
-    for (int r = 0; r < 8; ++r) {
-        // round r covers pairs wbase + 32r + lane, held by lane (r%4)*8 + lane/4,
-        // component lane%4 of load half r/4
-        const int h = r / 4;
-        const int srcl = (r % 4) * 8 + (lane >> 2);
-        uint32_t cand[4];
+        for (int r = 0; r < 4; ++r) {
+            // round r covers pairs wbase + g + 32r + lane, held by lane 8r + lane/4,
+            // component lane%4
+            const int srcl = r * 8 + (lane >> 2);
+            uint32_t cand[4];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) cand[c] = __shfl_sync(0xffffffffu, sl[h][c], srcl);
-        const uint32_t c4 = lane & 3;
-        const uint32_t slot = c4 == 0 ? cand[0] : c4 == 1 ? cand[1] : c4 == 2 ? cand[2] : cand[3];
-        const unsigned peers = __match_any_sync(0xffffffffu, slot);
-        uint32_t pos = 0;
-        if (slot != kNone) pos = mine[slot] + __popc(peers & lt);
-        __syncwarp();
-        if (slot != kNone && lane == static_cast<uint32_t>(__ffs(peers) - 1))
-            mine[slot] += __popc(peers);
-        __syncwarp();
-        if (slot != kNone) {
-            const uint64_t pair = wbase + r * 32 + lane;
-            sorted_pairs[pos] = static_cast<int32_t>(pair);
-            pair_pos[pair] = static_cast<int32_t>(pos);
+            for (int c = 0; c < 4; ++c) cand[c] = __shfl_sync(0xffffffffu, sl[c], srcl);
+            const uint32_t c4 = lane & 3;
+            const uint32_t slot = c4 == 0 ? cand[0] : c4 == 1 ? cand[1] : c4 == 2 ? cand[2] : cand[3];
+            // lanes holding the same slot: AND of per-bit ballots (short, independent
+            // ballots pipeline better than one long-latency MATCH.ANY)
+            const uint32_t key = slot == kNone ? (1u << p.key_bits) - 1u : slot;
+            unsigned peers = 0xffffffffu;
+            for (uint32_t b = 0; b < p.key_bits; ++b) {
+                const unsigned m = __ballot_sync(0xffffffffu, (key >> b) & 1u);
+                peers &= ((key >> b) & 1u) ? m : ~m;
+            }
+            uint32_t pos = 0;
+            if (slot != kNone) pos = mine[slot] + __popc(peers & lt);
+            __syncwarp();
+            if (slot != kNone && lane == static_cast<uint32_t>(__ffs(peers) - 1))
+                mine[slot] += __popc(peers);
+            __syncwarp();
+            if (slot != kNone) {
+                const uint32_t pair = wbase + g + r * 32 + lane;
+                sorted_pairs[pos] = static_cast<int32_t>(pair);
+                pair_pos[pair] = static_cast<int32_t>(pos);
+            }
         }
+    };
+#pragma unroll
+    for (uint32_t gi = 0; gi < kKeep; ++gi)
+        if (gi * 128 < wchunk) rank_group(gi * 128, keep[gi]);
+    for (uint32_t g = kKeep * 128; g < wchunk; g += 128) {
+        uint32_t sl[4];
+        slots_of(wbase + g + lane * 4, sl);
+        rank_group(g, sl);
     }
 }
 
@@ -493,6 +571,7 @@ mpb_status launch_layout(mpb_context *ctx, const mpb_tokens *tk, const mpb_place
     p.src2 = tk->src_group2;
     p.g2n = pl->d_g2n;
     p.slot_lut = pl->d_slot_lut;
+    p.cell_slot = pl->d_cell_slot;
     p.D = pl->D;
     p.E = pl->E;
     p.NS = pl->NS;
@@ -508,8 +587,20 @@ mpb_status launch_layout(mpb_context *ctx, const mpb_tokens *tk, const mpb_place
     if (p.demand2_smem) smem += DE4;
     p.tag_smem = p.n_tags && smem + size_t(p.n_tags) * pl->E * 4 <= kSmemLimit;
     if (p.tag_smem) smem += size_t(p.n_tags) * pl->E * 4;
-    const uint32_t nb = static_cast<uint32_t>((P + kChunk - 1) / kChunk);
+    const size_t cell4 = (size_t(pl->D) * pl->E + 1) / 2 * 4;
+    p.cell_smem = perm && p.demand_smem && smem + cell4 <= kSmemLimit;
+    if (p.cell_smem) smem += cell4;
+    // about one block per SM: per-block histogram zero/flush and slot-count
+    // work scale with D*E and NS, so fewer, fatter blocks amortise them
+    static const char *cenv = std::getenv("MPB_LAYOUT_BLOCKS_PER_SM");
+    const uint64_t want_blocks = uint64_t(ctx->num_sms) * (cenv ? std::max(1, std::atoi(cenv)) : 2);
+    uint64_t chunk = (P + want_blocks - 1) / want_blocks;
+    chunk = std::max<uint64_t>(kChunkQuantum, (chunk + kChunkQuantum - 1) / kChunkQuantum * kChunkQuantum);
+    const uint32_t nb = static_cast<uint32_t>((P + chunk - 1) / chunk);
     p.nb = nb;
+    p.chunk = static_cast<uint32_t>(chunk);
+    p.key_bits = 1;
+    while ((1u << p.key_bits) - 1u <= pl->NS) ++p.key_bits;
     if (perm) {
         MPB_CUDA(ctx->ensure_scratch((size_t(nb) + 1) * pl->NS * 4 + 256));
         p.bhist = static_cast<uint32_t *>(ctx->scratch);
@@ -520,7 +611,7 @@ mpb_status launch_layout(mpb_context *ctx, const mpb_tokens *tk, const mpb_place
     count<<<nb, kThreads, smem, ctx->stream>>>(p);
     MPB_LAUNCHED(ctx);
     if (!perm) return MPB_OK;
-    k_layout_scan<<<pl->NS, kThreads, 0, ctx->stream>>>(p.bhist, nb, p.totals);
+    k_layout_scan<<<(pl->NS + 31) / 32, kThreads, 0, ctx->stream>>>(p.bhist, nb, pl->NS, p.totals);
     MPB_LAUNCHED(ctx);
     const size_t sc_smem = (size_t(kWarps) * pl->NS + pl->NS + 1) * 4;
     MPB_CUDA(cudaFuncSetAttribute(k_layout_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,

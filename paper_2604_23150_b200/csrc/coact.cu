@@ -224,6 +224,8 @@ __global__ void __launch_bounds__(kMmaThreads, 1)
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = *s_tmem;
+    pdl_trigger();
+    pdl_wait();  // ids (previous kernels) and the partials buffer (WAR) from here on
 
     const uint64_t tok0 = static_cast<uint64_t>(blockIdx.x) * chunks_per_cta * 128;
     const uint64_t tok1 = min(T, tok0 + static_cast<uint64_t>(chunks_per_cta) * 128);
@@ -358,6 +360,8 @@ __global__ void __launch_bounds__(256) k_coact_mma_reduce(const uint32_t *partia
                                                           uint32_t E, uint32_t kRows,
                                                           uint64_t *coact) {
     __shared__ uint32_t s_red[8][256];
+    pdl_trigger();
+    pdl_wait();
     const uint32_t i = blockIdx.x, w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const size_t pstride = static_cast<size_t>(kRows) * kRows / 8;  // uint4 per partial
     uint32_t acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -448,11 +452,12 @@ extern "C" mpb_status mpb_coactivation(mpb_context *ctx, const int32_t *idx, uin
             ctas = (chunks + cpc - 1) / cpc;
             MPB_CUDA(ctx->ensure_scratch(size_t(ctas) * E8 * E8 * 2));
             auto *partials = static_cast<uint32_t *>(ctx->scratch);
-            kern<<<static_cast<unsigned>(ctas), kMmaThreads, smem, ctx->stream>>>(
-                idx + t0 * k, Tn, k, E, N0, N1, static_cast<uint32_t>(cpc), partials);
+            MPB_CUDA(launch_pdl(kern, dim3(static_cast<unsigned>(ctas)), dim3(kMmaThreads), smem,
+                                ctx->stream, idx + t0 * k, Tn, k, E, N0, N1,
+                                static_cast<uint32_t>(cpc), partials));
             MPB_LAUNCHED(ctx);
-            k_coact_mma_reduce<<<E, 256, 0, ctx->stream>>>(partials, static_cast<uint32_t>(ctas), E,
-                                                          E8, coact);
+            MPB_CUDA(launch_pdl(k_coact_mma_reduce, dim3(E), dim3(256), 0, ctx->stream, partials,
+                                static_cast<uint32_t>(ctas), E, E8, coact));
             MPB_LAUNCHED(ctx);
         }
         return MPB_OK;

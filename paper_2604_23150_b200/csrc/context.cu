@@ -7,6 +7,7 @@
 // into a [nodes x E] destination table so every kernel resolves a pair with a
 // single byte load.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "internal.cuh"
@@ -18,6 +19,14 @@ thread_local std::string g_last_error;
 }
 
 void set_error(const std::string &msg) { g_last_error = msg; }
+
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char *e = std::getenv("MPB_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
 
 mpb_status fail(mpb_status code, const std::string &msg) {
     g_last_error = msg;

@@ -40,6 +40,34 @@ mpb_status cuda_fail(cudaError_t err, const char *where);
         if (e_ != cudaSuccess) return ::mpb::cuda_fail(e_, "kernel launch");               \
     } while (0)
 
+// Programmatic dependent launch: kernels launched with launch_pdl may start
+// (prologue: smem zeroing, TMEM alloc, barrier init) while the previous kernel
+// in the stream drains; each calls pdl_wait() before touching global data the
+// previous kernels produce or read, and pdl_trigger() once every CTA is running.
+// MPB_PDL=0 disables the attribute (the device calls are then no-ops).
+bool pdl_enabled();
+
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t stream, Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 }  // namespace mpb
 
 struct mpb_context {

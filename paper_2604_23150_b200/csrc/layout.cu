@@ -157,9 +157,11 @@ __global__ void __launch_bounds__(kThreads) k_layout_count(LayoutParams p) {
                          (p.tag_smem ? p.n_tags * p.E : 0) + (kPerm ? p.NS : 0);
     // the (source, expert) -> slot table, staged for the flush
     uint16_t *s_cell = reinterpret_cast<uint16_t *>(sm + nsm);
-    if (kPerm && p.cell_smem)
+    pdl_trigger();
+    if (kPerm && p.cell_smem)  // placement data: not produced by earlier kernels
         for (uint32_t i = threadIdx.x; i < DE; i += kThreads) s_cell[i] = __ldg(p.cell_slot + i);
     for (uint32_t i = threadIdx.x; i < nsm; i += kThreads) sm[i] = 0;
+    pdl_wait();
     __syncthreads();
 
     const uint32_t base = blockIdx.x * p.chunk;
@@ -310,6 +312,8 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t *s_warp
 __global__ void __launch_bounds__(kThreads) k_layout_scan(uint32_t *bhist, uint32_t nb,
                                                           uint32_t NS, uint32_t *totals) {
     __shared__ uint32_t s_part[kWarps][32];
+    pdl_trigger();
+    pdl_wait();
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t slot = blockIdx.x * 32 + lane;
     const bool ok = slot < NS;
@@ -364,8 +368,10 @@ __global__ void __launch_bounds__(kThreads) k_layout_scatter(LayoutParams p, int
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     // slot bases: exclusive scan of the slot totals (coalesced loads into smem,
     // then a blocked scan; every block, NS is small)
-    for (uint32_t i = threadIdx.x; i < p.NS; i += kThreads) s_base[i] = __ldg(p.totals + i);
+    pdl_trigger();
     for (uint32_t i = threadIdx.x; i < kWarps * p.NS; i += kThreads) s_w[i] = 0;
+    pdl_wait();
+    for (uint32_t i = threadIdx.x; i < p.NS; i += kThreads) s_base[i] = __ldcg(p.totals + i);
     __syncthreads();
     {
         const uint32_t per = (p.NS + kThreads - 1) / kThreads;
@@ -608,17 +614,17 @@ mpb_status launch_layout(mpb_context *ctx, const mpb_tokens *tk, const mpb_place
     }
     auto count = perm ? k_layout_count<true> : k_layout_count<false>;
     MPB_CUDA(cudaFuncSetAttribute(count, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    count<<<nb, kThreads, smem, ctx->stream>>>(p);
+    MPB_CUDA(launch_pdl(count, dim3(nb), dim3(kThreads), smem, ctx->stream, p));
     MPB_LAUNCHED(ctx);
     if (!perm) return MPB_OK;
-    k_layout_scan<<<(pl->NS + 31) / 32, kThreads, 0, ctx->stream>>>(p.bhist, nb, pl->NS, p.totals);
+    MPB_CUDA(launch_pdl(k_layout_scan, dim3((pl->NS + 31) / 32), dim3(kThreads), 0, ctx->stream,
+                        p.bhist, nb, pl->NS, p.totals));
     MPB_LAUNCHED(ctx);
     const size_t sc_smem = (size_t(kWarps) * pl->NS + pl->NS + 1) * 4;
     MPB_CUDA(cudaFuncSetAttribute(k_layout_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(sc_smem)));
-    k_layout_scatter<<<nb, kThreads, sc_smem, ctx->stream>>>(p, sorted_pairs, pair_pos,
-                                                             pl->d_key_lb, pl->D * pl->E,
-                                                             key_offsets);
+    MPB_CUDA(launch_pdl(k_layout_scatter, dim3(nb), dim3(kThreads), sc_smem, ctx->stream, p,
+                        sorted_pairs, pair_pos, pl->d_key_lb, pl->D * pl->E, key_offsets));
     MPB_LAUNCHED(ctx);
     return MPB_OK;
 }

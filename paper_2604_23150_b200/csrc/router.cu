@@ -189,6 +189,10 @@ __global__ void __launch_bounds__(kThreadsR, 1)
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     const uint32_t nk = p.H / kBK;
+    // PDL: setup above overlapped the previous kernel; X, W, idx/w and the
+    // split-tail workspace are touched only after it completed
+    pdl_trigger();
+    pdl_wait();
 
     if (warp == 0 && lane == 0) {
         // ---------------- TMA producer ----------------
@@ -550,7 +554,7 @@ mpb_status launch_router_n(mpb_context *ctx, const CUtensorMap &mx, const CUtens
     auto kern = k_router<N, KMAX, PAIR>;
     MPB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     cudaLaunchConfig_t cfg{};
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     cfg.blockDim = dim3(kThreadsR);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = ctx->stream;
@@ -597,6 +601,13 @@ mpb_status launch_router_n(mpb_context *ctx, const CUtensorMap &mx, const CUtens
         cfg.numAttrs = 1;
     } else {
         cfg.gridDim = dim3(units);
+        cfg.attrs = attr;
+        cfg.numAttrs = 0;
+    }
+    if (pdl_enabled()) {
+        attr[cfg.numAttrs].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[cfg.numAttrs].val.programmaticStreamSerializationAllowed = 1;
+        ++cfg.numAttrs;
     }
     MPB_CUDA(cudaLaunchKernelEx(&cfg, kern, mx, mw, p));
     MPB_LAUNCHED(ctx);

@@ -265,6 +265,19 @@ MPB_API mpb_status mpb_kmeans(const double *rows, uint64_t n, uint32_t dim, uint
                               uint64_t seed, uint32_t max_iterations, double tolerance,
                               uint32_t *labels_out /* n */, double *centroids_out /* K*dim */,
                               double *objective_out, uint32_t *iterations_out);
+/* Device k-means (K7): same algorithm, order of operations and RNG draws as
+ * kmeans / l2_normalize_rows (clustering.cpp:15-230) — bit-identical labels,
+ * centroids and objective — on caller-owned device buffers, in ctx's stream
+ * (returns after the stream has drained: the Lloyd loop is host-driven). */
+MPB_API mpb_status mpb_l2_normalize_rows_device(mpb_context *ctx, const double *matrix /* dev */,
+                                                uint64_t rows, uint32_t cols,
+                                                double *out /* dev */);
+MPB_API mpb_status mpb_kmeans_device(mpb_context *ctx, const double *rows /* dev n*dim */,
+                                     uint64_t n, uint32_t dim, uint32_t K, uint64_t seed,
+                                     uint32_t max_iterations, double tolerance,
+                                     uint32_t *labels /* dev n */, double *centroids /* dev K*dim */,
+                                     double *objective_out /* host */,
+                                     uint32_t *iterations_out /* host */);
 MPB_API mpb_status mpb_assign_clusters_to_groups(const uint32_t *labels, uint64_t n, uint32_t K,
                                                  const double *raw, uint32_t dim, uint32_t D,
                                                  uint64_t seed, uint32_t *assign_flat /* <= K*D */,

@@ -74,6 +74,9 @@ _SIGS = {
     "mpb_l2_normalize_rows": (C.c_int, [_p, C.c_uint64, C.c_uint32, _p]),
     "mpb_kmeans": (C.c_int, [_p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint32,
                              C.c_double, _p, _p, _p, _p]),
+    "mpb_l2_normalize_rows_device": (C.c_int, [_p, _p, C.c_uint64, C.c_uint32, _p]),
+    "mpb_kmeans_device": (C.c_int, [_p, _p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint64,
+                                    C.c_uint32, C.c_double, _p, _p, _p, _p]),
     "mpb_assign_clusters_to_groups": (C.c_int, [_p, C.c_uint64, C.c_uint32, _p, C.c_uint32,
                                                 C.c_uint32, C.c_uint64, _p, _p, _p]),
     "mpb_trace_parse": (C.c_int, [C.c_char_p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32,

@@ -95,6 +95,7 @@ mpb_status mpb_context_destroy(mpb_context *ctx) {
     if (ctx->d_error) cudaFree(ctx->d_error);
     if (ctx->scratch) cudaFree(ctx->scratch);
     if (ctx->router_ws) cudaFree(ctx->router_ws);
+    if (ctx->pinned) cudaFreeHost(ctx->pinned);
     delete ctx;
     return MPB_OK;
 }

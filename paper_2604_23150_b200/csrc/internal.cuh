@@ -83,6 +83,8 @@ struct mpb_context {
     // router split-K tail: fp32 partial accumulators + per-slot ready flags
     void *router_ws = nullptr;
     size_t router_ws_bytes = 0;
+    void *pinned = nullptr;  // small pinned host area (k-means control values)
+    size_t pinned_bytes = 0;
 };
 
 struct mpb_placement {

@@ -167,6 +167,37 @@ def kmeans(rows, n_rows: int, dim: int, K: int, seed: int, max_iterations: int =
                         int(it[0]))
 
 
+def kmeans_device(engine, rows, n_rows: int, dim: int, K: int, seed: int,
+                  max_iterations: int = 100, tolerance: float = 1e-6) -> ClusterModel:
+    """kmeans() on the GPU (K7, bit-identical): `rows` is a device tensor
+    [n_rows, dim] float64 (already l2-normalised) or host values."""
+    import torch
+    x = rows if isinstance(rows, torch.Tensor) else torch.from_numpy(_f64(rows).reshape(-1))
+    x = x.to(device=engine.device, dtype=torch.float64).contiguous().view(-1)
+    if x.numel() != n_rows * dim:
+        raise ValidationError("kmeans: rows span size does not match n_rows * dim")
+    labels = torch.zeros(max(1, n_rows), dtype=torch.int32, device=engine.device)
+    cent = torch.zeros(max(1, K * dim), dtype=torch.float64, device=engine.device)
+    obj = np.zeros(1)
+    it = np.zeros(1, np.uint32)
+    _abi.call("mpb_kmeans_device", engine.ctx, C.c_void_p(x.data_ptr()), n_rows, dim, K, seed,
+              max_iterations, tolerance, C.c_void_p(labels.data_ptr()),
+              C.c_void_p(cent.data_ptr()), _p(obj), _p(it))
+    return ClusterModel(K, labels[:n_rows].cpu().numpy().astype(np.uint32),
+                        cent[: K * dim].cpu().numpy().reshape(K, dim), dim, float(obj[0]),
+                        int(it[0]))
+
+
+def l2_normalize_rows_device(engine, values):
+    """l2_normalize_rows on the GPU: device float64 tensor [rows, cols] -> same."""
+    import torch
+    x = values.to(device=engine.device, dtype=torch.float64).contiguous()
+    out = torch.empty_like(x)
+    _abi.call("mpb_l2_normalize_rows_device", engine.ctx, C.c_void_p(x.data_ptr()), x.shape[0],
+              x.shape[1], C.c_void_p(out.data_ptr()))
+    return out
+
+
 def assign_clusters_to_groups(model: ClusterModel, raw_matrix: ActivationMatrix, D: int,
                               seed: int) -> GroupMap:
     if raw_matrix.rows != len(model.labels):
@@ -201,17 +232,27 @@ class ClusterStage:
 
 
 def run_cluster_stage(matrix: ActivationMatrix, K: int, seed: int, D: int, restarts: int = 10,
-                      max_iterations: int = 100, tolerance: float = 1e-6) -> ClusterStage:
+                      max_iterations: int = 100, tolerance: float = 1e-6,
+                      engine=None) -> ClusterStage:
     """run_cluster_stage on an already-built clustering matrix: K = 0 means
-    the number of distinct row labels; best objective over `restarts` seeds."""
+    the number of distinct row labels; best objective over `restarts` seeds.
+    With `engine`, normalisation and every restart run on the GPU (K7)."""
     if K == 0:
         labels = set(matrix.row_labels)
         K = len(labels) if labels else D
-    norm = l2_normalize_rows(matrix)
+    if engine is not None:
+        import torch
+        vals = torch.from_numpy(_f64(matrix.values).reshape(matrix.rows, matrix.cols))
+        dnorm = l2_normalize_rows_device(engine, vals)
+        run = lambda sd: kmeans_device(engine, dnorm, matrix.rows, matrix.cols, K, sd,  # noqa
+                                       max_iterations, tolerance)
+    else:
+        norm = l2_normalize_rows(matrix)
+        run = lambda sd: kmeans(norm.values, norm.rows, norm.cols, K, sd,  # noqa: E731
+                                max_iterations, tolerance)
     best = None
     for attempt in range(max(restarts, 1)):
-        cand = kmeans(norm.values, norm.rows, norm.cols, K, seed + attempt, max_iterations,
-                      tolerance)
+        cand = run(seed + attempt)
         if best is None or cand.objective < best.objective:
             best = cand
     gm = assign_clusters_to_groups(best, matrix, D, seed)

@@ -7,6 +7,9 @@ torch.distributed (NCCL on the B200s, gloo in CPU tests).
   Topology::contiguous (/root/reference/proj/core/src/placement.cpp:75-94).
 * The only collective of the statistics path is one all-reduce(sum) of the
   fused uint64 statistics buffer (integer sums: bit-exact in any order).
+* Candidate scoring is sharded: rank r prices candidates [r·P/world,
+  (r+1)·P/world) of the global demand and the LayerSim rows are all-gathered
+  (SURVEY §8e collective 2); every rank ends with the full table.
 * The bf16 dispatch / combine all-to-all-v uses the K3 permutation's
   key_offsets to size the per-rank sends (a2a.py).
 """
@@ -55,3 +58,25 @@ def exchange_counts(send_counts: torch.Tensor, group=None) -> torch.Tensor:
     recv = torch.empty_like(send_counts)
     dist.all_to_all_single(recv, send_counts, group=group)
     return recv
+
+
+def shard_bounds(P: int, world: int, rank: int):
+    """Candidate slice of `rank` when P splits evenly over the ranks, else
+    None (every rank scores all P)."""
+    if world <= 1 or P % world != 0:
+        return None
+    per = P // world
+    return rank * per, (rank + 1) * per
+
+
+def gather_shards(full: torch.Tensor, rows_per_rank: int, group=None) -> torch.Tensor:
+    """All-gathers `full` in place along dim 0: rank r owns rows
+    [r·rows_per_rank, (r+1)·rows_per_rank) on entry, every rank holds all of
+    them on return (bit copies: float64 LayerSims stay bit-identical)."""
+    world = dist.get_world_size(group)
+    chunks = list(full.split(rows_per_rank, dim=0))
+    if len(chunks) != world:
+        raise ValueError("gather_shards: rows do not split evenly over the ranks")
+    mine = chunks[dist.get_rank(group)].clone()
+    dist.all_gather(chunks, mine, group=group)
+    return full

@@ -262,6 +262,8 @@ class RoutingPipeline:
                        torch.empty(2 * L, D, dtype=torch.float64, device=dev))
         self.fin_cl = (torch.empty(P * L, 6, dtype=torch.float64, device=dev),
                        torch.empty(P * L, D, dtype=torch.float64, device=dev))
+        from .distributed import shard_bounds
+        self.shard = shard_bounds(P, self.world, self.rank)
 
     @property
     def launches(self) -> int:
@@ -323,20 +325,34 @@ class RoutingPipeline:
             import torch.distributed as dist
             dist.all_reduce(self.stats.view(torch.int64), group=group)
         self._score_only()
+        self._gather_scores(group)
 
     def _score_only(self):
+        """Scores the global demand: the two round-robin baselines on every
+        rank, the cluster-routed candidates sharded over the ranks (rank r
+        prices its P/world slice; `_gather_scores` all-gathers the rows)."""
         s, eng = self.spec, self.eng
         L, D, E = s.layers, s.groups, s.experts
         eng.score_placements(self.dem_rr, self.luts_rr, self.g2n, D, row_node=self.g2n,
                              out=self.sc_rr)
-        eng.score_placements(self.dem_cl, self.luts_cl, self.g2n, D, row_node=self.g2n,
-                             out=self.sc_cl)
         inter, intra, rank = self.sc_rr
         eng.finalize(inter.view(-1), intra.view(-1), rank.view(-1, D), D, self.cost,
                      self.topology, out=self.fin_rr[0], payload=self.fin_rr[1])
-        inter, intra, rank = self.sc_cl
-        eng.finalize(inter.view(-1), intra.view(-1), rank.view(-1, D), D, self.cost,
-                     self.topology, out=self.fin_cl[0], payload=self.fin_cl[1])
+        lo, hi = self.shard if self.shard is not None else (0, self.luts_cl.shape[0])
+        inter, intra, rank = (t[lo:hi] for t in self.sc_cl)
+        eng.score_placements(self.dem_cl, self.luts_cl[lo:hi], self.g2n, D, row_node=self.g2n,
+                             out=(inter, intra, rank))
+        eng.finalize(inter.reshape(-1), intra.reshape(-1), rank.reshape(-1, D), D, self.cost,
+                     self.topology, out=self.fin_cl[0][lo * L:hi * L],
+                     payload=self.fin_cl[1][lo * L:hi * L])
+
+    def _gather_scores(self, group=None):
+        if self.shard is None:
+            return
+        from .distributed import gather_shards
+        rows = (self.shard[1] - self.shard[0]) * self.spec.layers
+        gather_shards(self.fin_cl[0], rows, group)
+        gather_shards(self.fin_cl[1], rows, group)
 
     def step(self, timed_router=False, group=None):
         if getattr(self, "graphs", None):
@@ -394,6 +410,7 @@ class RoutingPipeline:
             import torch.distributed as dist
             dist.all_reduce(self.stats.view(torch.int64), group=group)
         g_score.replay()
+        self._gather_scores(group)
 
     def graph_router_ms(self):
         return [a.elapsed_time(b) for a, b in self.graph_events]

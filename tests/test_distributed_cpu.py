@@ -12,8 +12,8 @@ import torch.distributed as dist
 import torch.multiprocessing as mp_
 
 from paper_2604_23150_b200.distributed import (all_reduce_stats, exchange_counts,
-                                               groups_per_rank, rank_of_group,
-                                               send_counts_from_offsets)
+                                               gather_shards, groups_per_rank, rank_of_group,
+                                               send_counts_from_offsets, shard_bounds)
 
 
 def _free_port():
@@ -33,7 +33,14 @@ def _worker(rank, world, port, q):
         all_reduce_stats(stats)
         sc = torch.tensor([rank * 10 + r for r in range(world)], dtype=torch.int64)
         rc = exchange_counts(sc)
-        q.put((rank, [int(x) for x in stats.tolist()], rc.tolist()))
+        # sharded scoring: each rank fills its candidate rows, then all-gather
+        P, L = 6, 3
+        lo, hi = shard_bounds(P, world, rank)
+        fin = torch.full((P * L, 4), -1.0, dtype=torch.float64)
+        for p in range(lo, hi):
+            fin[p * L:(p + 1) * L] = torch.arange(4, dtype=torch.float64) / 3 + p
+        gather_shards(fin, (hi - lo) * L)
+        q.put((rank, [int(x) for x in stats.tolist()], rc.tolist(), fin.numpy().copy()))
     finally:
         dist.destroy_process_group()
 
@@ -46,13 +53,15 @@ def test_gloo_stats_allreduce_and_count_exchange():
     procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
-    got = dict((r, (s, c)) for r, s, c in (q.get(timeout=120) for _ in range(world)))
+    got = dict((r, (s, c, f)) for r, s, c, f in (q.get(timeout=120) for _ in range(world)))
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
     expect = [((1 << 62) * 2 + 1) % (1 << 64), 7 + 14, 0]
+    full = np.concatenate([np.tile(np.arange(4) / 3 + p, (3, 1)) for p in range(6)])
     for r in range(world):
         assert got[r][0] == expect
+        np.testing.assert_array_equal(got[r][2], full)  # every rank holds all candidates
         assert got[r][1] == [src * 10 + r for src in range(world)]
 
 

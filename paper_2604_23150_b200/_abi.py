@@ -6,6 +6,7 @@ missing or the device is not an sm_100 part, calls fail loudly.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 from .errors import raise_for_status
@@ -107,7 +108,7 @@ def lib():
         if not LIB_PATH.exists():
             raise RuntimeError(f"{LIB_PATH} is missing: build it with "
                                "`python -m paper_2604_23150_b200.build` (no CPU fallback)")
-        L = C.CDLL(str(LIB_PATH))
+        L = C.CDLL(os.environ.get("MPB_LIB_PATH") or str(LIB_PATH))  # env: experiment builds
         for name, (res, args) in _SIGS.items():
             fn = getattr(L, name)
             fn.restype = res

@@ -39,6 +39,10 @@ constexpr int kBM = 128;
 constexpr int kBK = 64;  // 64 bf16 = 128 bytes: one 128B swizzle atom per row
 constexpr int kThreadsR = 384;  // 4 non-epilogue + 8 epilogue warps
 
+#ifndef MPB_ROUTER_STAGES_CAP
+#define MPB_ROUTER_STAGES_CAP 8  // build-time knob for stage-count experiments
+#endif
+
 template <int N, int KMAX, bool PAIR>
 struct RCfg {
     static constexpr int A_BYTES = kBM * kBK * 2;
@@ -51,7 +55,8 @@ struct RCfg {
     static constexpr int PARK_ROW = (2 * KMAX + 2 > 16 ? 2 * KMAX + 2 : 16) | 1;
     static constexpr int PARK = 256 * PARK_ROW * 4;
     static constexpr int BUDGET = 232448 - 1024 - PARK - 256;
-    static constexpr int STAGES = BUDGET / STAGE > 8 ? 8 : BUDGET / STAGE;
+    static constexpr int STAGES = BUDGET / STAGE > MPB_ROUTER_STAGES_CAP ? MPB_ROUTER_STAGES_CAP
+                                                                         : BUDGET / STAGE;
     static constexpr int SMEM = 1024 + STAGES * STAGE + PARK + (2 * STAGES + 4) * 8 + 16;
 };
 

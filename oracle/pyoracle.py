@@ -283,6 +283,8 @@ class Reference:
         L.ref_compare_scenario.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, _f64p]
         L.ref_bench_compare.argtypes = [C.c_char_p, C.c_uint32, _f64p]
         L.ref_analysis.argtypes = [C.c_char_p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_char_p]
+        L.ref_bench_parse.argtypes = [C.c_char_p, C.c_uint32, C.c_uint32, C.c_uint32, _f64p,
+                                      _f64p, C.POINTER(C.c_uint64)]
 
     def _check(self, st):
         if st:
@@ -395,6 +397,14 @@ class Reference:
         sec = np.zeros(1)
         self._check(self.lib.ref_bench_compare(str(config_path).encode(), reps, sec))
         return float(sec[0])
+
+    def bench_parse(self, trace_path, E, top_k, layers):
+        """(parse seconds, summed-matrix seconds, records) of the reference."""
+        a, b = np.zeros(1), np.zeros(1)
+        n = C.c_uint64()
+        self._check(self.lib.ref_bench_parse(str(trace_path).encode(), E, top_k, layers, a, b,
+                                             C.byref(n)))
+        return float(a[0]), float(b[0]), int(n.value)
 
 
 def have_reference() -> bool:

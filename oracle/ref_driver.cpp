@@ -459,4 +459,21 @@ int ref_bench_compare(const char *config_json_path, std::uint32_t reps, double *
     });
 }
 
+// Times read_trace_file + build_activation_matrix_summed (a1/a2 wire path).
+int ref_bench_parse(const char *trace_path, std::uint32_t E, std::uint32_t top_k,
+                    std::uint32_t layers, double *parse_seconds, double *matrix_seconds,
+                    std::uint64_t *records_out) {
+    return guarded([&] {
+        ModelConfig model{"m", E, top_k, layers, false};
+        auto t0 = std::chrono::steady_clock::now();
+        auto records = read_trace_file(trace_path, model);
+        auto t1 = std::chrono::steady_clock::now();
+        auto m = build_activation_matrix_summed(records, E, Stage::decode);
+        auto t2 = std::chrono::steady_clock::now();
+        *parse_seconds = std::chrono::duration<double>(t1 - t0).count();
+        *matrix_seconds = std::chrono::duration<double>(t2 - t1).count();
+        *records_out = records.size() + 0 * m.rows;
+    });
+}
+
 } // extern "C"

@@ -18,6 +18,7 @@
 // reference's nlohmann path measures 10.9 MB/s).
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <fstream>
 #include <map>
@@ -25,6 +26,8 @@
 #include <set>
 #include <sstream>
 #include <string>
+#include <string_view>
+#include <thread>
 #include <vector>
 
 #include "internal.cuh"
@@ -155,7 +158,9 @@ struct Scanner {
         uint64_t v = 0;
         while (p < end && *p >= '0' && *p <= '9') {
             const uint64_t d = static_cast<uint64_t>(*p++ - '0');
-            if (v > (UINT64_MAX - d) / 10) err(std::string("'") + field + "' out of range");
+            if (v >= 1844674407370955161ull &&  // 10*v + d would exceed UINT64_MAX
+                (v > 1844674407370955161ull || d > 5))
+                err(std::string("'") + field + "' out of range");
             v = v * 10 + d;
         }
         if (p < end && (*p == '.' || *p == 'e' || *p == 'E')) err(std::string("'") + field + "' must be an integer");
@@ -184,96 +189,207 @@ struct Scanner {
     }
 };
 
-void validate_record(const mpb_trace::Record &r, const std::string &label, uint32_t E,
+void validate_record(const mpb_trace::Record &r, std::string_view label, uint32_t E,
                      uint32_t top_k) {
-    const std::string name = "record (dataset=" + label + ", request_id=" +
-                             std::to_string(r.request_id) + ", stage=" + stage_name(r.stage) +
-                             ", layer=" + std::to_string(r.layer) + ")";
-    if (r.experts.empty()) bad(MPB_VALIDATION_ERROR, name + ": empty expert_counts");
+    auto name = [&] {
+        return "record (dataset=" + std::string(label) + ", request_id=" +
+               std::to_string(r.request_id) + ", stage=" + stage_name(r.stage) +
+               ", layer=" + std::to_string(r.layer) + ")";
+    };
+    if (r.experts.empty()) bad(MPB_VALIDATION_ERROR, name() + ": empty expert_counts");
     uint64_t sum = 0;
     for (const auto &[e, c] : r.experts) {
         if (e >= E)
-            bad(MPB_VALIDATION_ERROR, name + ": expert id " + std::to_string(e) + " >= E=" + std::to_string(E));
-        if (c == 0) bad(MPB_VALIDATION_ERROR, name + ": expert " + std::to_string(e) + " has zero count");
+            bad(MPB_VALIDATION_ERROR, name() + ": expert id " + std::to_string(e) + " >= E=" + std::to_string(E));
+        if (c == 0) bad(MPB_VALIDATION_ERROR, name() + ": expert " + std::to_string(e) + " has zero count");
         sum += c;
     }
     if (r.stage == 1 && sum != r.gen_tokens * top_k)
-        bad(MPB_VALIDATION_ERROR, name + ": decode counts sum to " + std::to_string(sum) +
+        bad(MPB_VALIDATION_ERROR, name() + ": decode counts sum to " + std::to_string(sum) +
                                       ", expected generated_tokens*top_k=" +
                                       std::to_string(r.gen_tokens * top_k));
 }
 
-void parse_into(mpb_trace &t, const char *text, size_t len, uint32_t E, uint32_t top_k) {
-    size_t line_no = 0;
-    const char *p = text, *end = text + len;
-    while (p < end) {
-        const char *nl = static_cast<const char *>(memchr(p, '\n', end - p));
-        const char *le = nl ? nl : end;
-        ++line_no;
-        const char *q = p;
-        while (q < le && (*q == ' ' || *q == '\t' || *q == '\r')) ++q;
-        if (q < le) {
-            Scanner s{p, le, line_no};
-            if (!s.eat('{')) s.err("not a JSON object");
-            mpb_trace::Record r;
-            std::string label;
-            unsigned seen = 0;
-            std::map<uint32_t, uint64_t> ex;
-            if (!s.eat('}')) {
-                do {
-                    const std::string key = s.str();
-                    s.expect(':', "expected ':'");
-                    if (key == "dataset") { label = s.str(); seen |= 1; }
-                    else if (key == "request_id") { r.request_id = s.u64("request_id"); seen |= 2; }
-                    else if (key == "stage") {
-                        const std::string st = s.str();
-                        if (st == "prefill") r.stage = 0;
-                        else if (st == "decode") r.stage = 1;
-                        else s.err("unknown stage '" + st + "' (expected prefill|decode)");
-                        seen |= 4;
-                    } else if (key == "layer") {
-                        const uint64_t v = s.u64("layer");
-                        if (v > UINT32_MAX) s.err("'layer' out of range");
-                        r.layer = static_cast<uint32_t>(v);
-                        seen |= 8;
-                    } else if (key == "input_len") { r.input_len = s.u64("input_len"); seen |= 16; }
-                    else if (key == "gen_tokens") { r.gen_tokens = s.u64("gen_tokens"); seen |= 32; }
-                    else if (key == "experts") {
-                        if (!s.eat('{')) s.err("'experts' must be an object");
-                        if (!s.eat('}')) {
-                            do {
-                                const std::string k = s.str();
-                                s.expect(':', "expected ':'");
-                                size_t i = 0;
-                                while (i < k.size() && (k[i] == ' ' || k[i] == '\t')) ++i;
-                                size_t j = i;
-                                uint64_t id = 0;
-                                while (j < k.size() && k[j] >= '0' && k[j] <= '9') id = id * 10 + (k[j++] - '0');
-                                if (j == i || j != k.size() || id > UINT32_MAX)
-                                    s.err("expert id key '" + k + "' is not decimal");
-                                ex[static_cast<uint32_t>(id)] = s.u64("experts");
-                            } while (s.eat(','));
-                            s.expect('}', "expected '}'");
+// Key or string value: a view into the line when it has no escapes (the
+// writer never emits any), else the decoded copy in `scratch`.
+std::string_view str_view(Scanner &s, std::string &scratch) {
+    s.ws();
+    if (s.p >= s.end || *s.p != '"') s.err("expected a string");
+    const char *b = s.p + 1, *q = b;
+    while (q < s.end && *q != '"' && *q != '\\') ++q;
+    if (q < s.end && *q == '"') {
+        s.p = q + 1;
+        return std::string_view(b, static_cast<size_t>(q - b));
+    }
+    scratch = s.str();
+    return scratch;
+}
+
+// One chunk of whole lines, parsed independently (line numbers from `line0`).
+struct Chunk {
+    std::vector<mpb_trace::Record> recs;          // .label = chunk-local label index
+    std::vector<std::string> labels;              // chunk-local, first-seen order
+    bool failed = false;
+    TraceError error{MPB_OK, ""};
+};
+
+void parse_chunk(Chunk &c, const char *text, const char *end, size_t line0, uint32_t E,
+                 uint32_t top_k) {
+    size_t line_no = line0;
+    const char *p = text;
+    c.recs.reserve(static_cast<size_t>(end - text) / 256 + 16);
+    std::string scratch, scratch2;
+    std::vector<std::pair<uint32_t, uint64_t>> ex;
+    try {
+        while (p < end) {
+            const char *nl = static_cast<const char *>(memchr(p, '\n', end - p));
+            const char *le = nl ? nl : end;
+            ++line_no;
+            const char *q = p;
+            while (q < le && (*q == ' ' || *q == '\t' || *q == '\r')) ++q;
+            if (q < le) {
+                Scanner s{p, le, line_no};
+                if (!s.eat('{')) s.err("not a JSON object");
+                mpb_trace::Record r;
+                std::string_view label;
+                std::string label_copy;
+                unsigned seen = 0;
+                ex.clear();
+                if (!s.eat('}')) {
+                    do {
+                        const std::string_view key = str_view(s, scratch);
+                        s.expect(':', "expected ':'");
+                        if (key == "dataset") {
+                            label = str_view(s, scratch2);
+                            if (label.data() == scratch2.data()) {  // escaped: keep a copy
+                                label_copy = scratch2;
+                                label = label_copy;
+                            }
+                            seen |= 1;
+                        } else if (key == "request_id") {
+                            r.request_id = s.u64("request_id");
+                            seen |= 2;
+                        } else if (key == "stage") {
+                            const std::string_view st = str_view(s, scratch);
+                            if (st == "prefill") r.stage = 0;
+                            else if (st == "decode") r.stage = 1;
+                            else s.err("unknown stage '" + std::string(st) + "' (expected prefill|decode)");
+                            seen |= 4;
+                        } else if (key == "layer") {
+                            const uint64_t v = s.u64("layer");
+                            if (v > UINT32_MAX) s.err("'layer' out of range");
+                            r.layer = static_cast<uint32_t>(v);
+                            seen |= 8;
+                        } else if (key == "input_len") {
+                            r.input_len = s.u64("input_len");
+                            seen |= 16;
+                        } else if (key == "gen_tokens") {
+                            r.gen_tokens = s.u64("gen_tokens");
+                            seen |= 32;
+                        } else if (key == "experts") {
+                            if (!s.eat('{')) s.err("'experts' must be an object");
+                            ex.clear();  // a repeated "experts" key replaces the object
+                            if (!s.eat('}')) {
+                                do {
+                                    const std::string_view k = str_view(s, scratch);
+                                    s.expect(':', "expected ':'");
+                                    size_t i = 0;
+                                    while (i < k.size() && (k[i] == ' ' || k[i] == '\t')) ++i;
+                                    size_t j = i;
+                                    uint64_t id = 0;
+                                    while (j < k.size() && k[j] >= '0' && k[j] <= '9' && id <= UINT32_MAX)
+                                        id = id * 10 + (k[j++] - '0');
+                                    if (j == i || j != k.size() || id > UINT32_MAX)
+                                        s.err("expert id key '" + std::string(k) + "' is not decimal");
+                                    ex.emplace_back(static_cast<uint32_t>(id), s.u64("experts"));
+                                } while (s.eat(','));
+                                s.expect('}', "expected '}'");
+                            }
+                            seen |= 64;
+                        } else {
+                            s.skip_value();
                         }
-                        seen |= 64;
-                    } else {
-                        s.skip_value();
+                    } while (s.eat(','));
+                    s.expect('}', "expected '}'");
+                }
+                s.ws();
+                if (s.p != le) s.err("trailing characters after the object");
+                static const char *names[] = {"dataset", "request_id", "stage", "layer",
+                                              "input_len", "gen_tokens", "experts"};
+                for (int b = 0; b < 7; ++b)
+                    if (!(seen & (1u << b))) s.err(std::string("key '") + names[b] + "' not found");
+                // ascending expert ids; a duplicated key keeps its last value (std::map
+                // assignment semantics of the reference's json -> map conversion)
+                for (size_t i = 1; i < ex.size(); ++i) {  // stable insertion sort (short lists)
+                    const auto v = ex[i];
+                    size_t j = i;
+                    while (j > 0 && ex[j - 1].first > v.first) {
+                        ex[j] = ex[j - 1];
+                        --j;
                     }
-                } while (s.eat(','));
-                s.expect('}', "expected '}'");
+                    ex[j] = v;
+                }
+                r.experts.reserve(ex.size());
+                for (size_t i = 0; i < ex.size(); ++i)
+                    if (i + 1 == ex.size() || ex[i + 1].first != ex[i].first)
+                        r.experts.push_back(ex[i]);
+                validate_record(r, label, E, top_k);
+                uint32_t lid = 0;
+                while (lid < c.labels.size() && c.labels[lid] != label) ++lid;
+                if (lid == c.labels.size()) c.labels.emplace_back(label);
+                r.label = lid;
+                c.recs.push_back(std::move(r));
             }
-            s.ws();
-            if (s.p != le) s.err("trailing characters after the object");
-            static const char *names[] = {"dataset", "request_id", "stage", "layer", "input_len",
-                                          "gen_tokens", "experts"};
-            for (int b = 0; b < 7; ++b)
-                if (!(seen & (1u << b))) s.err(std::string("key '") + names[b] + "' not found");
-            r.experts.assign(ex.begin(), ex.end());
-            validate_record(r, label, E, top_k);
-            r.label = t.label(label);
+            p = nl ? nl + 1 : end;
+        }
+    } catch (const TraceError &e) {
+        c.failed = true;
+        c.error = e;
+    }
+}
+
+// Whole-text parse: lines split into ~equal chunks at newline boundaries,
+// chunks parsed on worker threads, merged in document order (labels keep the
+// first-seen order; the first error in document order is reported).
+void parse_into(mpb_trace &t, const char *text, size_t len, uint32_t E, uint32_t top_k) {
+    const size_t min_chunk = size_t(1) << 22;  // 4 MiB
+    unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    if (const char *e = std::getenv("MPB_TRACE_THREADS")) hw = std::max(1, std::atoi(e));
+    const size_t n_chunks = std::max<size_t>(1, std::min<size_t>(hw, len / min_chunk));
+    std::vector<const char *> cut{text};
+    for (size_t i = 1; i < n_chunks; ++i) {
+        const char *c = text + len * i / n_chunks;
+        if (c < cut.back()) c = cut.back();
+        const char *nl = static_cast<const char *>(memchr(c, '\n', text + len - c));
+        cut.push_back(nl ? nl + 1 : text + len);
+    }
+    cut.push_back(text + len);
+    const size_t n = cut.size() - 1;
+    std::vector<size_t> line0(n, 0);
+    for (size_t i = 1; i < n; ++i)
+        line0[i] = line0[i - 1] + static_cast<size_t>(std::count(cut[i - 1], cut[i], '\n'));
+    std::vector<Chunk> chunks(n);
+    if (n == 1) {
+        parse_chunk(chunks[0], cut[0], cut[1], 0, E, top_k);
+    } else {
+        std::vector<std::thread> th;
+        for (size_t i = 0; i < n; ++i)
+            th.emplace_back(parse_chunk, std::ref(chunks[i]), cut[i], cut[i + 1], line0[i], E, top_k);
+        for (auto &x : th) x.join();
+    }
+    size_t total = 0;
+    for (auto &c : chunks) {
+        if (c.failed) throw c.error;
+        total += c.recs.size();
+    }
+    t.records.reserve(t.records.size() + total);
+    for (auto &c : chunks) {
+        std::vector<uint32_t> remap(c.labels.size());
+        for (size_t i = 0; i < c.labels.size(); ++i) remap[i] = t.label(c.labels[i]);
+        for (auto &r : c.recs) {
+            r.label = remap[r.label];
             t.records.push_back(std::move(r));
         }
-        p = nl ? nl + 1 : end;
     }
 }
 
@@ -356,11 +472,18 @@ mpb_status mpb_trace_parse(const char *text, uint64_t len, uint32_t E, uint32_t 
 
 mpb_status mpb_trace_read_file(const char *path, uint32_t E, uint32_t top_k, uint32_t layers,
                                mpb_trace **out) {
-    std::ifstream in(path ? path : "", std::ios::binary);
-    if (!in) return fail(MPB_ERROR, std::string("cannot open trace file: ") + (path ? path : ""));
-    std::stringstream ss;
-    ss << in.rdbuf();
-    const std::string s = ss.str();
+    FILE *f = std::fopen(path ? path : "", "rb");
+    if (!f) return fail(MPB_ERROR, std::string("cannot open trace file: ") + (path ? path : ""));
+    std::string s;
+    std::fseek(f, 0, SEEK_END);
+    const long size = std::ftell(f);
+    std::fseek(f, 0, SEEK_SET);
+    if (size > 0) {
+        s.resize(static_cast<size_t>(size));
+        const size_t got = std::fread(s.data(), 1, s.size(), f);
+        s.resize(got);
+    }
+    std::fclose(f);
     return mpb_trace_parse(s.data(), s.size(), E, top_k, layers, out);
 }
 

@@ -352,7 +352,8 @@ void parse_chunk(Chunk &c, const char *text, const char *end, size_t line0, uint
 // chunks parsed on worker threads, merged in document order (labels keep the
 // first-seen order; the first error in document order is reported).
 void parse_into(mpb_trace &t, const char *text, size_t len, uint32_t E, uint32_t top_k) {
-    const size_t min_chunk = size_t(1) << 22;  // 4 MiB
+    size_t min_chunk = size_t(1) << 22;  // 4 MiB
+    if (const char *e = std::getenv("MPB_TRACE_MIN_CHUNK")) min_chunk = std::max(1, std::atoi(e));
     unsigned hw = std::max(1u, std::thread::hardware_concurrency());
     if (const char *e = std::getenv("MPB_TRACE_THREADS")) hw = std::max(1, std::atoi(e));
     const size_t n_chunks = std::max<size_t>(1, std::min<size_t>(hw, len / min_chunk));

@@ -110,3 +110,28 @@ def test_parse_errors():
     t = tr.parse_trace(ok, M64x4)
     with pytest.raises(EmptySelectionError):
         tr.build_activation_matrix(t, 64, 0, tr.PREFILL)
+
+
+def test_chunked_parallel_parse_matches_serial(golden, monkeypatch):
+    """Lines split over worker threads: same records, same first-seen label
+    order, and the first error in document order with its true line number."""
+    src = (golden / "trace_analysis.jsonl").read_bytes()
+    lines = src.splitlines()
+    model = tr.ModelConfig("m", 64, 2, 3)
+    monkeypatch.setenv("MPB_TRACE_THREADS", "1")
+    serial = tr.parse_trace(src, model)
+    monkeypatch.setenv("MPB_TRACE_THREADS", "5")
+    monkeypatch.setenv("MPB_TRACE_MIN_CHUNK", "1000")
+    par = tr.parse_trace(src, model)
+    assert par.labels == serial.labels and len(par) == len(serial)
+    for name in ("request_id", "layer", "stage", "gen_tokens", "label", "pair_offset"):
+        np.testing.assert_array_equal(getattr(par, name), getattr(serial, name))
+    np.testing.assert_array_equal(par.expert[:par.n_pairs], serial.expert[:serial.n_pairs])
+    np.testing.assert_array_equal(par.count[:par.n_pairs], serial.count[:serial.n_pairs])
+    # two bad lines in different chunks: the earlier one is reported
+    bad = list(lines)
+    bad[len(bad) // 2] = b'{"dataset": 1}'
+    bad[-3] = b"[oops]"
+    with pytest.raises(ParseError) as e:
+        tr.parse_trace(b"\n".join(bad), model)
+    assert f"line {len(bad) // 2 + 1}:" in str(e.value)

@@ -68,6 +68,11 @@ MPB_API const char *mpb_last_error_message(void);
 MPB_API mpb_status mpb_context_create(int device, void *stream, mpb_context **out);
 MPB_API mpb_status mpb_context_destroy(mpb_context *ctx);
 MPB_API mpb_status mpb_context_set_stream(mpb_context *ctx, void *stream);
+/* Caps the SMs this context's grids are sized for (persistent router units,
+ * layout blocks, co-activation CTAs); 0 restores the device count. Two
+ * contexts with disjoint budgets run their kernels concurrently (e.g. the
+ * router of layer l+1 beside the statistics of layer l). */
+MPB_API mpb_status mpb_context_set_sm_budget(mpb_context *ctx, uint32_t sms);
 /* Synchronises the stream and reports input errors the kernels flagged
  * (uncovered expert, id >= E, source group >= D -> MPB_VALIDATION_ERROR,
  * exactly where simulate_layer throws, simulator.cpp:66-71). Clears the flag. */

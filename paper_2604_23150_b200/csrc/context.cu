@@ -78,6 +78,7 @@ mpb_status mpb_context_create(int device, void *stream, mpb_context **out) {
     ctx->device = device;
     ctx->stream = static_cast<cudaStream_t>(stream);
     cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
+    ctx->device_sms = ctx->num_sms;
     cudaError_t e = cudaMalloc(&ctx->d_error, sizeof(uint32_t));
     if (e == cudaSuccess) e = cudaMemset(ctx->d_error, 0, sizeof(uint32_t));
     if (e != cudaSuccess) {
@@ -107,6 +108,14 @@ mpb_status mpb_context_set_stream(mpb_context *ctx, void *stream) {
 }
 
 uint64_t mpb_context_launch_count(const mpb_context *ctx) { return ctx ? ctx->launches : 0; }
+
+mpb_status mpb_context_set_sm_budget(mpb_context *ctx, uint32_t sms) {
+    if (!ctx) return fail(MPB_VALIDATION_ERROR, "mpb_context_set_sm_budget: NULL context");
+    ctx->num_sms = sms == 0 ? ctx->device_sms
+                            : static_cast<int>(std::min<uint32_t>(sms, ctx->device_sms));
+    if (ctx->num_sms < 2) ctx->num_sms = 2;  // a router CTA pair
+    return MPB_OK;
+}
 
 mpb_status mpb_context_sync(mpb_context *ctx) {
     if (!ctx) return fail(MPB_VALIDATION_ERROR, "mpb_context_sync: NULL context");

@@ -73,7 +73,8 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
 struct mpb_context {
     int device = 0;
     cudaStream_t stream = nullptr;
-    int num_sms = 148;
+    int num_sms = 148;      // SM budget grids are sized for (<= device_sms)
+    int device_sms = 148;
     uint32_t *d_error = nullptr;
     uint64_t launches = 0;
     // grow-only scratch (permutation block histograms, co-activation partials)

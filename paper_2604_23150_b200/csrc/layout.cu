@@ -598,8 +598,14 @@ mpb_status launch_layout(mpb_context *ctx, const mpb_tokens *tk, const mpb_place
     if (p.cell_smem) smem += cell4;
     // about one block per SM: per-block histogram zero/flush and slot-count
     // work scale with D*E and NS, so fewer, fatter blocks amortise them
+    // (at least kMinBlocks: a context with a small SM budget — the statistics
+    // tail beside the router — needs several resident blocks per SM to hide
+    // latency)
     static const char *cenv = std::getenv("MPB_LAYOUT_BLOCKS_PER_SM");
-    const uint64_t want_blocks = uint64_t(ctx->num_sms) * (cenv ? std::max(1, std::atoi(cenv)) : 2);
+    static const char *menv = std::getenv("MPB_LAYOUT_MIN_BLOCKS");
+    const uint64_t kMinBlocks = menv ? std::max(1, std::atoi(menv)) : 160;
+    const uint64_t want_blocks = std::max<uint64_t>(
+        kMinBlocks, uint64_t(ctx->num_sms) * (cenv ? std::max(1, std::atoi(cenv)) : 2));
     uint64_t chunk = (P + want_blocks - 1) / want_blocks;
     chunk = std::max<uint64_t>(kChunkQuantum, (chunk + kChunkQuantum - 1) / kChunkQuantum * kChunkQuantum);
     const uint32_t nb = static_cast<uint32_t>((P + chunk - 1) / chunk);

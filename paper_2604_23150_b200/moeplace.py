@@ -306,6 +306,10 @@ class Engine:
         self.stream = stream
         _abi.call("mpb_context_set_stream", self.ctx, C.c_void_p(stream.cuda_stream))
 
+    def set_sm_budget(self, sms: int) -> None:
+        """Size this context's grids for `sms` SMs (0 = all of them)."""
+        _abi.call("mpb_context_set_sm_budget", self.ctx, int(sms))
+
     def sync(self) -> None:
         """Synchronise and raise ValidationError for inputs kernels flagged."""
         _abi.call("mpb_context_sync", self.ctx)

@@ -159,9 +159,35 @@ class RoutingPipeline:
         self.coact = self.stats[o:o + E * E].view(E, E)
         # co-activation runs on a side stream (own context + scratch) while the
         # layout kernels run on the main one: both only read the layer's idx
+        # MPB_SIDE_STREAM: 0 one stream; 1 co-activation on a side stream beside the
+        # layout; 2 + round-robin stats on the side; 3 the whole statistics tail of
+        # layer l on a side context with a small SM budget, concurrent with the
+        # router of layer l+1 (idx double-buffered)
         self.side = None
-        self.side_mode = int(os.environ.get("MPB_SIDE_STREAM", "1"))  # 0 off, 1 coact, 2 +rr stats
-        if s.coact and self.side_mode:
+        self.side_mode = int(os.environ.get("MPB_SIDE_STREAM", "3"))
+        if self.side_mode == 3:
+            # the router chain gets the high-priority stream (made current, so the
+            # caller's torch ops and timing events stay ordered with it): when SMs
+            # free up, the block scheduler serves its CTAs before the tail's
+            lo_prio, hi_prio = torch.cuda.Stream.priority_range()
+            main = torch.cuda.Stream(eng.device, priority=hi_prio)
+            main.wait_stream(torch.cuda.current_stream(eng.device))
+            torch.cuda.set_stream(main)
+            eng.set_stream(main)
+            self.side = mp.Engine(eng.device.index,
+                                  stream=torch.cuda.Stream(eng.device, priority=lo_prio))
+            n_sm = torch.cuda.get_device_properties(eng.device).multi_processor_count
+            self.side_sms = int(os.environ.get("MPB_SIDE_SMS", "20"))
+            self.side.set_sm_budget(self.side_sms)
+            eng.set_sm_budget(n_sm - self.side_sms)
+            # one idx / w buffer per layer (8 MiB each at the DSv3 shape): the
+            # router chain never waits on the tails (no write-after-read hazard),
+            # so consecutive routers keep their programmatic-launch overlap
+            self.idx_buf = [self.idx] + [torch.empty_like(self.idx) for _ in range(L - 1)]
+            self.w_buf = [self.w] + [torch.empty_like(self.w) for _ in range(L - 1)]
+            self._rdone = [torch.cuda.Event() for _ in range(L)]
+            self._tdone = torch.cuda.Event()
+        elif s.coact and self.side_mode:
             self.side = mp.Engine(eng.device.index, stream=torch.cuda.Stream(eng.device))
             self._fork, self._join = torch.cuda.Event(), torch.cuda.Event()
         # ---- calibration -> learned placement, routes, candidates
@@ -280,6 +306,8 @@ class RoutingPipeline:
 
     def layer(self, l: int, X: torch.Tensor, timed_router=False):
         s, eng = self.spec, self.eng
+        if self.side_mode == 3:
+            return self._overlapped_layer(l, X, timed_router)
         if timed_router:
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
@@ -321,6 +349,9 @@ class RoutingPipeline:
             eng.coactivation(self.idx, s.experts, out=self.coact)
 
     def reduce_and_score(self, group=None):
+        if self.side_mode == 3:  # join the statistics tails before scoring
+            self._tdone.record(self.side.stream)
+            self.eng.stream.wait_event(self._tdone)
         if self.world > 1:
             import torch.distributed as dist
             dist.all_reduce(self.stats.view(torch.int64), group=group)
@@ -362,6 +393,31 @@ class RoutingPipeline:
             self.layer(l, self.X[l], timed_router)
         self.reduce_and_score(group)
 
+    def _overlapped_layer(self, l: int, X: torch.Tensor, timed_router=False):
+        """Router of layer l on the main context (most SMs, high-priority
+        stream); the statistics tail of layer l on the side context
+        (MPB_SIDE_SMS SMs) starts when the router is done and runs beside router
+        l+1. Every layer has its own idx / w buffer, so the router chain never
+        waits on a tail; reduce_and_score joins the side stream."""
+        s, eng, side = self.spec, self.eng, self.side
+        idx, w = self.idx_buf[l], self.w_buf[l]
+        if timed_router:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(eng.stream)
+        eng.router_topk(X, self.model.W[l], s.top_k, s.score_fn, s.renorm, out=(idx, w))
+        if timed_router:
+            e1.record(eng.stream)
+            self.router_events.append((e0, e1))
+        self._rdone[l].record(eng.stream)
+        side.stream.wait_event(self._rdone[l])
+        side.dispatch_layout(idx, self.dp_deployed, src=self.src_cl, tag=self.dom_tok,
+                             n_tags=s.domains, demand=self.dem_cl[l], tag_pop=self.pop,
+                             perm_out=(self.sp, self.pp, self.ko), src2=self.src_rr,
+                             demand2=self.dem_rr[l])
+        if s.coact:
+            side.coactivation(idx, s.experts, out=self.coact)
+
     # ---------------------------------------------------------------- CUDA graphs
     def capture(self, group=None) -> bool:
         """Captures the step's launch sequence as CUDA graphs (one for the
@@ -372,6 +428,9 @@ class RoutingPipeline:
         eng = self.eng
         L = self.spec.layers
         old = eng.stream
+        if self.side_mode == 3:
+            self.graphs = None
+            return False
         try:
             self.graph_events = [(torch.cuda.Event(enable_timing=True),
                                   torch.cuda.Event(enable_timing=True)) for _ in range(L)]

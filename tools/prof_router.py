@@ -15,8 +15,11 @@ ap.add_argument("--E", type=int, default=256)
 ap.add_argument("--k", type=int, default=8)
 ap.add_argument("--fn", type=int, default=1)
 ap.add_argument("--iters", type=int, default=5)
+ap.add_argument("--sms", type=int, default=0, help="SM budget (0 = all)")
 a = ap.parse_args()
 eng = mp.Engine(0)
+if a.sms:
+    eng.set_sm_budget(a.sms)
 X = torch.randn(a.T, a.H, device="cuda").to(torch.bfloat16)
 W = (torch.randn(a.E, a.H, device="cuda") / a.H ** 0.5).to(torch.bfloat16)
 out = (torch.empty(a.T, a.k, dtype=torch.int32, device="cuda"),

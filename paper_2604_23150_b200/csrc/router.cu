@@ -108,16 +108,6 @@ __device__ __forceinline__ bool next_item(uint32_t n, uint32_t unit, uint32_t un
     return false;
 }
 
-// Selection order: (value desc, id asc), NaN below everything; a sentinel
-// slot (id < 0) is beaten by nothing.
-__device__ __forceinline__ bool sel_beats(float a, int ia, float b, int ib) {
-    if (ib < 0) return false;
-    const bool na = isnan(a), nb = isnan(b);
-    if (na || nb) return (na && nb) ? ia < ib : nb;
-    if (a != b) return a > b;
-    return ia < ib;
-}
-
 // Hands an accumulator's TMEM back to the MMA issuer after this thread's
 // tcgen05.ld reads: single CTA — every epilogue thread arrives; pair — one lane
 // per warp arrives on the LEADER's barrier (locally or through DSMEM).

@@ -246,7 +246,7 @@ class RoutingPipeline:
         labels = [f"domain{d}" for d in dom]
         matrix = mp.ActivationMatrix(R, s.experts, counts, labels, list(range(R)))
         K = s.groups if s.domains >= s.groups else s.domains
-        stage = pol.run_cluster_stage(matrix, K, 1, s.groups, restarts=10)
+        stage = pol.run_cluster_stage(matrix, K, 1, s.groups, restarts=10, engine=eng)  # K7
         strategies = pol.build_placements(stage, seed=2)
         # request-type classification stand-in: a new request of domain d goes to
         # the cluster that holds most calibration requests of domain d

@@ -341,10 +341,18 @@ def run_gpu_arm(args, spec):
     prof = ROOT / "profiles" / "ncu_router_summary.json"
     if prof.exists():
         traffic = json.loads(prof.read_text()).get(spec.name, {}).get("dram_bytes_per_launch")
-    roofline = {"bound": "tensor", "achieved": achieved_tf, "peak": tf_sust, "unit": "TFLOP/s",
-                "frac": achieved_tf / tf_sust, "traffic": traffic,
+    # bound by arithmetic intensity vs the sustained ridge (DSv3 255 FLOP/B vs
+    # 214.7: tensor; Maverick / Qwen3 ~128: HBM)
+    hbm_bound = flop / byts < tf_sust * 1e12 / (hbm * 1e9)
+    roofline = {"bound": "hbm" if hbm_bound else "tensor",
+                "achieved": achieved_gbs if hbm_bound else achieved_tf,
+                "peak": hbm if hbm_bound else tf_sust,
+                "unit": "GB/s" if hbm_bound else "TFLOP/s",
+                "frac": achieved_gbs / hbm if hbm_bound else achieved_tf / tf_sust,
+                "traffic": traffic,
                 "kernel": "k_router (tcgen05 GEMM + fused top-k)",
-                "peak_kind": f"sustained bf16, {peak_src}",
+                "peak_kind": (f"HBM copy bandwidth, {peak_src}" if hbm_bound
+                              else f"sustained bf16, {peak_src}"),
                 "algorithmic_flop_per_launch": flop, "algorithmic_bytes_per_launch": byts,
                 "hbm_achieved_gbs": achieved_gbs, "hbm_frac": achieved_gbs / hbm,
                 "ms_per_launch": r_ms, "share_of_step": share}

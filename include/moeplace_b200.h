@@ -235,6 +235,32 @@ MPB_API mpb_status mpb_combine_scatter(mpb_context *ctx, const void *recv, const
                                        const float *weights, uint64_t T, uint32_t k, uint32_t H,
                                        void *Y);
 
+/* Fused NVLink dispatch / combine (K6-P2P): `peer_recv` [world] holds the
+ * device addresses of every rank's receive buffer mapped into this process
+ * (symmetric memory over NVSwitch), `peer_counts` [world] every rank's
+ * [world][world] int64 count matrix. mpb_a2a_put_counts writes this rank's
+ * per-destination counts (from key_offsets; span = keys per rank = groups per
+ * rank * E) into every peer; after a cross-rank barrier mpb_dispatch_p2p
+ * writes each sorted pair's hidden-state row straight into the destination
+ * rank's buffer, and (after the experts and another barrier)
+ * mpb_combine_p2p reads each token's k rows out of the peers' buffers into
+ * the weighted sum — the same result as gather + all-to-all-v + combine,
+ * bit for bit, with no staging buffers. Rows past `capacity_rows` raise
+ * MPB_VALIDATION_ERROR at the next mpb_context_sync. */
+MPB_API mpb_status mpb_a2a_put_counts(mpb_context *ctx, const int64_t *key_offsets,
+                                      uint32_t span, uint32_t world, uint32_t rank,
+                                      const uint64_t *peer_counts);
+MPB_API mpb_status mpb_dispatch_p2p(mpb_context *ctx, const void *X, const int32_t *sorted_pairs,
+                                    uint64_t n_pairs, uint32_t k, uint32_t H,
+                                    const int64_t *counts, const int64_t *key_offsets,
+                                    uint32_t span, uint32_t world, uint32_t rank,
+                                    const uint64_t *peer_recv, uint64_t capacity_rows);
+MPB_API mpb_status mpb_combine_p2p(mpb_context *ctx, const int32_t *pair_pos,
+                                   const float *weights, uint64_t T, uint32_t k, uint32_t H,
+                                   const int64_t *counts, const int64_t *key_offsets,
+                                   uint32_t span, uint32_t world, uint32_t rank,
+                                   const uint64_t *peer_recv, void *Y);
+
 /* ---- host placement / grouping policies (no device needed) ----------------
  * Restatements of the reference policies with the same std::mt19937_64 /
  * libstdc++ distribution calls (bit-identical results):

@@ -13,8 +13,15 @@ Per MoE layer on each rank (one process per GPU):
      in token order (deterministic, no atomics).
 The bytes crossing "nodes" (contiguous rank blocks) are what simulate_layer
 prices (/root/reference/proj/core/src/simulator.cpp:57-88), here moved for
-real; a fused compute+collective kernel over NVLink peer memory is the next
-step.
+real.
+
+`p2p=True` replaces 2-5 with the fused NVLink path (K6-P2P): receive buffers
+are symmetric memory mapped into every rank; one kernel gathers each sorted
+pair's row straight into the destination rank's buffer (remote stores), and
+one kernel reads each token's k rows back out of the peers' buffers into the
+weighted sum (remote loads) — no send / back staging, no NCCL payload
+collective; the per-destination counts travel through peer memory too. Cross-
+rank ordering uses the symmetric-memory barrier (stream-ordered signal pads).
 """
 from __future__ import annotations
 
@@ -55,6 +62,38 @@ class ExpertParallelA2A:
         self.ko = torch.empty(self.D * self.E + 1, dtype=torch.int64, device=dev)
         per_node = max(1, world // max(1, nodes))
         self.node_of_rank = [r // per_node for r in range(world)]
+        self.p2p = False
+
+    def enable_p2p(self, capacity_rows: int) -> None:
+        """Maps a `capacity_rows` x H bf16 receive buffer and a [world][world]
+        count matrix of every rank into this process (symmetric memory)."""
+        dev = self.eng.device
+        if self.world == 1:
+            self.recv = torch.empty(capacity_rows, self.H, dtype=torch.bfloat16, device=dev)
+            self.cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+            self.peer_recv = torch.tensor([self.recv.data_ptr()], dtype=torch.uint64, device=dev)
+            self.peer_cnt = torch.tensor([self.cnt.data_ptr()], dtype=torch.uint64, device=dev)
+            self.hdl = None
+        else:
+            import torch.distributed._symmetric_memory as symm_mem
+            gname = (self.group or dist.group.WORLD).group_name
+            cap = torch.tensor([capacity_rows], dtype=torch.int64, device=dev)
+            dist.all_reduce(cap, op=dist.ReduceOp.MAX, group=self.group)  # same size everywhere
+            capacity_rows = int(cap.item())
+            self.recv = symm_mem.empty(capacity_rows, self.H, dtype=torch.bfloat16, device=dev)
+            self.hdl = symm_mem.rendezvous(self.recv, gname)
+            self.cnt = symm_mem.empty(self.world * self.world, dtype=torch.int64, device=dev)
+            hc = symm_mem.rendezvous(self.cnt, gname)
+            self.peer_recv = torch.tensor(list(self.hdl.buffer_ptrs), dtype=torch.uint64,
+                                          device=dev)
+            self.peer_cnt = torch.tensor(list(hc.buffer_ptrs), dtype=torch.uint64, device=dev)
+            self._hc = hc
+        self.capacity = capacity_rows
+        self.p2p = True
+
+    def _barrier(self):
+        if self.hdl is not None:
+            self.hdl.barrier(channel=0)
 
     def __call__(self, X: torch.Tensor, idx: torch.Tensor, w: torch.Tensor, src: torch.Tensor,
                  stats: A2AStats | None = None) -> torch.Tensor:
@@ -64,6 +103,8 @@ class ExpertParallelA2A:
         self.demand.zero_()
         eng.dispatch_layout(idx, self.dp, src=src, demand=self.demand,
                             perm_out=(self.sp[:n], self.pp[:n], self.ko))
+        if self.p2p:
+            return self._p2p(X, idx, w, n, k, stats)
         eng.dispatch_gather(X, self.sp[:n], k, out=self.send[:n])
         counts = send_counts_from_offsets(self.ko.cpu().numpy(), self.D, self.E, self.world)
         if stats is not None:
@@ -87,6 +128,33 @@ class ExpertParallelA2A:
             back = self.back[:n]
             dist.all_to_all_single(back, recv, scl, rcl, group=self.group)
         return eng.combine_scatter(back, self.pp[:n], w)
+
+    def _count_stats(self, stats: A2AStats) -> None:
+        counts = send_counts_from_offsets(self.ko.cpu().numpy(), self.D, self.E, self.world)
+        for r, c in enumerate(counts):
+            stats.sent_rows += int(c)
+            if self.node_of_rank[r] == self.node_of_rank[self.rank]:
+                stats.intra_node_rows += int(c)
+            else:
+                stats.inter_node_rows += int(c)
+
+    def _p2p(self, X, idx, w, n, k, stats):
+        eng = self.eng
+        span = groups_per_rank(self.D, self.world) * self.E
+        if stats is not None:
+            self._count_stats(stats)
+        eng.a2a_put_counts(self.ko, span, self.world, self.rank, self.peer_cnt)
+        self._barrier()  # every rank's counts are in every count matrix
+        eng.dispatch_p2p(X, self.sp[:n], k, self.cnt, self.ko, span, self.world, self.rank,
+                         self.peer_recv, self.capacity)
+        self._barrier()  # every row has landed in its destination buffer
+        # expert FFN stand-in: identity on this rank's received rows
+        self._barrier()  # every rank's experts are done with its rows
+        Y = torch.empty(idx.shape[0], self.H, dtype=torch.bfloat16, device=X.device)
+        eng.combine_p2p(self.pp[:n], w, self.H, self.cnt, self.ko, span, self.world, self.rank,
+                        self.peer_recv, Y)
+        self._barrier()  # peers have read their rows back: buffers reusable
+        return Y
 
 
 def source_groups_cluster(domains: np.ndarray, domain_route, seed: int = 0) -> np.ndarray:

@@ -130,6 +130,7 @@ mpb_status mpb_context_sync(mpb_context *ctx) {
         if (flags & kErrSourceRange) what += " source group out of range;";
         if (flags & kErrExpertRange) what += " expert id out of range (>= E);";
         if (flags & kErrUncovered) what += " expert is not covered by the placement;";
+        if (flags & kErrCapacity) what = "all-to-all: rows beyond the receive buffer capacity;";
         return fail(MPB_VALIDATION_ERROR, what);
     }
     return MPB_OK;

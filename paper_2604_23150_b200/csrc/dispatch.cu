@@ -1,9 +1,18 @@
-// K6 (local halves): bf16 hidden-state gather into the dispatch send buffer
-// and weighted combine back into token order, both driven by the K3
-// permutation. Between them the host runs the all-to-all (NCCL) with the
-// per-destination counts from key_offsets. One warp per row, 16-byte vector
-// loads/stores; combine accumulates the k rows of a token in fp32 in a fixed
-// order (deterministic, no atomics).
+// K6: bf16 expert-parallel dispatch / combine driven by the K3 permutation.
+//
+// Local halves (NCCL path): hidden-state gather into the send buffer and the
+// weighted combine back into token order; the host runs the all-to-all-v in
+// between. Fused NVLink path (P2P): every rank's recv buffer is mapped into
+// every peer (symmetric memory over NVSwitch); k_put_counts writes this rank's
+// per-destination counts into every peer's count matrix, k_dispatch_p2p
+// gathers each sorted pair's row straight into the destination rank's recv
+// buffer (remote 16-byte stores: gather and transfer are one pass), and
+// k_combine_p2p reads each token's k returned rows straight out of the peers'
+// buffers (remote loads) into the fp32 weighted sum — no send / back buffers,
+// no second all-to-all. Rows of rank s for rank r land at
+// sum_{s'<s} C[s'][r] + (position - first position for r) in r's buffer.
+// One warp per row, 16-byte vectors; combine accumulates the k rows in a fixed
+// order (bit-identical to the local combine).
 #include <cuda_bf16.h>
 
 #include "internal.cuh"
@@ -49,6 +58,96 @@ __global__ void __launch_bounds__(256) k_combine(const uint4 *recv, const int32_
     }
 }
 
+// C[me][r] = rows this rank sends to rank r (its contiguous slice of the
+// sorted pairs), written into every peer's [world][world] count matrix.
+__global__ void k_put_counts(const int64_t *ko, uint32_t span, uint32_t world, uint32_t me,
+                             const uint64_t *peer_cnt) {
+    const uint32_t q = threadIdx.x / world, r = threadIdx.x % world;
+    if (q >= world) return;
+    const int64_t c = ko[static_cast<size_t>(r + 1) * span] - ko[static_cast<size_t>(r) * span];
+    reinterpret_cast<int64_t *>(peer_cnt[q])[me * world + r] = c;
+}
+
+struct P2PMap {
+    int64_t first[9];  // first sorted position for rank r (r <= world)
+    int64_t base[8];   // where this rank's rows start in rank r's recv buffer
+};
+
+__device__ __forceinline__ void p2p_map(const int64_t *C, const int64_t *ko, uint32_t span,
+                                        uint32_t world, uint32_t me, P2PMap &m) {
+    for (uint32_t r = 0; r <= world; ++r) m.first[r] = ko[static_cast<size_t>(r) * span];
+    for (uint32_t r = 0; r < world; ++r) {
+        int64_t b = 0;
+        for (uint32_t s = 0; s < me; ++s) b += C[s * world + r];
+        m.base[r] = b;
+    }
+}
+
+__device__ __forceinline__ uint32_t rank_of_pos(const P2PMap &m, uint32_t world, int64_t pos) {
+    uint32_t r = 0;
+    while (r + 1 < world && pos >= m.first[r + 1]) ++r;
+    return r;
+}
+
+__global__ void __launch_bounds__(256) k_dispatch_p2p(const uint4 *X, const int32_t *sorted_pairs,
+                                                      uint64_t n, uint32_t k, uint32_t hv,
+                                                      const int64_t *C, const int64_t *ko,
+                                                      uint32_t span, uint32_t world, uint32_t me,
+                                                      const uint64_t *peer_recv, uint64_t cap,
+                                                      uint32_t *err) {
+    __shared__ P2PMap m;
+    if (threadIdx.x == 0) p2p_map(C, ko, span, world, me, m);
+    __syncthreads();
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+    if (i >= n) return;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t r = rank_of_pos(m, world, static_cast<int64_t>(i));
+    const uint64_t row = static_cast<uint64_t>(m.base[r] + static_cast<int64_t>(i) - m.first[r]);
+    if (row >= cap) {
+        if (lane == 0) atomicOr(err, kErrCapacity);
+        return;
+    }
+    const uint64_t tok = static_cast<uint64_t>(sorted_pairs[i]) / k;
+    const uint4 *src = X + tok * hv;
+    uint4 *dst = reinterpret_cast<uint4 *>(peer_recv[r]) + row * hv;
+    for (uint32_t c = lane; c < hv; c += 32) dst[c] = __ldg(src + c);
+}
+
+__global__ void __launch_bounds__(256) k_combine_p2p(const int32_t *pair_pos, const float *w,
+                                                     uint64_t T, uint32_t k, uint32_t hv,
+                                                     const int64_t *C, const int64_t *ko,
+                                                     uint32_t span, uint32_t world, uint32_t me,
+                                                     const uint64_t *peer_recv, uint4 *Y) {
+    __shared__ P2PMap m;
+    if (threadIdx.x == 0) p2p_map(C, ko, span, world, me, m);
+    __syncthreads();
+    const uint64_t t = static_cast<uint64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+    if (t >= T) return;
+    const uint32_t lane = threadIdx.x & 31;
+    for (uint32_t c = lane; c < hv; c += 32) {
+        float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (uint32_t j = 0; j < k; ++j) {
+            const float wj = w[t * k + j];
+            const int64_t pos = pair_pos[t * k + j];
+            const uint32_t r = rank_of_pos(m, world, pos);
+            const uint64_t row = static_cast<uint64_t>(m.base[r] + pos - m.first[r]);
+            const uint4 v = reinterpret_cast<const uint4 *>(peer_recv[r])[row * hv + c];
+            const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&v);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const float2 f = __bfloat1622float2(h[q]);
+                acc[2 * q] = fmaf(wj, f.x, acc[2 * q]);
+                acc[2 * q + 1] = fmaf(wj, f.y, acc[2 * q + 1]);
+            }
+        }
+        uint4 o;
+        __nv_bfloat162 *oh = reinterpret_cast<__nv_bfloat162 *>(&o);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) oh[q] = __floats2bfloat162_rn(acc[2 * q], acc[2 * q + 1]);
+        Y[t * hv + c] = o;
+    }
+}
+
 }  // namespace
 }  // namespace mpb
 
@@ -76,6 +175,51 @@ mpb_status mpb_combine_scatter(mpb_context *ctx, const void *recv, const int32_t
     if (T == 0) return MPB_OK;
     k_combine<<<static_cast<unsigned>((T + 7) / 8), 256, 0, ctx->stream>>>(
         static_cast<const uint4 *>(recv), pair_pos, weights, T, k, H / 8, static_cast<uint4 *>(Y));
+    MPB_LAUNCHED(ctx);
+    return MPB_OK;
+}
+
+mpb_status mpb_a2a_put_counts(mpb_context *ctx, const int64_t *key_offsets, uint32_t span,
+                              uint32_t world, uint32_t rank, const uint64_t *peer_counts) {
+    if (!ctx || !key_offsets || !peer_counts)
+        return fail(MPB_VALIDATION_ERROR, "mpb_a2a_put_counts: NULL argument");
+    if (world < 1 || world > 8 || rank >= world)
+        return fail(MPB_CONFIG_ERROR, "mpb_a2a_put_counts: need 1 <= world <= 8, rank < world");
+    k_put_counts<<<1, 64, 0, ctx->stream>>>(key_offsets, span, world, rank, peer_counts);
+    MPB_LAUNCHED(ctx);
+    return MPB_OK;
+}
+
+mpb_status mpb_dispatch_p2p(mpb_context *ctx, const void *X, const int32_t *sorted_pairs,
+                            uint64_t n_pairs, uint32_t k, uint32_t H, const int64_t *counts,
+                            const int64_t *key_offsets, uint32_t span, uint32_t world,
+                            uint32_t rank, const uint64_t *peer_recv, uint64_t capacity_rows) {
+    if (!ctx || !counts || !key_offsets || !peer_recv || (n_pairs && (!X || !sorted_pairs)))
+        return fail(MPB_VALIDATION_ERROR, "mpb_dispatch_p2p: NULL argument");
+    if (H % 8 != 0 || k == 0) return fail(MPB_CONFIG_ERROR, "mpb_dispatch_p2p: need H % 8 == 0, k >= 1");
+    if (world < 1 || world > 8 || rank >= world)
+        return fail(MPB_CONFIG_ERROR, "mpb_dispatch_p2p: need 1 <= world <= 8, rank < world");
+    if (n_pairs == 0) return MPB_OK;
+    k_dispatch_p2p<<<static_cast<unsigned>((n_pairs + 7) / 8), 256, 0, ctx->stream>>>(
+        static_cast<const uint4 *>(X), sorted_pairs, n_pairs, k, H / 8, counts, key_offsets, span,
+        world, rank, peer_recv, capacity_rows, ctx->d_error);
+    MPB_LAUNCHED(ctx);
+    return MPB_OK;
+}
+
+mpb_status mpb_combine_p2p(mpb_context *ctx, const int32_t *pair_pos, const float *weights,
+                           uint64_t T, uint32_t k, uint32_t H, const int64_t *counts,
+                           const int64_t *key_offsets, uint32_t span, uint32_t world,
+                           uint32_t rank, const uint64_t *peer_recv, void *Y) {
+    if (!ctx || !counts || !key_offsets || !peer_recv || (T && (!pair_pos || !weights || !Y)))
+        return fail(MPB_VALIDATION_ERROR, "mpb_combine_p2p: NULL argument");
+    if (H % 8 != 0 || k == 0) return fail(MPB_CONFIG_ERROR, "mpb_combine_p2p: need H % 8 == 0, k >= 1");
+    if (world < 1 || world > 8 || rank >= world)
+        return fail(MPB_CONFIG_ERROR, "mpb_combine_p2p: need 1 <= world <= 8, rank < world");
+    if (T == 0) return MPB_OK;
+    k_combine_p2p<<<static_cast<unsigned>((T + 7) / 8), 256, 0, ctx->stream>>>(
+        pair_pos, weights, T, k, H / 8, counts, key_offsets, span, world, rank, peer_recv,
+        static_cast<uint4 *>(Y));
     MPB_LAUNCHED(ctx);
     return MPB_OK;
 }

@@ -16,6 +16,7 @@ enum : uint32_t {
     kErrExpertRange = 1u,  // expert id < 0 or >= E
     kErrSourceRange = 2u,  // source group >= D
     kErrUncovered = 4u,    // expert not held by any group of the placement
+    kErrCapacity = 8u,     // a2a rows beyond a receive buffer's capacity
 };
 
 struct Status {

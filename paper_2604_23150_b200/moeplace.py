@@ -466,6 +466,24 @@ class Engine:
                   T, k, H, _ptr(out))
         return out
 
+    # --- fused NVLink dispatch / combine (peer-mapped receive buffers) ---
+    def a2a_put_counts(self, key_offsets, span: int, world: int, rank: int, peer_counts):
+        _abi.call("mpb_a2a_put_counts", self.ctx, _ptr(key_offsets), span, world, rank,
+                  _ptr(peer_counts))
+
+    def dispatch_p2p(self, X, sorted_pairs, k: int, counts, key_offsets, span: int, world: int,
+                     rank: int, peer_recv, capacity_rows: int):
+        _abi.call("mpb_dispatch_p2p", self.ctx, _ptr(X), _ptr(sorted_pairs), sorted_pairs.numel(),
+                  k, X.shape[1], _ptr(counts), _ptr(key_offsets), span, world, rank,
+                  _ptr(peer_recv), capacity_rows)
+
+    def combine_p2p(self, pair_pos, weights, H: int, counts, key_offsets, span: int, world: int,
+                    rank: int, peer_recv, out):
+        T, k = weights.shape
+        _abi.call("mpb_combine_p2p", self.ctx, _ptr(pair_pos), _ptr(weights), T, k, H,
+                  _ptr(counts), _ptr(key_offsets), span, world, rank, _ptr(peer_recv), _ptr(out))
+        return out
+
 
 _engines: dict = {}
 

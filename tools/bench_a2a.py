@@ -66,6 +66,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--nodes", type=int, default=2)
+    ap.add_argument("--no-p2p", action="store_true", help="skip the fused NVLink path")
     a = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -105,32 +106,47 @@ def main():
         src = torch.from_numpy(tok_src).to(eng.device)
         op = ExpertParallelA2A(eng, placement, top, spec.hidden, T * spec.top_k, rank, world,
                                nodes)
-        for _ in range(a.warmup):
-            Y = op(X, idx, w, src)
+
+        def timed(fn):
+            for _ in range(a.warmup):
+                Y = fn(None)
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            st = A2AStats()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            for i in range(a.steps):
+                fn(st if i == 0 else None)
+            e.record()
+            torch.cuda.synchronize()
+            ms = torch.tensor([s.elapsed_time(e) / a.steps], device=eng.device,
+                              dtype=torch.float64)
+            if world > 1:
+                dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+            return Y, float(ms.item()), st
+
+        Y, ms, st = timed(lambda st_: op(X, idx, w, src, st_))
         # correctness: identity experts -> Y = X * sum(w) = X (renormalised weights)
         err = (Y.float() - X.float()).abs().max().item()
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        st = A2AStats()
-        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        s.record()
-        for i in range(a.steps):
-            op(X, idx, w, src, st if i == 0 else None)
-        e.record()
-        torch.cuda.synchronize()
-        ms = torch.tensor([s.elapsed_time(e) / a.steps], device=eng.device, dtype=torch.float64)
         tot = torch.tensor([st.sent_rows, st.inter_node_rows, st.intra_node_rows],
                            device=eng.device, dtype=torch.int64)
         if world > 1:
-            dist.all_reduce(ms, op=dist.ReduceOp.MAX)
             dist.all_reduce(tot)
         sent, inter, intra = (int(x) for x in tot.tolist())
-        results[policy] = dict(ms_per_step=float(ms.item()), rows=sent, inter_node_rows=inter,
+        results[policy] = dict(ms_per_step=ms, rows=sent, inter_node_rows=inter,
                                intra_node_rows=intra,
                                inter_node_bytes=inter * spec.hidden * 2,
                                inter_fraction=inter / max(1, sent), max_abs_err=err,
                                tokens_per_rank=T)
+        if not a.no_p2p:  # fused NVLink path: same output bit for bit
+            op.enable_p2p(2 * T * spec.top_k)
+            Yp, ms_p, _ = timed(lambda st_: op(X, idx, w, src, st_))
+            eng.sync()
+            same = torch.tensor([int(torch.equal(Yp, Y))], device=eng.device)
+            if world > 1:
+                dist.all_reduce(same, op=dist.ReduceOp.MIN)
+            results[policy].update(p2p_ms_per_step=ms_p, p2p_bit_identical=bool(same.item()))
     if rank == 0:
         base = results["round_robin"]["inter_node_bytes"]
         saved = 1.0 - results["learned"]["inter_node_bytes"] / base if base else float("nan")

@@ -255,6 +255,13 @@ MPB_API mpb_status mpb_dispatch_p2p(mpb_context *ctx, const void *X, const int32
                                     const int64_t *counts, const int64_t *key_offsets,
                                     uint32_t span, uint32_t world, uint32_t rank,
                                     const uint64_t *peer_recv, uint64_t capacity_rows);
+/* Return leg pushed instead of pulled: every received row (the first
+ * `recv_rows` rows of this rank's buffer, grouped by source rank) is written
+ * into its source rank's `back` buffer at its position in that rank's sorted
+ * order; after a barrier the source runs mpb_combine_scatter on `back`. */
+MPB_API mpb_status mpb_return_p2p(mpb_context *ctx, const void *recv, uint64_t recv_rows,
+                                  uint32_t H, const int64_t *counts, uint32_t world,
+                                  uint32_t rank, const uint64_t *peer_back);
 MPB_API mpb_status mpb_combine_p2p(mpb_context *ctx, const int32_t *pair_pos,
                                    const float *weights, uint64_t T, uint32_t k, uint32_t H,
                                    const int64_t *counts, const int64_t *key_offsets,

@@ -15,13 +15,16 @@ The bytes crossing "nodes" (contiguous rank blocks) are what simulate_layer
 prices (/root/reference/proj/core/src/simulator.cpp:57-88), here moved for
 real.
 
-`p2p=True` replaces 2-5 with the fused NVLink path (K6-P2P): receive buffers
-are symmetric memory mapped into every rank; one kernel gathers each sorted
-pair's row straight into the destination rank's buffer (remote stores), and
-one kernel reads each token's k rows back out of the peers' buffers into the
-weighted sum (remote loads) — no send / back staging, no NCCL payload
-collective; the per-destination counts travel through peer memory too. Cross-
-rank ordering uses the symmetric-memory barrier (stream-ordered signal pads).
+`enable_p2p()` replaces 2-5 with the fused NVLink path (K6-P2P): receive
+buffers are symmetric memory mapped into every rank; one kernel gathers each
+sorted pair's row straight into the destination rank's buffer (remote stores).
+The return leg is pulled by default: the combine reads each token's k rows
+out of the peers' buffers inside the weighted sum (remote loads);
+`combine="push"` instead writes the received rows back into their source
+ranks' symmetric `back` buffers at the sources' sorted positions and the
+source combines from local memory (measured slower: profiles/r01_a2a_n*.json). No send staging, no NCCL payload collective; the
+per-destination counts travel through peer memory too. Cross-rank ordering
+uses the symmetric-memory barrier (stream-ordered signal pads).
 """
 from __future__ import annotations
 
@@ -64,12 +67,14 @@ class ExpertParallelA2A:
         self.node_of_rank = [r // per_node for r in range(world)]
         self.p2p = False
 
-    def enable_p2p(self, capacity_rows: int) -> None:
+    def enable_p2p(self, capacity_rows: int, combine: str = "pull") -> None:
         """Maps a `capacity_rows` x H bf16 receive buffer and a [world][world]
         count matrix of every rank into this process (symmetric memory)."""
         dev = self.eng.device
         if self.world == 1:
             self.recv = torch.empty(capacity_rows, self.H, dtype=torch.bfloat16, device=dev)
+            self.back_sym = self.back
+            self.peer_back = torch.tensor([self.back.data_ptr()], dtype=torch.uint64, device=dev)
             self.cnt = torch.zeros(1, dtype=torch.int64, device=dev)
             self.peer_recv = torch.tensor([self.recv.data_ptr()], dtype=torch.uint64, device=dev)
             self.peer_cnt = torch.tensor([self.cnt.data_ptr()], dtype=torch.uint64, device=dev)
@@ -82,6 +87,13 @@ class ExpertParallelA2A:
             capacity_rows = int(cap.item())
             self.recv = symm_mem.empty(capacity_rows, self.H, dtype=torch.bfloat16, device=dev)
             self.hdl = symm_mem.rendezvous(self.recv, gname)
+            mx = torch.tensor([self.send.shape[0]], dtype=torch.int64, device=dev)
+            dist.all_reduce(mx, op=dist.ReduceOp.MAX, group=self.group)
+            self.back_sym = symm_mem.empty(int(mx.item()), self.H, dtype=torch.bfloat16,
+                                           device=dev)
+            hb = symm_mem.rendezvous(self.back_sym, gname)
+            self.peer_back = torch.tensor(list(hb.buffer_ptrs), dtype=torch.uint64, device=dev)
+            self._hb = hb
             self.cnt = symm_mem.empty(self.world * self.world, dtype=torch.int64, device=dev)
             hc = symm_mem.rendezvous(self.cnt, gname)
             self.peer_recv = torch.tensor(list(self.hdl.buffer_ptrs), dtype=torch.uint64,
@@ -89,6 +101,7 @@ class ExpertParallelA2A:
             self.peer_cnt = torch.tensor(list(hc.buffer_ptrs), dtype=torch.uint64, device=dev)
             self._hc = hc
         self.capacity = capacity_rows
+        self.combine_mode = combine  # "pull": remote loads in the combine (default); "push"
         self.p2p = True
 
     def _barrier(self):
@@ -149,6 +162,13 @@ class ExpertParallelA2A:
                          self.peer_recv, self.capacity)
         self._barrier()  # every row has landed in its destination buffer
         # expert FFN stand-in: identity on this rank's received rows
+        if self.combine_mode == "push":
+            # each rank pushes the rows it received (after its experts) back to
+            # their source ranks' `back` buffers, in the sources' sorted order
+            eng.return_p2p(self.recv, self.capacity, self.cnt, self.world, self.rank,
+                           self.peer_back)
+            self._barrier()  # every row is home
+            return eng.combine_scatter(self.back_sym[:n], self.pp[:n], w)
         self._barrier()  # every rank's experts are done with its rows
         Y = torch.empty(idx.shape[0], self.H, dtype=torch.bfloat16, device=X.device)
         eng.combine_p2p(self.pp[:n], w, self.H, self.cnt, self.ko, span, self.world, self.rank,

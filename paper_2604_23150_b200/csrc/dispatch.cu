@@ -148,6 +148,39 @@ __global__ void __launch_bounds__(256) k_combine_p2p(const int32_t *pair_pos, co
     }
 }
 
+// Return leg, pushed: every row this rank received goes back to its source
+// rank s, into s's symmetric `back` buffer at the row's position in s's
+// sorted order (s's slice for this rank starts at sum_{r'<me} C[s][r']).
+// Remote stores only; the source then combines from local memory.
+__global__ void __launch_bounds__(256) k_return_p2p(const uint4 *recv, uint64_t rows,
+                                                    uint32_t hv, const int64_t *C,
+                                                    uint32_t world, uint32_t me,
+                                                    const uint64_t *peer_back) {
+    __shared__ int64_t s_base[9];   // first recv row from source s (s <= world)
+    __shared__ int64_t s_first[8];  // where this rank's slice starts in s's order
+    if (threadIdx.x == 0) {
+        int64_t b = 0;
+        for (uint32_t q = 0; q < world; ++q) {
+            s_base[q] = b;
+            b += C[q * world + me];
+            int64_t f = 0;
+            for (uint32_t r = 0; r < me; ++r) f += C[q * world + r];
+            s_first[q] = f;
+        }
+        s_base[world] = b;
+    }
+    __syncthreads();
+    const uint64_t row = static_cast<uint64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+    if (row >= rows || static_cast<int64_t>(row) >= s_base[world]) return;
+    const uint32_t lane = threadIdx.x & 31;
+    uint32_t q = 0;
+    while (q + 1 < world && static_cast<int64_t>(row) >= s_base[q + 1]) ++q;
+    const uint64_t pos = static_cast<uint64_t>(s_first[q] + static_cast<int64_t>(row) - s_base[q]);
+    const uint4 *src = recv + row * hv;
+    uint4 *dst = reinterpret_cast<uint4 *>(peer_back[q]) + pos * hv;
+    for (uint32_t c = lane; c < hv; c += 32) dst[c] = src[c];
+}
+
 }  // namespace
 }  // namespace mpb
 
@@ -220,6 +253,21 @@ mpb_status mpb_combine_p2p(mpb_context *ctx, const int32_t *pair_pos, const floa
     k_combine_p2p<<<static_cast<unsigned>((T + 7) / 8), 256, 0, ctx->stream>>>(
         pair_pos, weights, T, k, H / 8, counts, key_offsets, span, world, rank, peer_recv,
         static_cast<uint4 *>(Y));
+    MPB_LAUNCHED(ctx);
+    return MPB_OK;
+}
+
+mpb_status mpb_return_p2p(mpb_context *ctx, const void *recv, uint64_t recv_rows, uint32_t H,
+                          const int64_t *counts, uint32_t world, uint32_t rank,
+                          const uint64_t *peer_back) {
+    if (!ctx || !recv || !counts || !peer_back)
+        return fail(MPB_VALIDATION_ERROR, "mpb_return_p2p: NULL argument");
+    if (H % 8 != 0) return fail(MPB_CONFIG_ERROR, "mpb_return_p2p: need H % 8 == 0");
+    if (world < 1 || world > 8 || rank >= world)
+        return fail(MPB_CONFIG_ERROR, "mpb_return_p2p: need 1 <= world <= 8, rank < world");
+    if (recv_rows == 0) return MPB_OK;
+    k_return_p2p<<<static_cast<unsigned>((recv_rows + 7) / 8), 256, 0, ctx->stream>>>(
+        static_cast<const uint4 *>(recv), recv_rows, H / 8, counts, world, rank, peer_back);
     MPB_LAUNCHED(ctx);
     return MPB_OK;
 }

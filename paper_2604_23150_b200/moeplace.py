@@ -477,6 +477,10 @@ class Engine:
                   k, X.shape[1], _ptr(counts), _ptr(key_offsets), span, world, rank,
                   _ptr(peer_recv), capacity_rows)
 
+    def return_p2p(self, recv, recv_rows: int, counts, world: int, rank: int, peer_back):
+        _abi.call("mpb_return_p2p", self.ctx, _ptr(recv), recv_rows, recv.shape[1], _ptr(counts),
+                  world, rank, _ptr(peer_back))
+
     def combine_p2p(self, pair_pos, weights, H: int, counts, key_offsets, span: int, world: int,
                     rank: int, peer_recv, out):
         T, k = weights.shape

@@ -140,13 +140,15 @@ def main():
                                inter_fraction=inter / max(1, sent), max_abs_err=err,
                                tokens_per_rank=T)
         if not a.no_p2p:  # fused NVLink path: same output bit for bit
-            op.enable_p2p(2 * T * spec.top_k)
-            Yp, ms_p, _ = timed(lambda st_: op(X, idx, w, src, st_))
-            eng.sync()
-            same = torch.tensor([int(torch.equal(Yp, Y))], device=eng.device)
-            if world > 1:
-                dist.all_reduce(same, op=dist.ReduceOp.MIN)
-            results[policy].update(p2p_ms_per_step=ms_p, p2p_bit_identical=bool(same.item()))
+            for mode in ("push", "pull"):
+                op.enable_p2p(2 * T * spec.top_k, combine=mode)
+                Yp, ms_p, _ = timed(lambda st_: op(X, idx, w, src, st_))
+                eng.sync()
+                same = torch.tensor([int(torch.equal(Yp, Y))], device=eng.device)
+                if world > 1:
+                    dist.all_reduce(same, op=dist.ReduceOp.MIN)
+                results[policy].update({f"p2p_{mode}_ms_per_step": ms_p,
+                                        f"p2p_{mode}_bit_identical": bool(same.item())})
     if rank == 0:
         base = results["round_robin"]["inter_node_bytes"]
         saved = 1.0 - results["learned"]["inter_node_bytes"] / base if base else float("nan")

@@ -325,3 +325,24 @@ def test_coactivation_unaligned_ids(eng, oracle, k):
     c = eng.coactivation(buf[1:].view(T, k), E)
     eng.sync()
     np.testing.assert_array_equal(c.cpu().numpy(), oracle.coactivation(idx, E))
+
+
+@pytest.mark.parametrize("mode", ["pull", "push"])
+def test_p2p_dispatch_combine_matches_local(eng, mode):
+    """K6-P2P at world 1 (the peer map is this rank's own buffers): the fused
+    dispatch / return / combine equals gather + local permute + combine."""
+    from paper_2604_23150_b200.a2a import ExpertParallelA2A
+    rng = np.random.default_rng(5)
+    T, E, k, D, H = 3000, 64, 4, 8, 256
+    idx = dev(random_idx(rng, T, E, k))
+    w = torch.rand(T, k, device="cuda")
+    w = w / w.sum(1, keepdim=True)
+    X = torch.randn(T, H, device="cuda").to(torch.bfloat16)
+    src = dev(rng.integers(0, D, T).astype(np.uint8))
+    pl, top = make_placement(rng, E, D, 0), topo(D, 2)
+    op = ExpertParallelA2A(eng, pl, top, H, T * k)
+    ref = op(X, idx, w, src)
+    op.enable_p2p(2 * T * k, combine=mode)
+    got = op(X, idx, w, src)
+    eng.sync()
+    assert torch.equal(got, ref)

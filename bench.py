@@ -318,8 +318,7 @@ def run_gpu_arm(args, spec):
     if graphed:  # kernels replayed from the graphs: launches per step x steps
         launches = pipe.launches_per_step * args.steps
     ms = start.elapsed_time(end)
-    router_ms = pipe.graph_router_ms() if graphed else \
-        [a.elapsed_time(b) for a, b in pipe.router_events]
+    router_ms = pipe.graph_router_ms() if graphed else pipe.router_ms()
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)

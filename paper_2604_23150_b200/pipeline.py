@@ -389,9 +389,28 @@ class RoutingPipeline:
         if getattr(self, "graphs", None):
             return self._replay(group)
         self.stats.zero_()
-        for l in range(self.spec.layers):
-            self.layer(l, self.X[l], timed_router)
+        if self.side_mode == 3 and timed_router:
+            # the main stream carries only the router chain: time it as a whole
+            # (no event pair between consecutive routers)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(self.eng.stream)
+            for l in range(self.spec.layers):
+                self._overlapped_layer(l, self.X[l], False)
+            e1.record(self.eng.stream)
+            self.router_events.append((e0, e1, self.spec.layers))
+        else:
+            for l in range(self.spec.layers):
+                self.layer(l, self.X[l], timed_router)
         self.reduce_and_score(group)
+
+    def router_ms(self):
+        """Per-launch router times (ms) recorded by timed steps."""
+        out = []
+        for ev in self.router_events:
+            n = ev[2] if len(ev) > 2 else 1
+            out += [ev[0].elapsed_time(ev[1]) / n] * n
+        return out
 
     def _overlapped_layer(self, l: int, X: torch.Tensor, timed_router=False):
         """Router of layer l on the main context (most SMs, high-priority

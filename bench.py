@@ -387,6 +387,7 @@ def run_gpu_arm(args, spec):
                            "l2": "inputs larger than L2 (each layer's X is "
                                  f"{spec.tokens * spec.hidden * 2 / 2**20:.0f} MiB)"},
                 "a2a_bytes_saved_pct": res["a2a_bytes_saved_pct"],
+                "searched_a2a_bytes_saved_pct": res["searched_bytes_saved_pct"],
                 "normalized_inter_node_bytes": res["normalized"],
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches, "cuda_graph": graphed, "clocks": clocks.summary()}

@@ -22,7 +22,6 @@ from __future__ import annotations
 
 import math
 import os
-import sys
 from dataclasses import dataclass, replace
 from typing import Optional
 

@@ -459,19 +459,8 @@ class RoutingPipeline:
         if getattr(self, "graphs", None):
             return self._replay(group)
         self.stats.zero_()
-        if self.side_mode == 3 and timed_router:
-            # the main stream carries only the router chain: time it as a whole
-            # (no event pair between consecutive routers)
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(self.eng.stream)
-            for l in range(self.spec.layers):
-                self._overlapped_layer(l, self.X[l], False)
-            e1.record(self.eng.stream)
-            self.router_events.append((e0, e1, self.spec.layers))
-        else:
-            for l in range(self.spec.layers):
-                self.layer(l, self.X[l], timed_router)
+        for l in range(self.spec.layers):
+            self.layer(l, self.X[l], timed_router)
         self.reduce_and_score(group)
 
     def router_ms(self):

@@ -94,3 +94,30 @@ def test_router_and_coact_graph_replay(eng):
         torch.cuda.synchronize()
         assert torch.equal(idx, ri) and torch.equal(w, rw), rep
         assert torch.equal(co, rc), rep
+
+
+def test_sm_budget_changes_nothing_but_the_grid(eng):
+    """Contexts sized for fewer SMs (the overlapped schedule: router on 128,
+    statistics on 20): the router's logits stay within the fp32
+    accumulation-order bound (the split-K tail of the last wave depends on the
+    unit count), its top-k equals the oracle's on the budgeted logits, and the
+    integer kernels (co-activation) are bit-identical."""
+    T, H, E, k = 65536, 1024, 256, 8
+    g = torch.Generator(device="cuda").manual_seed(9)
+    X = torch.randn(T, H, device="cuda", generator=g).to(torch.bfloat16)
+    W = (torch.randn(E, H, device="cuda", generator=g) / H ** 0.5).to(torch.bfloat16)
+    full = mp.Engine(0)
+    ref_idx, ref_w, ref_logits = full.router_topk(X, W, k, 1, True, want_logits=True)
+    ref_c = full.coactivation(ref_idx, E)
+    tol = 1e-4 * H ** 0.5 * float(X.float().pow(2).mean().sqrt()) * \
+        float(W.float().pow(2).mean().sqrt()) + 1e-5
+    for sms in (128, 20, 2):
+        e = mp.Engine(0)
+        e.set_sm_budget(sms)
+        idx, w, logits = e.router_topk(X, W, k, 1, True, want_logits=True)
+        c = e.coactivation(ref_idx, E)
+        torch.cuda.synchronize()
+        assert (logits - ref_logits).abs().max().item() <= tol, sms
+        ti, tw = e.topk_logits(logits, k, 1, True)
+        assert torch.equal(ti, idx) and torch.equal(tw, w), sms
+        assert torch.equal(c, ref_c), sms

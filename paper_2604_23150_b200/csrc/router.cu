@@ -37,6 +37,11 @@ namespace {
 
 constexpr int kBM = 128;
 constexpr int kBK = 64;  // 64 bf16 = 128 bytes: one 128B swizzle atom per row
+#ifndef MPB_ROUTER_KBLOCKS
+#define MPB_ROUTER_KBLOCKS 1  // 64-column K blocks per pipeline stage (build-time knob)
+#endif
+constexpr int kKB = MPB_ROUTER_KBLOCKS;
+constexpr int kStageK = kBK * kKB;  // K columns per stage
 constexpr int kThreadsR = 384;  // 4 non-epilogue + 8 epilogue warps
 
 #ifndef MPB_ROUTER_STAGES_CAP
@@ -45,8 +50,10 @@ constexpr int kThreadsR = 384;  // 4 non-epilogue + 8 epilogue warps
 
 template <int N, int KMAX, bool PAIR>
 struct RCfg {
-    static constexpr int A_BYTES = kBM * kBK * 2;
-    static constexpr int B_BYTES = (PAIR ? N / 2 : N) * kBK * 2;  // pair: this CTA's half of W
+    static constexpr int A_BLOCK = kBM * kBK * 2;                       // one 64-col box
+    static constexpr int B_BLOCK = (PAIR ? N / 2 : N) * kBK * 2;       // pair: half of W
+    static constexpr int A_BYTES = A_BLOCK * kKB;
+    static constexpr int B_BYTES = B_BLOCK * kKB;
     static constexpr int STAGE = A_BYTES + B_BYTES;
     static constexpr uint32_t TMEM_COLS = 2 * N < 32 ? 32 : 2 * N;
     static constexpr int ROWS_PER_TILE = PAIR ? 2 * kBM : kBM;
@@ -183,7 +190,7 @@ __global__ void __launch_bounds__(kThreadsR, 1)
         __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
-    const uint32_t nk = p.H / kBK;
+    const uint32_t nk = p.H / kStageK;
     // PDL: setup above overlapped the previous kernel; X, W, idx/w and the
     // split-tail workspace are touched only after it completed
     pdl_trigger();
@@ -204,16 +211,24 @@ __global__ void __launch_bounds__(kThreadsR, 1)
                     // both CTAs' loads complete on the leader's full barrier
                     if (rank == 0) ptx::mbar_arrive_expect_tx(&full[stage], 2 * Cfg::STAGE);
                     const uint32_t bar = ptx::mapa(ptx::smem_u32(&full[stage]), 0);
-                    ptx::tma_load_2d_2sm(&tmX, bar, sA + stage * Cfg::A_BYTES, kb * kBK, m0,
-                                         pol_x);
-                    ptx::tma_load_2d_2sm(&tmW, bar, sB + stage * Cfg::B_BYTES, kb * kBK,
-                                         static_cast<int32_t>(rank) * (N / 2), pol_w);
+#pragma unroll
+                    for (int j = 0; j < kKB; ++j) {
+                        const int32_t kc = static_cast<int32_t>(kb * kStageK + j * kBK);
+                        ptx::tma_load_2d_2sm(&tmX, bar, sA + stage * Cfg::A_BYTES + j * Cfg::A_BLOCK,
+                                             kc, m0, pol_x);
+                        ptx::tma_load_2d_2sm(&tmW, bar, sB + stage * Cfg::B_BYTES + j * Cfg::B_BLOCK,
+                                             kc, static_cast<int32_t>(rank) * (N / 2), pol_w);
+                    }
                 } else {
                     ptx::mbar_arrive_expect_tx(&full[stage], Cfg::STAGE);
-                    ptx::tma_load_2d(&tmX, &full[stage], sA + stage * Cfg::A_BYTES, kb * kBK, m0,
-                                     pol_x);
-                    ptx::tma_load_2d(&tmW, &full[stage], sB + stage * Cfg::B_BYTES, kb * kBK, 0,
-                                     pol_w);
+#pragma unroll
+                    for (int j = 0; j < kKB; ++j) {
+                        const int32_t kc = static_cast<int32_t>(kb * kStageK + j * kBK);
+                        ptx::tma_load_2d(&tmX, &full[stage], sA + stage * Cfg::A_BYTES + j * Cfg::A_BLOCK,
+                                         kc, m0, pol_x);
+                        ptx::tma_load_2d(&tmW, &full[stage], sB + stage * Cfg::B_BYTES + j * Cfg::B_BLOCK,
+                                         kc, 0, pol_w);
+                    }
                 }
                 if (++stage == S) {
                     stage = 0;
@@ -234,15 +249,20 @@ __global__ void __launch_bounds__(kThreadsR, 1)
             for (uint32_t kb = it.k0; kb < it.k1; ++kb) {
                 ptx::mbar_wait(&full[stage], phase);
                 ptx::tc_fence_after();
-                const uint64_t ad = ptx::sw128_kmajor_desc(ptx::smem_u32(sA + stage * Cfg::A_BYTES));
-                const uint64_t bd = ptx::sw128_kmajor_desc(ptx::smem_u32(sB + stage * Cfg::B_BYTES));
 #pragma unroll
-                for (int kk = 0; kk < kBK / 16; ++kk) {  // +32 bytes along K per UMMA_K = 16
-                    const uint32_t accum = (kb != it.k0) | (kk != 0);
-                    if constexpr (PAIR)
-                        ptx::mma_bf16_2sm(d, ad + 2 * kk, bd + 2 * kk, idesc, accum);
-                    else
-                        ptx::mma_bf16(d, ad + 2 * kk, bd + 2 * kk, idesc, accum);
+                for (int j = 0; j < kKB; ++j) {
+                    const uint64_t ad = ptx::sw128_kmajor_desc(
+                        ptx::smem_u32(sA + stage * Cfg::A_BYTES + j * Cfg::A_BLOCK));
+                    const uint64_t bd = ptx::sw128_kmajor_desc(
+                        ptx::smem_u32(sB + stage * Cfg::B_BYTES + j * Cfg::B_BLOCK));
+#pragma unroll
+                    for (int kk = 0; kk < kBK / 16; ++kk) {  // +32 bytes along K per UMMA_K = 16
+                        const uint32_t accum = (kb != it.k0) | (j != 0) | (kk != 0);
+                        if constexpr (PAIR)
+                            ptx::mma_bf16_2sm(d, ad + 2 * kk, bd + 2 * kk, idesc, accum);
+                        else
+                            ptx::mma_bf16(d, ad + 2 * kk, bd + 2 * kk, idesc, accum);
+                    }
                 }
                 if constexpr (PAIR)
                     ptx::mma_commit_2sm_mc(&empty[stage], 0x3);  // frees the stage in both CTAs
@@ -564,7 +584,7 @@ mpb_status launch_router_n(mpb_context *ctx, const CUtensorMap &mx, const CUtens
     // its tiles are split in two K halves over twice as many units
     const uint32_t full_units = PAIR ? static_cast<uint32_t>(ctx->num_sms) / 2
                                      : static_cast<uint32_t>(ctx->num_sms);
-    const uint32_t nk = p.H / kBK;
+    const uint32_t nk = p.H / kStageK;
     const uint32_t waves = p.num_tiles / full_units;
     const uint32_t rem = p.num_tiles - waves * full_units;
     p.split_tail = rem > 0 && 2 * rem <= full_units && nk >= 2 && !std::getenv("MPB_ROUTER_NO_SPLIT");
@@ -634,7 +654,9 @@ extern "C" mpb_status mpb_router_topk(mpb_context *ctx, const void *X, const voi
         return fail(MPB_VALIDATION_ERROR, "mpb_router_topk: NULL argument");
     if (E != 64 && E != 128 && E != 256)
         return fail(MPB_CONFIG_ERROR, "mpb_router_topk: E must be 64, 128 or 256");
-    if (H == 0 || H % kBK != 0) return fail(MPB_CONFIG_ERROR, "mpb_router_topk: H % 64 != 0");
+    if (H == 0 || H % kStageK != 0)
+        return fail(MPB_CONFIG_ERROR, "mpb_router_topk: H must be a multiple of " +
+                                          std::to_string(kStageK));
     if (k == 0 || k > 16 || k > E) return fail(MPB_CONFIG_ERROR, "mpb_router_topk: need 1 <= k <= 16");
     if (score_fn != MPB_SCORE_SOFTMAX && score_fn != MPB_SCORE_SIGMOID)
         return fail(MPB_CONFIG_ERROR, "mpb_router_topk: unknown score_fn");

@@ -21,6 +21,7 @@
 // (No reference implementation: the closest analogue is aggregate_usage,
 // /root/reference/proj/core/src/placement.cpp:96-125.)
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
 #include "internal.cuh"
@@ -264,6 +265,11 @@ __global__ void __launch_bounds__(kMmaThreads, 1)
             for (uint32_t n = 0; n < nch; ++n) {
                 const uint32_t s = n % kMmaStages;
                 if (n >= kMmaStages) ptx::mbar_wait(&idempty[s], ((n / kMmaStages) - 1) & 1);
+                // the producers' generic reads of this slot (ordered by the idempty
+                // barrier) must also be ordered before the async-proxy bulk write
+                // that overwrites it: without this proxy fence a bulk copy can land
+                // under a producer still reading the previous chunk's ids
+                ptx::fence_proxy_async_smem();
                 const uint64_t t = tok0 + static_cast<uint64_t>(n) * 128;
                 const uint32_t ntok = static_cast<uint32_t>(min(static_cast<uint64_t>(128), tok1 - t));
                 const uint32_t bytes = ntok * k * 4;

@@ -83,6 +83,7 @@ struct RouterParams {
     uint32_t epoch;
     float *partial;      // [slot][rank][N/16 chunks][128 rows][16]
     uint32_t *flags;     // [slot][rank]: 1 when the partial is ready, reset to 0 by the reader
+    uint32_t E;          // real experts (<= N): columns >= E are padding, never selected
 };
 
 // Work item n of a scheduling unit: full waves of whole tiles, then (split
@@ -371,19 +372,30 @@ __global__ void __launch_bounds__(kThreadsR, 1)
                 ti[j] = j < off ? -1 : 0x7FFFFFFF;
             }
             float m = -INFINITY;
-            float *lrow = (p.logits && row < p.T) ? p.logits + row * N : nullptr;
+            float *lrow = (p.logits && row < p.T) ? p.logits + row * p.E : nullptr;
 #pragma unroll 1
             for (int c = half * NH; c < (half + 1) * NH; c += 16) {
                 uint32_t r[16];
                 ptx::tmem_ld_32x32b_x16(taddr + c, r);
                 ptx::tmem_ld_wait();
-                if (lrow) {
-                    float4 *dst = reinterpret_cast<float4 *>(lrow + c);
+                const bool padded = static_cast<uint32_t>(c + 16) > p.E;
+                if (padded)  // padding columns (E < N): -inf, never selected
 #pragma unroll
-                    for (int i = 0; i < 4; ++i)
-                        dst[i] = make_float4(__uint_as_float(r[4 * i]), __uint_as_float(r[4 * i + 1]),
-                                             __uint_as_float(r[4 * i + 2]),
-                                             __uint_as_float(r[4 * i + 3]));
+                    for (int i = 0; i < 16; ++i)
+                        if (static_cast<uint32_t>(c + i) >= p.E) r[i] = __float_as_uint(-INFINITY);
+                if (lrow) {
+                    if (!padded && (p.E & 3) == 0) {
+                        float4 *dst = reinterpret_cast<float4 *>(lrow + c);
+#pragma unroll
+                        for (int i = 0; i < 4; ++i)
+                            dst[i] = make_float4(__uint_as_float(r[4 * i]), __uint_as_float(r[4 * i + 1]),
+                                                 __uint_as_float(r[4 * i + 2]),
+                                                 __uint_as_float(r[4 * i + 3]));
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < 16; ++i)
+                            if (static_cast<uint32_t>(c + i) < p.E) lrow[c + i] = __uint_as_float(r[i]);
+                    }
                 }
                 const float thr = tv[KMAX - 1];
                 uint32_t hit = 0;
@@ -423,7 +435,8 @@ __global__ void __launch_bounds__(kThreadsR, 1)
 #pragma unroll
                     for (int i = 0; i < 16; ++i) {
                         const float v = __uint_as_float(r[i]);
-                        ssum += v == v ? exp2f(fmaf(v, 1.4426950408889634f, -mlog)) : 0.f;
+                        const bool real = static_cast<uint32_t>(c + i) < p.E;
+                        ssum += (real && v == v) ? exp2f(fmaf(v, 1.4426950408889634f, -mlog)) : 0.f;
                     }
                 }
             }
@@ -476,7 +489,7 @@ __global__ void __launch_bounds__(kThreadsR, 1)
                             for (int i = 0; i < 16; ++i) {
                                 const float v = __uint_as_float(r[i]);
                                 const bool want = pass == 0 ? v == -INFINITY : v != v;
-                                if (!want) continue;
+                                if (!want || static_cast<uint32_t>(c + i) >= p.E) continue;
                                 bool placed = false;
 #pragma unroll
                                 for (int j = 0; j < KMAX; ++j)
@@ -652,8 +665,7 @@ extern "C" mpb_status mpb_router_topk(mpb_context *ctx, const void *X, const voi
                                       int32_t *idx, float *weights, float *logits_out) {
     if (!ctx || (T && (!X || !W || !idx || !weights)))
         return fail(MPB_VALIDATION_ERROR, "mpb_router_topk: NULL argument");
-    if (E != 64 && E != 128 && E != 256)
-        return fail(MPB_CONFIG_ERROR, "mpb_router_topk: E must be 64, 128 or 256");
+    if (E == 0 || E > 256) return fail(MPB_CONFIG_ERROR, "mpb_router_topk: need 1 <= E <= 256");
     if (H == 0 || H % kStageK != 0)
         return fail(MPB_CONFIG_ERROR, "mpb_router_topk: H must be a multiple of " +
                                           std::to_string(kStageK));
@@ -665,7 +677,7 @@ extern "C" mpb_status mpb_router_topk(mpb_context *ctx, const void *X, const voi
     if (T == 0) return MPB_OK;
     if (T > 0x7fffffffull) return fail(MPB_CONFIG_ERROR, "mpb_router_topk: T too large");
     RouterParams p{T, H, k, score_fn, renorm, static_cast<uint32_t>((T + kBM - 1) / kBM),
-                   idx, weights, logits_out, 0, 0, nullptr, nullptr};
+                   idx, weights, logits_out, 0, 0, nullptr, nullptr, E};
     CUtensorMap mx, mw;
     // E = 256 (tensor-bound): 2-SM CTA pairs (UMMA M=256) by default;
     // MPB_ROUTER_SINGLE=1 forces the single-CTA kernel. E <= 128 is HBM-bound:
@@ -674,11 +686,14 @@ extern "C" mpb_status mpb_router_topk(mpb_context *ctx, const void *X, const voi
         const char *v = std::getenv("MPB_ROUTER_SINGLE");
         return v && v[0] == '1';
     }();
-    const bool pair = E == 256 && !single;
-    if (!make_map(&mx, X, T, H, kBM) || !make_map(&mw, W, E, H, pair ? E / 2 : E))
+    // the tile width N is the next of 64 / 128 / 256: W rows past E come in as
+    // TMA out-of-bounds zeros and their columns are masked in the epilogue
+    const uint32_t N = E <= 64 ? 64 : E <= 128 ? 128 : 256;
+    const bool pair = N == 256 && !single;
+    if (!make_map(&mx, X, T, H, kBM) || !make_map(&mw, W, E, H, pair ? N / 2 : N))
         return fail(MPB_CUDA_ERROR, "mpb_router_topk: cuTensorMapEncodeTiled failed");
     if (pair) return launch_router_k<256, true>(ctx, mx, mw, p);
-    if (E == 64) return launch_router_k<64, false>(ctx, mx, mw, p);
-    if (E == 128) return launch_router_k<128, false>(ctx, mx, mw, p);
+    if (N == 64) return launch_router_k<64, false>(ctx, mx, mw, p);
+    if (N == 128) return launch_router_k<128, false>(ctx, mx, mw, p);
     return launch_router_k<256, false>(ctx, mx, mw, p);
 }

@@ -24,7 +24,10 @@ def eng():
 CASES = [  # T, H, E, k, score_fn, renorm
     (128, 64, 64, 2, 0, False), (1000, 512, 128, 8, 0, True), (4096, 4096, 128, 8, 0, False),
     (2048, 7168, 256, 8, 1, True), (3001, 5120, 128, 1, 1, False), (257, 1024, 256, 16, 0, True),
-    (65536, 7168, 256, 8, 1, True)]
+    (65536, 7168, 256, 8, 1, True),
+    # E not a tile width: padded to 64 / 128 / 256 with masked columns
+    (4096, 1024, 160, 8, 1, True), (3000, 512, 96, 6, 0, False), (2048, 768, 32, 2, 0, True),
+    (1000, 256, 8, 2, 0, False), (5000, 2048, 200, 16, 1, True), (777, 128, 1, 1, 1, False)]
 
 
 @pytest.mark.parametrize("case", CASES)

@@ -20,6 +20,10 @@ SPEC = WorkloadSpec("tiny", 4, 8192, 512, 64, 8, 1, True, groups=8, nodes=2, dom
 
 def _run(mode, monkeypatch):
     monkeypatch.setenv("MPB_SIDE_STREAM", str(mode))
+    # a 4-SM side context: its layout and co-activation CTAs loop over many
+    # chunks (pipeline stages recycled), as the 20-SM side context does at the
+    # DSv3 shape
+    monkeypatch.setenv("MPB_SIDE_SMS", "4")
     cur = torch.cuda.current_stream()
     eng = mp.Engine(0)
     pipe = RoutingPipeline(SPEC, eng, 0, 1, resident=True)

@@ -34,6 +34,10 @@ def dev(a, dtype=None):
 def random_idx(rng, T, E, k):
     if T == 0:
         return np.zeros((0, k), np.int32)
+    if T > 100000:  # bounded host memory for the large cases
+        return np.concatenate([np.argsort(rng.random((min(65536, T - t), E), dtype=np.float32),
+                                          axis=1)[:, :k] for t in range(0, T, 65536)]
+                              ).astype(np.int32)
     return np.argsort(rng.random((T, E)), axis=1)[:, :k].astype(np.int32)
 
 
@@ -176,7 +180,9 @@ def test_device_sampler_matches_oracle(eng, oracle):
 LAYOUT_CASES = [  # T, E, D, nodes, k, redundancy, block_src
     (0, 64, 4, 2, 2, 0, False), (1, 16, 2, 2, 2, 0, False), (999, 64, 4, 2, 4, 1, False),
     (4096, 128, 8, 2, 8, 0, False), (5000, 256, 8, 4, 8, 2, True), (70000, 128, 8, 8, 1, 0, False),
-    (65536, 256, 8, 2, 8, 0, True), (3333, 64, 16, 4, 6, 3, False)]
+    (65536, 256, 8, 2, 8, 0, True), (3333, 64, 16, 4, 6, 3, False),
+    # > 4 groups of 128 pairs per warp: slot ids recomputed in the rank pass
+    (1048576, 128, 8, 2, 8, 0, False)]
 
 
 @pytest.mark.parametrize("case", LAYOUT_CASES)

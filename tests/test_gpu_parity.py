@@ -370,3 +370,17 @@ def test_coactivation_many_chunks_per_cta(oracle, sms):
         c = e.coactivation(d, E)
         e.sync()
         np.testing.assert_array_equal(c.cpu().numpy(), ref)
+
+
+def test_coactivation_multi_launch_accumulates(oracle):
+    """Beyond 511 chunks per CTA (u16 partials) the token range is split over
+    several launches that accumulate into C: at a 2-SM budget 300,000 tokens
+    take three launches."""
+    rng = np.random.default_rng(21)
+    T, E, k = 300000, 256, 8
+    idx = random_idx(rng, T, E, k)
+    e = mp.Engine(0)
+    e.set_sm_budget(2)
+    c = e.coactivation(dev(idx), E)
+    e.sync()
+    np.testing.assert_array_equal(c.cpu().numpy(), oracle.coactivation(idx, E))

@@ -16,12 +16,15 @@ ap.add_argument("--k", type=int, default=8)
 ap.add_argument("--fn", type=int, default=1)
 ap.add_argument("--iters", type=int, default=5)
 ap.add_argument("--sms", type=int, default=0, help="SM budget (0 = all)")
+ap.add_argument("--nx", type=int, default=1, help="distinct X / W buffers rotated per launch")
+ap.add_argument("--events", action="store_true", help="an event pair around every launch")
 a = ap.parse_args()
 eng = mp.Engine(0)
 if a.sms:
     eng.set_sm_budget(a.sms)
-X = torch.randn(a.T, a.H, device="cuda").to(torch.bfloat16)
-W = (torch.randn(a.E, a.H, device="cuda") / a.H ** 0.5).to(torch.bfloat16)
+Xs = [torch.randn(a.T, a.H, device="cuda").to(torch.bfloat16) for _ in range(a.nx)]
+Ws = [(torch.randn(a.E, a.H, device="cuda") / a.H ** 0.5).to(torch.bfloat16) for _ in range(a.nx)]
+X, W = Xs[0], Ws[0]
 out = (torch.empty(a.T, a.k, dtype=torch.int32, device="cuda"),
        torch.empty(a.T, a.k, dtype=torch.float32, device="cuda"))
 for _ in range(2):
@@ -29,11 +32,20 @@ for _ in range(2):
 torch.cuda.synchronize()
 s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 s.record()
-for _ in range(a.iters):
-    eng.router_topk(X, W, a.k, a.fn, True, out=out)
+pairs = []
+for i in range(a.iters):
+    if a.events:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+    eng.router_topk(Xs[i % a.nx], Ws[i % a.nx], a.k, a.fn, True, out=out)
+    if a.events:
+        e1.record()
+        pairs.append((e0, e1))
 e.record()
 torch.cuda.synchronize()
 ms = s.elapsed_time(e) / a.iters
+if pairs:
+    print(f"per-launch events: {sum(x.elapsed_time(y) for x, y in pairs) / len(pairs):.4f} ms")
 tf = 2 * a.T * a.H * a.E / ms / 1e9
 print(f"router T={a.T} H={a.H} E={a.E} k={a.k}: {ms:.4f} ms  {tf:.1f} TFLOP/s  "
       f"{(a.T * a.H * 2) / ms / 1e6:.0f} GB/s(X)")

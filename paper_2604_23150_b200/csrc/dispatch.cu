@@ -15,7 +15,11 @@
 // order (bit-identical to the local combine).
 #include <cuda_bf16.h>
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "internal.cuh"
+#include "tc_ptx.cuh"
 
 namespace mpb {
 namespace {
@@ -110,7 +114,17 @@ __global__ void __launch_bounds__(256) k_dispatch_p2p(const uint4 *X, const int3
     const uint64_t tok = static_cast<uint64_t>(sorted_pairs[i]) / k;
     const uint4 *src = X + tok * hv;
     uint4 *dst = reinterpret_cast<uint4 *>(peer_recv[r]) + row * hv;
-    for (uint32_t c = lane; c < hv; c += 32) dst[c] = __ldg(src + c);
+    // batches of 8 independent 16-byte loads before their remote stores: more
+    // bytes in flight per warp over NVLink
+    uint32_t c = lane;
+    for (; c + 7 * 32 < hv; c += 8 * 32) {
+        uint4 v[8];
+#pragma unroll
+        for (int b = 0; b < 8; ++b) v[b] = __ldg(src + c + b * 32);
+#pragma unroll
+        for (int b = 0; b < 8; ++b) dst[c + b * 32] = v[b];
+    }
+    for (; c < hv; c += 32) dst[c] = __ldg(src + c);
 }
 
 __global__ void __launch_bounds__(256) k_combine_p2p(const int32_t *pair_pos, const float *w,
@@ -146,6 +160,57 @@ __global__ void __launch_bounds__(256) k_combine_p2p(const int32_t *pair_pos, co
         for (int q = 0; q < 4; ++q) oh[q] = __floats2bfloat162_rn(acc[2 * q], acc[2 * q + 1]);
         Y[t * hv + c] = o;
     }
+}
+
+// TMA variant of the dispatch: one issuing thread per CTA streams rows
+// through a ring of kRing shared-memory row buffers — bulk load of the token's
+// row from local HBM, then bulk store straight into the destination rank's
+// receive buffer (large NVLink transactions, no per-lane stores). Rows are
+// dealt round-robin over the CTAs; loads run kRing-1 rows ahead.
+constexpr int kRing = 8;
+__global__ void __launch_bounds__(32) k_dispatch_p2p_tma(const uint8_t *X, const int32_t *sorted_pairs,
+                                                         uint64_t n, uint32_t k, uint32_t row_bytes,
+                                                         const int64_t *C, const int64_t *ko,
+                                                         uint32_t span, uint32_t world, uint32_t me,
+                                                         const uint64_t *peer_recv, uint64_t cap,
+                                                         uint32_t *err) {
+    extern __shared__ __align__(128) uint8_t s_buf[];  // [kRing][row_bytes]
+    __shared__ P2PMap m;
+    __shared__ __align__(8) uint64_t bars[kRing];
+    if (threadIdx.x != 0) return;
+    p2p_map(C, ko, span, world, me, m);
+    for (int i = 0; i < kRing; ++i) ptx::mbar_init(&bars[i], 1);
+    ptx::fence_barrier_init();
+    const uint64_t first = blockIdx.x, step = gridDim.x;
+    const uint64_t cnt = first < n ? (n - first + step - 1) / step : 0;
+    auto row_of = [&](uint64_t j) { return first + j * step; };
+    auto load = [&](uint64_t j) {
+        const int slot = static_cast<int>(j % kRing);
+        const uint64_t tok = static_cast<uint64_t>(sorted_pairs[row_of(j)]) / k;
+        ptx::mbar_arrive_expect_tx(&bars[slot], row_bytes);
+        ptx::bulk_load(s_buf + static_cast<size_t>(slot) * row_bytes, X + tok * row_bytes, row_bytes,
+                       &bars[slot]);
+    };
+    for (uint64_t j = 0; j < cnt && j < kRing; ++j) load(j);
+    for (uint64_t j = 0; j < cnt; ++j) {
+        const int slot = static_cast<int>(j % kRing);
+        ptx::mbar_wait(&bars[slot], static_cast<uint32_t>((j / kRing) & 1));
+        const uint64_t i = row_of(j);
+        const uint32_t r = rank_of_pos(m, world, static_cast<int64_t>(i));
+        const uint64_t row = static_cast<uint64_t>(m.base[r] + static_cast<int64_t>(i) - m.first[r]);
+        if (row < cap) {
+            ptx::bulk_store(reinterpret_cast<uint8_t *>(peer_recv[r]) + row * row_bytes,
+                            s_buf + static_cast<size_t>(slot) * row_bytes, row_bytes);
+        } else {
+            atomicOr(err, kErrCapacity);
+        }
+        ptx::bulk_commit();
+        if (j >= 1 && j - 1 + kRing < cnt) {
+            ptx::bulk_wait_read<1>();  // row j-1's store has left its buffer
+            load(j - 1 + kRing);
+        }
+    }
+    ptx::bulk_wait<0>();  // every store complete before the CTA exits
 }
 
 // Return leg, pushed: every row this rank received goes back to its source
@@ -233,6 +298,22 @@ mpb_status mpb_dispatch_p2p(mpb_context *ctx, const void *X, const int32_t *sort
     if (world < 1 || world > 8 || rank >= world)
         return fail(MPB_CONFIG_ERROR, "mpb_dispatch_p2p: need 1 <= world <= 8, rank < world");
     if (n_pairs == 0) return MPB_OK;
+    static const bool tma = [] {
+        const char *v = std::getenv("MPB_P2P_TMA");
+        return !(v && v[0] == '0');
+    }();
+    const size_t row_bytes = size_t(H) * 2;
+    if (tma && (reinterpret_cast<uintptr_t>(X) & 15) == 0 && kRing * row_bytes <= 200 * 1024) {
+        const size_t smem = kRing * row_bytes;
+        MPB_CUDA(cudaFuncSetAttribute(k_dispatch_p2p_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(smem)));
+        const unsigned ctas = static_cast<unsigned>(std::min<uint64_t>(n_pairs, ctx->num_sms * 2ull));
+        k_dispatch_p2p_tma<<<ctas, 32, smem, ctx->stream>>>(
+            static_cast<const uint8_t *>(X), sorted_pairs, n_pairs, k, static_cast<uint32_t>(row_bytes),
+            counts, key_offsets, span, world, rank, peer_recv, capacity_rows, ctx->d_error);
+        MPB_LAUNCHED(ctx);
+        return MPB_OK;
+    }
     k_dispatch_p2p<<<static_cast<unsigned>((n_pairs + 7) / 8), 256, 0, ctx->stream>>>(
         static_cast<const uint4 *>(X), sorted_pairs, n_pairs, k, H / 8, counts, key_offsets, span,
         world, rank, peer_recv, capacity_rows, ctx->d_error);

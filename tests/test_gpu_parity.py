@@ -384,3 +384,30 @@ def test_coactivation_multi_launch_accumulates(oracle):
     c = e.coactivation(dev(idx), E)
     e.sync()
     np.testing.assert_array_equal(c.cpu().numpy(), oracle.coactivation(idx, E))
+
+
+@pytest.mark.parametrize("sms", [0, 2])
+def test_score_placements_group_rows_pipeline_shape(oracle, sms):
+    """The pipeline's call: demand rows are source GROUPS folded to nodes
+    inside the kernel (row_node = group_to_node), 1024 candidates x 58 layers;
+    at a 2-SM budget every CTA loops over many candidates."""
+    rng = np.random.default_rng(31 + sms)
+    E, D, nodes, P, B = 256, 8, 2, 1024, 58
+    dem = rng.integers(0, 400, (B, D, E)).astype(np.uint64)
+    dem[dem < 150] = 0
+    g2n = [d // (D // nodes) for d in range(D)]
+    nd = np.zeros((B, nodes, E), np.uint64)
+    for d in range(D):
+        nd[:, g2n[d]] += dem[:, d]
+    luts = np.stack([oracle.dest_lut(make_placement(rng, E, D, p % 3).groups, g2n, E)
+                     for p in range(P)])
+    e = mp.Engine(0)
+    if sms:
+        e.set_sm_budget(sms)
+    g2n_t = dev(np.array(g2n, np.uint8))
+    inter, intra, rank = e.score_placements(dev(dem), dev(luts), g2n_t, D, row_node=g2n_t)
+    e.sync()
+    ri, ra, rr = oracle.score_placements(nd, luts, D, g2n)
+    np.testing.assert_array_equal(inter.cpu().numpy(), ri)
+    np.testing.assert_array_equal(intra.cpu().numpy(), ra)
+    np.testing.assert_array_equal(rank.cpu().numpy(), rr)

@@ -12,6 +12,7 @@
  *                          (placement.hpp:35-65, simulator.cpp:52-55,74-80)
  *   mpb_router_topk        (new) router GEMM + top-k; feeds what route_tokens
  *                          produces (trace.cpp:240-259)
+ *   mpb_router_topk_layers (new) the same for several layers in one launch
  *   mpb_topk_logits        (new) top-k over given logits, tie rule of
  *                          placement.cpp:143-152
  *   mpb_dispatch_layout    simulate_layer's per-destination accounting
@@ -114,6 +115,18 @@ MPB_API mpb_status mpb_build_dest_lut(const uint32_t *groups_flat, const uint32_
 MPB_API mpb_status mpb_router_topk(mpb_context *ctx, const void *X, const void *W, uint64_t T,
                                    uint32_t H, uint32_t E, uint32_t k, int score_fn, int renorm,
                                    int32_t *idx, float *weights, float *logits_out);
+/* mpb_router_topk for `layers` independent layers of the same shape in ONE
+ * persistent launch: X[l] [T,H] and W[l] [E,H] (host arrays of device
+ * pointers); idx / weights are [layers][T][k] (device). Results equal
+ * mpb_router_topk per layer up to the fp32 order of the split-K tail (the last
+ * wave of the whole launch). Only one exposed last-tile epilogue per launch
+ * instead of one per layer. The TMA descriptors are encoded and uploaded on
+ * the first call for a given (shape, X, W) set and cached in the context (the
+ * first call must not be inside a stream capture). */
+MPB_API mpb_status mpb_router_topk_layers(mpb_context *ctx, uint32_t layers, const void *const *X,
+                                          const void *const *W, uint64_t T, uint32_t H, uint32_t E,
+                                          uint32_t k, int score_fn, int renorm, int32_t *idx,
+                                          float *weights);
 /* Top-k over given fp32 logits [T,E] (device), E <= 1024. */
 MPB_API mpb_status mpb_topk_logits(mpb_context *ctx, const float *logits, uint64_t T, uint32_t E,
                                    uint32_t k, int score_fn, int renorm, int32_t *idx,

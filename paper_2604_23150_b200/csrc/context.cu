@@ -96,6 +96,7 @@ mpb_status mpb_context_destroy(mpb_context *ctx) {
     if (ctx->d_error) cudaFree(ctx->d_error);
     if (ctx->scratch) cudaFree(ctx->scratch);
     if (ctx->router_ws) cudaFree(ctx->router_ws);
+    for (auto &kv : ctx->router_maps) cudaFree(kv.second);
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
     delete ctx;
     return MPB_OK;

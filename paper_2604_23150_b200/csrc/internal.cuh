@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -87,6 +88,9 @@ struct mpb_context {
     size_t router_ws_bytes = 0;
     void *pinned = nullptr;  // small pinned host area (k-means control values)
     size_t pinned_bytes = 0;
+    // grouped router: device tables of TMA descriptors ([layer][X, W]), keyed by
+    // (shape, tile width, X / W pointers); written once, reused by every later call
+    std::map<std::vector<uint64_t>, void *> router_maps;
 };
 
 struct mpb_placement {

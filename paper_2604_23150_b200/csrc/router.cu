@@ -78,39 +78,45 @@ struct RouterParams {
     float *w;
     float *logits;
     // split-K tail (wave quantisation): the last partial wave's tiles are split in
-    // two K halves run by two units; the second half dumps its fp32 partial
-    uint32_t split_tail;
-    uint32_t epoch;
-    float *partial;      // [slot][rank][N/16 chunks][128 rows][16]
-    uint32_t *flags;     // [slot][rank]: 1 when the partial is ready, reset to 0 by the reader
+    // S K parts run by S units; parts 1..S-1 dump their fp32 partials, part 0 adds
+    // them (in part order) and finishes the tile. S = 1: no split
+    uint32_t splits;
+    float *partial;      // [slot][part-1][rank][N/16 chunks][128 rows][16]
+    uint32_t *flags;     // [slot][rank]: partials ready, reset to 0 by the finisher
     uint32_t E;          // real experts (<= N): columns >= E are padding, never selected
+    // grouped launch over several layers: tile t belongs to layer t / tiles_per_layer;
+    // maps = [layer][X, W] descriptors in global memory (nullptr: the kernel
+    // parameters tmX / tmW, one layer); idx / w are [layers][T][k]
+    const CUtensorMap *maps;
+    uint32_t tiles_per_layer;
+    uint32_t layers;
 };
 
 // Work item n of a scheduling unit: full waves of whole tiles, then (split
-// tail) unit u takes K-half (u & 1) of tail tile u / 2. role 0 = whole tile,
-// 1 = first K half + fix-up with the partial, 2 = second K half, dump only.
+// tail) unit u takes K part (u % S) of tail tile u / S. role 0 = whole tile,
+// 1 = K part 0 + fix-up with the other parts' partials, 2 = K part > 0, dump only.
 struct WorkItem {
-    uint32_t tile, k0, k1, role, slot;
+    uint32_t tile, k0, k1, role, slot, part;
 };
 
 __device__ __forceinline__ bool next_item(uint32_t n, uint32_t unit, uint32_t units,
-                                          uint32_t num_tiles, uint32_t nk, uint32_t split,
+                                          uint32_t num_tiles, uint32_t nk, uint32_t S,
                                           WorkItem &w) {
-    if (!split) {
+    if (S <= 1) {
         const uint32_t t = unit + n * units;
         if (t >= num_tiles) return false;
-        w = {t, 0, nk, 0, 0};
+        w = {t, 0, nk, 0, 0, 0};
         return true;
     }
     const uint32_t waves = num_tiles / units;
     if (n < waves) {
-        w = {unit + n * units, 0, nk, 0, 0};
+        w = {unit + n * units, 0, nk, 0, 0, 0};
         return true;
     }
     const uint32_t rem = num_tiles - waves * units;
-    if (n == waves && unit < 2 * rem) {
-        const uint32_t slot = unit >> 1, h = unit & 1;
-        w = {waves * units + slot, h ? nk / 2 : 0, h ? nk : nk / 2, h ? 2u : 1u, slot};
+    if (n == waves && unit < S * rem) {
+        const uint32_t slot = unit / S, h = unit - slot * S;
+        w = {waves * units + slot, h * nk / S, (h + 1) * nk / S, h ? 2u : 1u, slot, h};
         return true;
     }
     return false;
@@ -164,8 +170,8 @@ __global__ void __launch_bounds__(kThreadsR, 1)
     const uint32_t unit = PAIR ? blockIdx.x >> 1 : blockIdx.x;     // tile-scheduling unit
     const uint32_t units = PAIR ? gridDim.x >> 1 : gridDim.x;
     if (warp == 0 && lane == 0) {
-        ptx::tma_prefetch_desc(&tmX);
-        ptx::tma_prefetch_desc(&tmW);
+        ptx::tma_prefetch_desc(p.maps ? p.maps : &tmX);
+        ptx::tma_prefetch_desc(p.maps ? p.maps + 1 : &tmW);
         for (int s = 0; s < S; ++s) {
             ptx::mbar_init(&full[s], 1);
             ptx::mbar_init(&empty[s], 1);
@@ -204,8 +210,12 @@ __global__ void __launch_bounds__(kThreadsR, 1)
         int stage = 0;
         uint32_t phase = 0;
         WorkItem it;
-        for (uint32_t n = 0; next_item(n, unit, units, p.num_tiles, nk, p.split_tail, it); ++n) {
-            const int32_t m0 = static_cast<int32_t>(it.tile * Cfg::ROWS_PER_TILE + rank * kBM);
+        for (uint32_t n = 0; next_item(n, unit, units, p.num_tiles, nk, p.splits, it); ++n) {
+            const uint32_t layer = it.tile / p.tiles_per_layer;
+            const int32_t m0 = static_cast<int32_t>((it.tile - layer * p.tiles_per_layer) * Cfg::ROWS_PER_TILE +
+                                                    rank * kBM);
+            const CUtensorMap *mX = p.maps ? p.maps + 2 * layer : &tmX;
+            const CUtensorMap *mW = p.maps ? p.maps + 2 * layer + 1 : &tmW;
             for (uint32_t kb = it.k0; kb < it.k1; ++kb) {
                 ptx::mbar_wait(&empty[stage], phase ^ 1);
                 if constexpr (PAIR) {
@@ -215,9 +225,9 @@ __global__ void __launch_bounds__(kThreadsR, 1)
 #pragma unroll
                     for (int j = 0; j < kKB; ++j) {
                         const int32_t kc = static_cast<int32_t>(kb * kStageK + j * kBK);
-                        ptx::tma_load_2d_2sm(&tmX, bar, sA + stage * Cfg::A_BYTES + j * Cfg::A_BLOCK,
+                        ptx::tma_load_2d_2sm(mX, bar, sA + stage * Cfg::A_BYTES + j * Cfg::A_BLOCK,
                                              kc, m0, pol_x);
-                        ptx::tma_load_2d_2sm(&tmW, bar, sB + stage * Cfg::B_BYTES + j * Cfg::B_BLOCK,
+                        ptx::tma_load_2d_2sm(mW, bar, sB + stage * Cfg::B_BYTES + j * Cfg::B_BLOCK,
                                              kc, static_cast<int32_t>(rank) * (N / 2), pol_w);
                     }
                 } else {
@@ -225,9 +235,9 @@ __global__ void __launch_bounds__(kThreadsR, 1)
 #pragma unroll
                     for (int j = 0; j < kKB; ++j) {
                         const int32_t kc = static_cast<int32_t>(kb * kStageK + j * kBK);
-                        ptx::tma_load_2d(&tmX, &full[stage], sA + stage * Cfg::A_BYTES + j * Cfg::A_BLOCK,
+                        ptx::tma_load_2d(mX, &full[stage], sA + stage * Cfg::A_BYTES + j * Cfg::A_BLOCK,
                                          kc, m0, pol_x);
-                        ptx::tma_load_2d(&tmW, &full[stage], sB + stage * Cfg::B_BYTES + j * Cfg::B_BLOCK,
+                        ptx::tma_load_2d(mW, &full[stage], sB + stage * Cfg::B_BYTES + j * Cfg::B_BLOCK,
                                          kc, 0, pol_w);
                     }
                 }
@@ -243,7 +253,7 @@ __global__ void __launch_bounds__(kThreadsR, 1)
         int stage = 0;
         uint32_t phase = 0, acc = 0, aphase = 0;
         WorkItem it;
-        for (uint32_t n = 0; next_item(n, unit, units, p.num_tiles, nk, p.split_tail, it); ++n) {
+        for (uint32_t n = 0; next_item(n, unit, units, p.num_tiles, nk, p.splits, it); ++n) {
             ptx::mbar_wait(&tempty[acc], aphase ^ 1);
             ptx::tc_fence_after();
             const uint32_t d = tmem_base + acc * N;
@@ -301,18 +311,23 @@ __global__ void __launch_bounds__(kThreadsR, 1)
         const int off = KMAX - static_cast<int>(p.k);
         uint32_t acc = 0, aphase = 0;
         WorkItem it;
-        for (uint32_t n = 0; next_item(n, unit, units, p.num_tiles, nk, p.split_tail, it); ++n) {
+        for (uint32_t n = 0; next_item(n, unit, units, p.num_tiles, nk, p.splits, it); ++n) {
             ptx::mbar_wait(&tfull[acc], aphase);
             ptx::tc_fence_after();
-            const uint64_t row =
-                static_cast<uint64_t>(it.tile) * Cfg::ROWS_PER_TILE + rank * kBM + row_in_tile;
+            const uint32_t layer = it.tile / p.tiles_per_layer;
+            const uint64_t row = static_cast<uint64_t>(it.tile - layer * p.tiles_per_layer) * Cfg::ROWS_PER_TILE +
+                                 rank * kBM + row_in_tile;  // token within the layer
+            const uint64_t out_row = static_cast<uint64_t>(layer) * p.T + row;
             const uint32_t taddr = tmem_base + acc * N + ((q * 32) << 16);
             if (it.role != 0) {
-                // split-K tail: partial [slot][rank][chunk][row][16] fp32, coalesced rows
-                float *part = p.partial + (static_cast<size_t>(it.slot) * (PAIR ? 2 : 1) + rank) *
-                                              (static_cast<size_t>(N) * kBM);
+                // split-K tail: partial [slot][part-1][rank][chunk][row][16] fp32, coalesced rows
+                constexpr size_t kPartFloats = static_cast<size_t>(N) * kBM;
+                const size_t part_stride = (PAIR ? 2 : 1) * kPartFloats;  // between K parts
+                float *part0 = p.partial + static_cast<size_t>(it.slot) * (p.splits - 1) * part_stride +
+                               rank * kPartFloats;
                 uint32_t *flag = p.flags + it.slot * (PAIR ? 2 : 1) + rank;
                 if (it.role == 2) {
+                    float *part = part0 + (it.part - 1) * part_stride;
 #pragma unroll 1
                     for (int c = half * NH; c < (half + 1) * NH; c += 16) {
                         uint32_t r[16];
@@ -328,32 +343,46 @@ __global__ void __launch_bounds__(kThreadsR, 1)
                     __threadfence();
                     asm volatile("bar.sync 5, 256;" ::: "memory");  // every epilogue thread dumped
                     if (warp == 4 && lane == 0)
-                        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flag), "r"(p.epoch)
-                                     : "memory");
+                        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(flag) : "memory");
                     release_tmem<PAIR>(&tempty[acc], rank, lane);
                     acc ^= 1;
                     if (acc == 0) aphase ^= 1;
                     continue;
                 }
-                // role 1: wait for the other K half, add it into TMEM, then finish
-                uint32_t seen;
-                do {
-                    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(flag) : "memory");
-                } while (seen != p.epoch);
+                // role 1: wait for the other K parts, add them into TMEM (in part
+                // order: a fixed fp32 summation order), then finish. One thread
+                // polls (an acquire load invalidates L1); the named barrier hands
+                // its view to the other epilogue threads, whose partial loads go
+                // to L2 (ld.cg)
+                if (warp == 4 && lane == 0) {
+                    uint32_t seen;
+                    do {
+                        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(flag) : "memory");
+                    } while (seen != p.splits - 1);
+                }
+                asm volatile("bar.sync 5, 256;" ::: "memory");
 #pragma unroll 1
                 for (int c = half * NH; c < (half + 1) * NH; c += 16) {
                     uint32_t r[16];
                     ptx::tmem_ld_32x32b_x16(taddr + c, r);
-                    ptx::tmem_ld_wait();
-                    const float4 *src =
-                        reinterpret_cast<const float4 *>(part + ((c / 16) * kBM + row_in_tile) * 16);
+                    const float4 *src = reinterpret_cast<const float4 *>(
+                        part0 + ((c / 16) * kBM + row_in_tile) * 16);
+                    constexpr uint32_t kMaxParts = 8;
 #pragma unroll
                     for (int i = 0; i < 4; ++i) {
-                        const float4 v = __ldcg(src + i);
-                        r[4 * i] = __float_as_uint(__uint_as_float(r[4 * i]) + v.x);
-                        r[4 * i + 1] = __float_as_uint(__uint_as_float(r[4 * i + 1]) + v.y);
-                        r[4 * i + 2] = __float_as_uint(__uint_as_float(r[4 * i + 2]) + v.z);
-                        r[4 * i + 3] = __float_as_uint(__uint_as_float(r[4 * i + 3]) + v.w);
+                        float4 v[kMaxParts - 1];  // every part's float4 in flight at once
+#pragma unroll
+                        for (uint32_t h = 1; h < kMaxParts; ++h)
+                            if (h < p.splits) v[h - 1] = __ldcg(src + (h - 1) * (part_stride / 4) + i);
+                        if (i == 0) ptx::tmem_ld_wait();
+#pragma unroll
+                        for (uint32_t h = 1; h < kMaxParts; ++h)
+                            if (h < p.splits) {
+                                r[4 * i] = __float_as_uint(__uint_as_float(r[4 * i]) + v[h - 1].x);
+                                r[4 * i + 1] = __float_as_uint(__uint_as_float(r[4 * i + 1]) + v[h - 1].y);
+                                r[4 * i + 2] = __float_as_uint(__uint_as_float(r[4 * i + 2]) + v[h - 1].z);
+                                r[4 * i + 3] = __float_as_uint(__uint_as_float(r[4 * i + 3]) + v[h - 1].w);
+                            }
                     }
                     ptx::tmem_st_32x32b_x16(taddr + c, r);
                 }
@@ -523,8 +552,8 @@ __global__ void __launch_bounds__(kThreadsR, 1)
                     for (int j = 0; j < KMAX; ++j) {
                         if (j < off) continue;
                         const float x = p.renorm ? (wsum > 0.f ? w[j] / wsum : 0.f) : w[j];
-                        p.idx[row * p.k + (j - off)] = ti[j];
-                        p.w[row * p.k + (j - off)] = x;
+                        p.idx[out_row * p.k + (j - off)] = ti[j];
+                        p.w[out_row * p.k + (j - off)] = x;
                     }
                 }
             }
@@ -578,7 +607,8 @@ bool make_map(CUtensorMap *map, const void *ptr, uint64_t rows, uint64_t cols, u
 template <int N, int KMAX, bool PAIR>
 mpb_status launch_router_n(mpb_context *ctx, const CUtensorMap &mx, const CUtensorMap &mw,
                            RouterParams p) {
-    constexpr int smem = RCfg<N, KMAX, PAIR>::SMEM;
+    using Cfg = RCfg<N, KMAX, PAIR>;
+    constexpr int smem = Cfg::SMEM;
     auto kern = k_router<N, KMAX, PAIR>;
     MPB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     cudaLaunchConfig_t cfg{};
@@ -587,25 +617,35 @@ mpb_status launch_router_n(mpb_context *ctx, const CUtensorMap &mx, const CUtens
     cfg.dynamicSmemBytes = smem;
     cfg.stream = ctx->stream;
     uint32_t units;
-    if constexpr (PAIR) {
-        p.num_tiles = static_cast<uint32_t>((p.T + 2 * kBM - 1) / (2 * kBM));
+    p.tiles_per_layer = static_cast<uint32_t>((p.T + Cfg::ROWS_PER_TILE - 1) / Cfg::ROWS_PER_TILE);
+    p.num_tiles = p.tiles_per_layer * p.layers;
+    if constexpr (PAIR)
         units = std::min<uint32_t>(p.num_tiles, static_cast<uint32_t>(ctx->num_sms) / 2);
-    } else {
+    else
         units = std::min<uint32_t>(p.num_tiles, static_cast<uint32_t>(ctx->num_sms));
-    }
     // split-K tail: when the last wave would leave at least half the units idle,
-    // its tiles are split in two K halves over twice as many units
+    // its tiles are split in S K parts over S times as many units (S <= 8, at
+    // least kMinPartK k-steps per part); S = 2 for every multi-wave shape so far
+    // (DSv3, Maverick), up to 8 for small decode batches (a few tiles only)
     const uint32_t full_units = PAIR ? static_cast<uint32_t>(ctx->num_sms) / 2
                                      : static_cast<uint32_t>(ctx->num_sms);
     const uint32_t nk = p.H / kStageK;
     const uint32_t waves = p.num_tiles / full_units;
     const uint32_t rem = p.num_tiles - waves * full_units;
-    p.split_tail = rem > 0 && 2 * rem <= full_units && nk >= 2 && !std::getenv("MPB_ROUTER_NO_SPLIT");
-    if (p.split_tail) {
+    constexpr uint32_t kMaxSplits = 8, kMinPartK = 4;  // kMaxSplits <= the epilogue's kMaxParts
+    uint32_t S = 1;
+    if (rem > 0 && !std::getenv("MPB_ROUTER_NO_SPLIT")) {
+        S = std::min(full_units / rem, kMaxSplits);
+        if (const char *e = std::getenv("MPB_ROUTER_MAX_SPLITS")) S = std::min<uint32_t>(S, std::atoi(e));
+        S = std::min(S, std::max<uint32_t>(nk / kMinPartK, nk >= 2 ? 2u : 1u));
+        if (S < 2 || nk < 2) S = 1;
+    }
+    p.splits = S;
+    if (S > 1) {
         units = full_units;
         const size_t ranks = PAIR ? 2 : 1;
         const size_t flag_bytes = 4096;
-        const size_t need = flag_bytes + size_t(rem) * ranks * N * kBM * sizeof(float);
+        const size_t need = flag_bytes + size_t(rem) * (S - 1) * ranks * N * kBM * sizeof(float);
         if (ctx->router_ws_bytes < need) {
             MPB_CUDA(cudaStreamSynchronize(ctx->stream));
             if (ctx->router_ws) cudaFree(ctx->router_ws);
@@ -615,7 +655,7 @@ mpb_status launch_router_n(mpb_context *ctx, const CUtensorMap &mx, const CUtens
             MPB_CUDA(cudaMemset(ctx->router_ws, 0, flag_bytes));
             ctx->router_ws_bytes = need;
         }
-        p.epoch = 1;  // flags: 0 idle, 1 partial ready (reset by the finisher)
+        // flags: count of K parts > 0 whose partial is ready (reset by the finisher)
         p.flags = static_cast<uint32_t *>(ctx->router_ws);
         p.partial = reinterpret_cast<float *>(static_cast<char *>(ctx->router_ws) + flag_bytes);
     }
@@ -660,40 +700,114 @@ mpb_status launch_router_k(mpb_context *ctx, const CUtensorMap &mx, const CUtens
 
 using namespace mpb;
 
+namespace {
+// shared validation + tile-width choice of the single and grouped entry points
+mpb_status router_check(const char *fn, uint64_t T, uint32_t H, uint32_t E, uint32_t k, int score_fn) {
+    if (E == 0 || E > 256) return fail(MPB_CONFIG_ERROR, std::string(fn) + ": need 1 <= E <= 256");
+    if (H == 0 || H % kStageK != 0)
+        return fail(MPB_CONFIG_ERROR, std::string(fn) + ": H must be a multiple of " + std::to_string(kStageK));
+    if (k == 0 || k > 16 || k > E) return fail(MPB_CONFIG_ERROR, std::string(fn) + ": need 1 <= k <= 16");
+    if (score_fn != MPB_SCORE_SOFTMAX && score_fn != MPB_SCORE_SIGMOID)
+        return fail(MPB_CONFIG_ERROR, std::string(fn) + ": unknown score_fn");
+    if (T > 0x7fffffffull) return fail(MPB_CONFIG_ERROR, std::string(fn) + ": T too large");
+    return MPB_OK;
+}
+
+// E = 256 (tensor-bound): 2-SM CTA pairs (UMMA M=256) by default;
+// MPB_ROUTER_SINGLE=1 forces the single-CTA kernel. E <= 128 is HBM-bound:
+// single-CTA tiles already stream X at the HBM roofline. The tile width N is
+// the next of 64 / 128 / 256: W rows past E come in as TMA out-of-bounds zeros
+// and their columns are masked in the epilogue.
+uint32_t router_tile_n(uint32_t E, bool *pair) {
+    static const bool single = [] {
+        const char *v = std::getenv("MPB_ROUTER_SINGLE");
+        return v && v[0] == '1';
+    }();
+    const uint32_t N = E <= 64 ? 64 : E <= 128 ? 128 : 256;
+    *pair = N == 256 && !single;
+    return N;
+}
+
+mpb_status router_dispatch(mpb_context *ctx, uint32_t N, bool pair, const CUtensorMap &mx,
+                           const CUtensorMap &mw, const RouterParams &p) {
+    if (pair) return launch_router_k<256, true>(ctx, mx, mw, p);
+    if (N == 64) return launch_router_k<64, false>(ctx, mx, mw, p);
+    if (N == 128) return launch_router_k<128, false>(ctx, mx, mw, p);
+    return launch_router_k<256, false>(ctx, mx, mw, p);
+}
+}  // namespace
+
 extern "C" mpb_status mpb_router_topk(mpb_context *ctx, const void *X, const void *W, uint64_t T,
                                       uint32_t H, uint32_t E, uint32_t k, int score_fn, int renorm,
                                       int32_t *idx, float *weights, float *logits_out) {
     if (!ctx || (T && (!X || !W || !idx || !weights)))
         return fail(MPB_VALIDATION_ERROR, "mpb_router_topk: NULL argument");
-    if (E == 0 || E > 256) return fail(MPB_CONFIG_ERROR, "mpb_router_topk: need 1 <= E <= 256");
-    if (H == 0 || H % kStageK != 0)
-        return fail(MPB_CONFIG_ERROR, "mpb_router_topk: H must be a multiple of " +
-                                          std::to_string(kStageK));
-    if (k == 0 || k > 16 || k > E) return fail(MPB_CONFIG_ERROR, "mpb_router_topk: need 1 <= k <= 16");
-    if (score_fn != MPB_SCORE_SOFTMAX && score_fn != MPB_SCORE_SIGMOID)
-        return fail(MPB_CONFIG_ERROR, "mpb_router_topk: unknown score_fn");
+    if (mpb_status st = router_check("mpb_router_topk", T, H, E, k, score_fn)) return st;
     if ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(W)) & 15)
         return fail(MPB_CONFIG_ERROR, "mpb_router_topk: X and W must be 16-byte aligned");
     if (T == 0) return MPB_OK;
-    if (T > 0x7fffffffull) return fail(MPB_CONFIG_ERROR, "mpb_router_topk: T too large");
-    RouterParams p{T, H, k, score_fn, renorm, static_cast<uint32_t>((T + kBM - 1) / kBM),
-                   idx, weights, logits_out, 0, 0, nullptr, nullptr, E};
+    RouterParams p{T, H, k, score_fn, renorm, 0, idx, weights, logits_out, 1, nullptr, nullptr, E,
+                   nullptr, 0, 1};
+    bool pair;
+    const uint32_t N = router_tile_n(E, &pair);
     CUtensorMap mx, mw;
-    // E = 256 (tensor-bound): 2-SM CTA pairs (UMMA M=256) by default;
-    // MPB_ROUTER_SINGLE=1 forces the single-CTA kernel. E <= 128 is HBM-bound:
-    // single-CTA tiles already stream X at the HBM roofline.
-    static const bool single = [] {
-        const char *v = std::getenv("MPB_ROUTER_SINGLE");
-        return v && v[0] == '1';
-    }();
-    // the tile width N is the next of 64 / 128 / 256: W rows past E come in as
-    // TMA out-of-bounds zeros and their columns are masked in the epilogue
-    const uint32_t N = E <= 64 ? 64 : E <= 128 ? 128 : 256;
-    const bool pair = N == 256 && !single;
     if (!make_map(&mx, X, T, H, kBM) || !make_map(&mw, W, E, H, pair ? N / 2 : N))
         return fail(MPB_CUDA_ERROR, "mpb_router_topk: cuTensorMapEncodeTiled failed");
-    if (pair) return launch_router_k<256, true>(ctx, mx, mw, p);
-    if (N == 64) return launch_router_k<64, false>(ctx, mx, mw, p);
-    if (N == 128) return launch_router_k<128, false>(ctx, mx, mw, p);
-    return launch_router_k<256, false>(ctx, mx, mw, p);
+    return router_dispatch(ctx, N, pair, mx, mw, p);
+}
+
+extern "C" mpb_status mpb_router_topk_layers(mpb_context *ctx, uint32_t layers, const void *const *X,
+                                             const void *const *W, uint64_t T, uint32_t H, uint32_t E,
+                                             uint32_t k, int score_fn, int renorm, int32_t *idx,
+                                             float *weights) {
+    if (!ctx || (layers && T && (!X || !W || !idx || !weights)))
+        return fail(MPB_VALIDATION_ERROR, "mpb_router_topk_layers: NULL argument");
+    if (mpb_status st = router_check("mpb_router_topk_layers", T, H, E, k, score_fn)) return st;
+    if (layers == 0 || T == 0) return MPB_OK;
+    if (static_cast<uint64_t>(layers) * ((T + kBM - 1) / kBM) > 0xffffffffull)
+        return fail(MPB_CONFIG_ERROR, "mpb_router_topk_layers: too many tiles");
+    for (uint32_t l = 0; l < layers; ++l) {
+        if (!X[l] || !W[l]) return fail(MPB_VALIDATION_ERROR, "mpb_router_topk_layers: NULL X / W");
+        if ((reinterpret_cast<uintptr_t>(X[l]) | reinterpret_cast<uintptr_t>(W[l])) & 15)
+            return fail(MPB_CONFIG_ERROR, "mpb_router_topk_layers: X and W must be 16-byte aligned");
+    }
+    bool pair;
+    const uint32_t N = router_tile_n(E, &pair);
+    // descriptor table: encoded and uploaded once per (shape, pointers); the
+    // kernel reads the descriptors from global memory
+    std::vector<uint64_t> key{T, H, E, N, pair ? 1u : 0u};
+    for (uint32_t l = 0; l < layers; ++l) {
+        key.push_back(reinterpret_cast<uint64_t>(X[l]));
+        key.push_back(reinterpret_cast<uint64_t>(W[l]));
+    }
+    auto it = ctx->router_maps.find(key);
+    if (it == ctx->router_maps.end()) {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        MPB_CUDA(cudaStreamIsCapturing(ctx->stream, &cs));
+        if (cs != cudaStreamCaptureStatusNone)
+            return fail(MPB_CONFIG_ERROR,
+                        "mpb_router_topk_layers: first call for these buffers inside a stream capture "
+                        "(call once before capturing)");
+        if (ctx->router_maps.size() >= 256) {  // bounded: drop the tables once in-flight work is done
+            MPB_CUDA(cudaStreamSynchronize(ctx->stream));
+            for (auto &kv : ctx->router_maps) cudaFree(kv.second);
+            ctx->router_maps.clear();
+        }
+        std::vector<CUtensorMap> maps(2 * static_cast<size_t>(layers));
+        for (uint32_t l = 0; l < layers; ++l)
+            if (!make_map(&maps[2 * l], X[l], T, H, kBM) || !make_map(&maps[2 * l + 1], W[l], E, H, pair ? N / 2 : N))
+                return fail(MPB_CUDA_ERROR, "mpb_router_topk_layers: cuTensorMapEncodeTiled failed");
+        void *d = nullptr;
+        MPB_CUDA(cudaMalloc(&d, maps.size() * sizeof(CUtensorMap)));
+        const cudaError_t e = cudaMemcpy(d, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) {
+            cudaFree(d);
+            return cuda_fail(e, "mpb_router_topk_layers");
+        }
+        it = ctx->router_maps.emplace(std::move(key), d).first;
+    }
+    RouterParams p{T, H, k, score_fn, renorm, 0, idx, weights, nullptr, 1, nullptr, nullptr, E,
+                   static_cast<const CUtensorMap *>(it->second), 0, layers};
+    CUtensorMap unused{};
+    return router_dispatch(ctx, N, pair, unused, unused, p);
 }

@@ -348,6 +348,28 @@ class Engine:
                   int(renorm), _ptr(idx), _ptr(w), _ptr(logits))
         return (idx, w, logits) if want_logits else (idx, w)
 
+    def router_topk_layers(self, Xs, Ws, k: int, score_fn: int = 0, renorm: bool = False,
+                           out=None):
+        """Router + top-k of several layers (same T, H, E) in one launch
+        (mpb_router_topk_layers). Returns idx [L,T,k] i32 and w [L,T,k] f32."""
+        L = len(Xs)
+        assert len(Ws) == L and L > 0
+        T, H = Xs[0].shape
+        E = Ws[0].shape[0]
+        for X, W in zip(Xs, Ws):
+            assert tuple(X.shape) == (T, H) and tuple(W.shape) == (E, H)
+        if out is None:
+            idx = torch.empty(L, T, k, dtype=torch.int32, device=self.device)
+            w = torch.empty(L, T, k, dtype=torch.float32, device=self.device)
+        else:
+            idx, w = out
+            assert idx.is_contiguous() and w.is_contiguous() and idx.numel() == L * T * k
+        xp = (C.c_void_p * L)(*[X.data_ptr() for X in Xs])
+        wp = (C.c_void_p * L)(*[W.data_ptr() for W in Ws])
+        _abi.call("mpb_router_topk_layers", self.ctx, L, xp, wp, T, H, E, k, score_fn,
+                  int(renorm), _ptr(idx), _ptr(w))
+        return idx, w
+
     # --- layout ---------------------------------------------------------
     def dispatch_layout(self, idx: torch.Tensor, dp: DevicePlacement,
                         src: Optional[torch.Tensor] = None, src_base: int = 0,

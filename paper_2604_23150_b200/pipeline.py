@@ -78,6 +78,25 @@ def _lcg_domains(n: int, domains: int, seed: int) -> np.ndarray:
     return np.random.default_rng(seed).integers(0, domains, n).astype(np.int64)
 
 
+def _taper_chunks(L: int, G: int):
+    """Layer chunks [l0, l1) for grouped router launches: chunks of G layers,
+    tapering to 4, 2, 1 at the end (the last chunk's statistics tails run after
+    the last router, exposed). E.g. L=58, G=8: 3, 8 x 6, 4, 2, 1."""
+    tail, c = [], 1
+    while c < G and sum(tail) + c <= L:
+        tail.insert(0, c)
+        c *= 2
+    rest = L - sum(tail)
+    head = [G] * (rest // G)
+    if rest % G:
+        head.insert(0, rest % G)
+    out, l0 = [], 0
+    for n in head + tail:
+        out.append((l0, l0 + n))
+        l0 += n
+    return out
+
+
 class SyntheticModel:
     """Router weights + domain-planted hidden states for one rank."""
 
@@ -165,7 +184,8 @@ class RoutingPipeline:
         # layer l on a side context with a small SM budget, concurrent with the
         # router of layer l+1 (idx double-buffered)
         self.side = None
-        self.side_mode = int(os.environ.get("MPB_SIDE_STREAM", "3"))
+        # (one layer: nothing to overlap the tail with — co-activation beside the layout)
+        self.side_mode = int(os.environ.get("MPB_SIDE_STREAM", "3" if s.layers > 1 else "1"))
         if self.side_mode == 3:
             # the router chain gets the high-priority stream (made current, so the
             # caller's torch ops and timing events stay ordered with it): when SMs
@@ -184,9 +204,19 @@ class RoutingPipeline:
             # one idx / w buffer per layer (8 MiB each at the DSv3 shape): the
             # router chain never waits on the tails (no write-after-read hazard),
             # so consecutive routers keep their programmatic-launch overlap
-            self.idx_buf = [self.idx] + [torch.empty_like(self.idx) for _ in range(L - 1)]
-            self.w_buf = [self.w] + [torch.empty_like(self.w) for _ in range(L - 1)]
+            # (one [L, T, k] allocation: a chunk of layers is one contiguous slice,
+            # the output of one grouped router launch)
+            self.idx_all = torch.empty(L, T, k, dtype=torch.int32, device=dev)
+            self.w_all = torch.empty(L, T, k, dtype=torch.float32, device=dev)
+            self.idx, self.w = self.idx_all[0], self.w_all[0]
+            self.idx_buf, self.w_buf = list(self.idx_all), list(self.w_all)
             self._rdone = [torch.cuda.Event() for _ in range(L)]
+            # grouped router launches (mpb_router_topk_layers): one persistent launch
+            # per chunk of layers, so the last-tile epilogue and the launch gap are
+            # paid once per chunk instead of once per layer; chunks taper (..., 4,
+            # 2, 1) so the statistics tails left after the last router are short
+            self.router_group = max(1, int(os.environ.get("MPB_ROUTER_GROUP", "8")))
+            self.chunks = _taper_chunks(L, self.router_group)
             self._tdone = torch.cuda.Event()
         elif s.coact and self.side_mode:
             self.side = mp.Engine(eng.device.index, stream=torch.cuda.Stream(eng.device))
@@ -459,8 +489,12 @@ class RoutingPipeline:
         if getattr(self, "graphs", None):
             return self._replay(group)
         self.stats.zero_()
-        for l in range(self.spec.layers):
-            self.layer(l, self.X[l], timed_router)
+        if self.side_mode == 3 and self.router_group > 1 and self.X is not None:
+            for l0, l1 in self.chunks:
+                self._overlapped_chunk(l0, l1, timed_router)
+        else:
+            for l in range(self.spec.layers):
+                self.layer(l, self.X[l], timed_router)
         self.reduce_and_score(group)
 
     def router_ms(self):
@@ -470,6 +504,37 @@ class RoutingPipeline:
             n = ev[2] if len(ev) > 2 else 1
             out += [ev[0].elapsed_time(ev[1]) / n] * n
         return out
+
+    def _overlapped_chunk(self, l0: int, l1: int, timed_router=False):
+        """Routers of layers [l0, l1) in one grouped launch on the main context,
+        then the statistics tails of those layers on the side context, beside
+        the next chunk's router."""
+        s, eng = self.spec, self.eng
+        if l1 - l0 == 1:
+            return self._overlapped_layer(l0, self.X[l0], timed_router)
+        if timed_router:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(eng.stream)
+        eng.router_topk_layers(self.X[l0:l1], self.model.W[l0:l1], s.top_k, s.score_fn, s.renorm,
+                               out=(self.idx_all[l0:l1], self.w_all[l0:l1]))
+        if timed_router:
+            e1.record(eng.stream)
+            self.router_events.append((e0, e1, l1 - l0))
+        self._rdone[l0].record(eng.stream)
+        self.side.stream.wait_event(self._rdone[l0])
+        for l in range(l0, l1):
+            self._side_tail(l)
+
+    def _side_tail(self, l: int):
+        s, side = self.spec, self.side
+        idx = self.idx_buf[l]
+        side.dispatch_layout(idx, self.dp_deployed, src=self.src_cl, tag=self.dom_tok,
+                             n_tags=s.domains, demand=self.dem_cl[l], tag_pop=self.pop,
+                             perm_out=(self.sp, self.pp, self.ko), src2=self.src_rr,
+                             demand2=self.dem_rr[l])
+        if s.coact:
+            side.coactivation(idx, s.experts, out=self.coact)
 
     def _overlapped_layer(self, l: int, X: torch.Tensor, timed_router=False):
         """Router of layer l on the main context (most SMs, high-priority
@@ -489,12 +554,7 @@ class RoutingPipeline:
             self.router_events.append((e0, e1))
         self._rdone[l].record(eng.stream)
         side.stream.wait_event(self._rdone[l])
-        side.dispatch_layout(idx, self.dp_deployed, src=self.src_cl, tag=self.dom_tok,
-                             n_tags=s.domains, demand=self.dem_cl[l], tag_pop=self.pop,
-                             perm_out=(self.sp, self.pp, self.ko), src2=self.src_rr,
-                             demand2=self.dem_rr[l])
-        if s.coact:
-            side.coactivation(idx, s.experts, out=self.coact)
+        self._side_tail(l)
 
     # ---------------------------------------------------------------- CUDA graphs
     def capture(self, group=None) -> bool:

@@ -18,8 +18,12 @@ SPEC = WorkloadSpec("tiny", 4, 8192, 512, 64, 8, 1, True, groups=8, nodes=2, dom
                     preferred=8, candidates=64)
 
 
-def _run(mode, monkeypatch):
+def _run(mode, monkeypatch, group=8):
     monkeypatch.setenv("MPB_SIDE_STREAM", str(mode))
+    monkeypatch.setenv("MPB_ROUTER_GROUP", str(group))
+    # no split-K tail: every router tile then sums its K range in one order, so
+    # the routing is bit-identical whatever the SM budget or layer grouping
+    monkeypatch.setenv("MPB_ROUTER_NO_SPLIT", "1")
     # a 4-SM side context: its layout and co-activation CTAs loop over many
     # chunks (pipeline stages recycled), as the 20-SM side context does at the
     # DSv3 shape
@@ -35,11 +39,13 @@ def _run(mode, monkeypatch):
     return pipe, idx
 
 
-def test_overlapped_schedule_matches_serial(monkeypatch, oracle):
+@pytest.mark.parametrize("group", [1, 2, 8])
+def test_overlapped_schedule_matches_serial(monkeypatch, oracle, group):
+    """group = layers per grouped router launch (1: one launch per layer)."""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     p1, _ = _run(1, monkeypatch)
-    p3, idx3 = _run(3, monkeypatch)
+    p3, idx3 = _run(3, monkeypatch, group)
     assert torch.equal(p1.stats, p3.stats)
     assert torch.equal(p1.fin_cl[0], p3.fin_cl[0]) and torch.equal(p1.fin_rr[0], p3.fin_rr[0])
     assert p1.results() == p3.results()

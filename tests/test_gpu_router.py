@@ -124,3 +124,63 @@ def test_sm_budget_changes_nothing_but_the_grid(eng):
         ti, tw = e.topk_logits(logits, k, 1, True)
         assert torch.equal(ti, idx) and torch.equal(tw, w), sms
         assert torch.equal(c, ref_c), sms
+
+
+@pytest.mark.parametrize("shape", [(4096, 4096, 128, 8, 0, False), (1024, 7168, 256, 8, 1, True),
+                                   (300, 1088, 64, 4, 0, True)])
+def test_router_split_k_parts(eng, oracle, shape, monkeypatch):
+    """Small decode batches (fewer tiles than SMs) split every tile's K range
+    over up to 8 units (router.cu next_item / launch_router_n). Whatever the
+    number of parts (uneven ones included: 1088 / 64 = 17 k-steps), the logits
+    stay within the fp32 accumulation-order bound of the float64 reference and
+    the top-k is the oracle's on the same logits; the partial flags reset
+    themselves, so back-to-back launches with different splits stay correct."""
+    T, H, E, k, fn, renorm = shape
+    g = torch.Generator(device="cuda").manual_seed(T * 7 + H)
+    X = torch.randn(T, H, device="cuda", generator=g).to(torch.bfloat16)
+    W = (torch.randn(E, H, device="cuda", generator=g) / H ** 0.5).to(torch.bfloat16)
+    ref = X.double() @ W.double().t()
+    tol = 1e-4 * H ** 0.5 * float(X.float().pow(2).mean().sqrt()) * \
+        float(W.float().pow(2).mean().sqrt()) + 1e-5
+    for cap in ("1", "2", "3", "8", "8", "2"):
+        monkeypatch.setenv("MPB_ROUTER_MAX_SPLITS", cap)
+        idx, w, logits = eng.router_topk(X, W, k, fn, renorm, want_logits=True)
+        torch.cuda.synchronize()
+        assert (logits.double() - ref).abs().max().item() <= tol, cap
+        ri, rw = oracle.topk_logits(logits.cpu().numpy(), k, fn, renorm)
+        np.testing.assert_array_equal(idx.cpu().numpy(), ri)
+        np.testing.assert_allclose(w.cpu().numpy(), rw, rtol=2e-6, atol=1e-7)
+
+
+@pytest.mark.parametrize("shape", [(3, 5000, 1024, 256, 8, 1, True), (4, 4096, 4096, 128, 8, 0, False),
+                                   (2, 300, 512, 64, 4, 0, True), (5, 65536, 7168, 256, 8, 1, True)])
+def test_router_topk_layers_matches_per_layer(eng, shape, monkeypatch):
+    """One grouped launch over L layers (mpb_router_topk_layers) == L single
+    launches. Without the split-K tail every tile accumulates its K range in
+    the same order in both, so idx / w are bit-identical; with it, only the
+    last wave's tiles differ in fp32 summation order (near-tie flips only)."""
+    L, T, H, E, k, fn, renorm = shape
+    g = torch.Generator(device="cuda").manual_seed(L * T + H)
+    Xs = [torch.randn(T, H, device="cuda", generator=g).to(torch.bfloat16) for _ in range(L)]
+    Ws = [(torch.randn(E, H, device="cuda", generator=g) / H ** 0.5).to(torch.bfloat16)
+          for _ in range(L)]
+    monkeypatch.setenv("MPB_ROUTER_NO_SPLIT", "1")
+    ref = [eng.router_topk(X, W, k, fn, renorm) for X, W in zip(Xs, Ws)]
+    idx, w = eng.router_topk_layers(Xs, Ws, k, fn, renorm)
+    torch.cuda.synchronize()
+    for l in range(L):
+        assert torch.equal(idx[l], ref[l][0]), l
+        assert torch.equal(w[l], ref[l][1]), l
+    monkeypatch.delenv("MPB_ROUTER_NO_SPLIT")
+    idx2, w2 = eng.router_topk_layers(Xs, Ws, k, fn, renorm)
+    ref2 = [eng.router_topk(X, W, k, fn, renorm) for X, W in zip(Xs, Ws)]
+    torch.cuda.synchronize()
+    for l in range(L):
+        same = (idx2[l] == ref2[l][0]).all(1)
+        assert same.float().mean().item() >= 0.999, l
+        # weights follow logits that differ by fp32 summation order (|dlogit| ~
+        # 1e-5 at H = 4096): relative weight error of the same order
+        torch.testing.assert_close(w2[l][same], ref2[l][1][same], rtol=2e-4, atol=1e-6)
+    # the descriptor table is cached: a second call with the same buffers reuses it
+    idx3, w3 = eng.router_topk_layers(Xs, Ws, k, fn, renorm)
+    assert torch.equal(idx3, idx2) and torch.equal(w3, w2)

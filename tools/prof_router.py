@@ -18,6 +18,9 @@ ap.add_argument("--iters", type=int, default=5)
 ap.add_argument("--sms", type=int, default=0, help="SM budget (0 = all)")
 ap.add_argument("--nx", type=int, default=1, help="distinct X / W buffers rotated per launch")
 ap.add_argument("--events", action="store_true", help="an event pair around every launch")
+ap.add_argument("--sleep", type=float, default=0.0,
+                help="ms of device sleep queued before the timed launches, so small-T launches are "
+                     "timed on the GPU rather than at the host's launch rate")
 a = ap.parse_args()
 eng = mp.Engine(0)
 if a.sms:
@@ -31,6 +34,9 @@ for _ in range(2):
     eng.router_topk(X, W, a.k, a.fn, True, out=out)
 torch.cuda.synchronize()
 s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+cycles = int(a.sleep * 1e-3 * torch.cuda.get_device_properties(0).clock_rate * 1e3)
+if cycles:
+    torch.cuda._sleep(cycles)
 s.record()
 pairs = []
 for i in range(a.iters):
@@ -54,6 +60,8 @@ C = torch.empty(a.T, a.E, device="cuda", dtype=torch.bfloat16)
 for _ in range(2):
     torch.matmul(X, W.t(), out=C)
 torch.cuda.synchronize()
+if cycles:
+    torch.cuda._sleep(cycles)
 s.record()
 for _ in range(a.iters):
     torch.matmul(X, W.t(), out=C)

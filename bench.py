@@ -384,6 +384,7 @@ def run_gpu_arm(args, spec):
                            "ep_groups": spec.groups, "nodes": spec.nodes,
                            "domains": spec.domains, "candidates": spec.candidates,
                            "parallelism": f"dp{world} (token shards) + NCCL stats all-reduce",
+                           "schedule": pipe.schedule(),
                            "l2": "inputs larger than L2 (each layer's X is "
                                  f"{spec.tokens * spec.hidden * 2 / 2**20:.0f} MiB)"},
                 "a2a_bytes_saved_pct": res["a2a_bytes_saved_pct"],

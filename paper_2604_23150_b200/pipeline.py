@@ -497,6 +497,14 @@ class RoutingPipeline:
                 self.layer(l, self.X[l], timed_router)
         self.reduce_and_score(group)
 
+    def schedule(self) -> dict:
+        """How one step launches its routers (reported in the bench line)."""
+        grouped = self.side_mode == 3 and self.router_group > 1 and self.X is not None
+        chunks = [l1 - l0 for l0, l1 in self.chunks] if grouped else [1] * self.spec.layers
+        return {"side_stream_mode": self.side_mode,
+                "side_sms": getattr(self, "side_sms", 0),
+                "router_launches_per_step": len(chunks), "layers_per_router_launch": chunks}
+
     def router_ms(self):
         """Per-launch router times (ms) recorded by timed steps."""
         out = []

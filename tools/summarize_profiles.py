@@ -63,17 +63,26 @@ start = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
 hdr = rows[start]
 ki, vi = hdr.index("Kernel Name"), hdr.index("Metric Value")
 seq = [(r[ki], num(r[vi])) for r in rows[start + 1:] if len(r) > vi]
-# the last step's launches: from the last k_router of the second-to-last step onwards
+# the last step's launches: from its first k_router launch onwards (grouped
+# router launches: several layers per launch, config.schedule)
 router_idx = [i for i, (k, _) in enumerate(seq) if "k_router" in k]
 L = bench["config"]["layers"]
-step = seq[router_idx[-L]:]
+sched = bench["config"].get("schedule")
+if sched:
+    n_router = sched["router_launches_per_step"]
+else:
+    sys.path.insert(0, str(ROOT))
+    from paper_2604_23150_b200.pipeline import _taper_chunks  # noqa: E402
+    n_router = len(_taper_chunks(L, 8))
+step = seq[router_idx[-n_router]:]
 agg = collections.defaultdict(lambda: [0, 0.0])
 for k, v in step:
     name = k.split("(")[0].replace("void ", "").strip()
     agg[name][0] += 1
     agg[name][1] += v
 tot = sum(v for _, v in agg.values())
-lines = [f"# {RND}: per-kernel share of one DSv3 step (ncu gpu__time_duration, cold/serialised)",
+lines = [f"# {RND}: per-kernel share of one DSv3 step (ncu gpu__time_duration, cold/serialised; "
+         f"{n_router} grouped router launches for {L} layers)",
          "", f"command: `python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline`", "",
          "| kernel | launches | total us | share |", "|---|---|---|---|"]
 for name, (n, v) in sorted(agg.items(), key=lambda x: -x[1][1]):

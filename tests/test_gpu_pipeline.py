@@ -57,3 +57,27 @@ def test_overlapped_schedule_matches_serial(monkeypatch, oracle, group):
         ref = oracle.dispatch_layout(idx.cpu().numpy(), p3.h_src_cl.astype(np.uint32), lut,
                                      SPEC.groups, SPEC.experts, top.group_to_node)
         np.testing.assert_array_equal(p3.dem_cl[l].cpu().numpy(), ref["demand"])
+
+
+def test_graph_replay_matches_eager(monkeypatch):
+    """Single-layer workloads replay the step from CUDA graphs by default
+    (bench.py): the replayed step's statistics and LayerSims equal the eager
+    step's, and the replay still launches this library's kernels."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    monkeypatch.delenv("MPB_SIDE_STREAM", raising=False)
+    spec = WorkloadSpec("tiny1", 1, 4096, 512, 128, 8, 0, True, groups=8, nodes=2, domains=8,
+                        preferred=16, candidates=64)
+    eng = mp.Engine(0)
+    pipe = RoutingPipeline(spec, eng, 0, 1, resident=True)
+    assert pipe.side_mode == 1  # one layer: co-activation beside the layout
+    pipe.step()
+    torch.cuda.synchronize()
+    stats, fin_cl, fin_rr = pipe.stats.clone(), pipe.fin_cl[0].clone(), pipe.fin_rr[0].clone()
+    assert pipe.capture()
+    for _ in range(2):
+        pipe.step()
+    torch.cuda.synchronize()
+    assert pipe.launches_per_step > 0
+    assert torch.equal(pipe.stats, stats)
+    assert torch.equal(pipe.fin_cl[0], fin_cl) and torch.equal(pipe.fin_rr[0], fin_rr)

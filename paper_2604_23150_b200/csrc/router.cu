@@ -367,7 +367,7 @@ __global__ void __launch_bounds__(kThreadsR, 1)
                     ptx::tmem_ld_32x32b_x16(taddr + c, r);
                     const float4 *src = reinterpret_cast<const float4 *>(
                         part0 + ((c / 16) * kBM + row_in_tile) * 16);
-                    constexpr uint32_t kMaxParts = 8;
+                    constexpr uint32_t kMaxParts = 4;
 #pragma unroll
                     for (int i = 0; i < 4; ++i) {
                         float4 v[kMaxParts - 1];  // every part's float4 in flight at once
@@ -624,15 +624,15 @@ mpb_status launch_router_n(mpb_context *ctx, const CUtensorMap &mx, const CUtens
     else
         units = std::min<uint32_t>(p.num_tiles, static_cast<uint32_t>(ctx->num_sms));
     // split-K tail: when the last wave would leave at least half the units idle,
-    // its tiles are split in S K parts over S times as many units (S <= 8, at
+    // its tiles are split in S K parts over S times as many units (S <= 4, at
     // least kMinPartK k-steps per part); S = 2 for every multi-wave shape so far
-    // (DSv3, Maverick), up to 8 for small decode batches (a few tiles only)
+    // (DSv3, Maverick), up to 4 for small decode batches (a few tiles only)
     const uint32_t full_units = PAIR ? static_cast<uint32_t>(ctx->num_sms) / 2
                                      : static_cast<uint32_t>(ctx->num_sms);
     const uint32_t nk = p.H / kStageK;
     const uint32_t waves = p.num_tiles / full_units;
     const uint32_t rem = p.num_tiles - waves * full_units;
-    constexpr uint32_t kMaxSplits = 8, kMinPartK = 4;  // kMaxSplits <= the epilogue's kMaxParts
+    constexpr uint32_t kMaxSplits = 4, kMinPartK = 4;  // 8 measured slower at T=1024 (fix-up); <= the epilogue's kMaxParts
     uint32_t S = 1;
     if (rem > 0 && !std::getenv("MPB_ROUTER_NO_SPLIT")) {
         S = std::min(full_units / rem, kMaxSplits);

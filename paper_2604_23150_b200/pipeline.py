@@ -221,6 +221,7 @@ class RoutingPipeline:
         elif s.coact and self.side_mode:
             self.side = mp.Engine(eng.device.index, stream=torch.cuda.Stream(eng.device))
             self._fork, self._join = torch.cuda.Event(), torch.cuda.Event()
+        self._sfork, self._sjoin = torch.cuda.Event(), torch.cuda.Event()
         # ---- calibration -> learned placement, routes, candidates
         self.calib = self._calibrate(progress)
         self._build_candidates()
@@ -464,11 +465,20 @@ class RoutingPipeline:
         prices its P/world slice; `_gather_scores` all-gathers the rows)."""
         s, eng = self.spec, self.eng
         L, D, E = s.layers, s.groups, s.experts
-        eng.score_placements(self.dem_rr, self.luts_rr, self.g2n, D, row_node=self.g2n,
-                             out=self.sc_rr)
+        # the two baselines are priced on the side stream (when there is one)
+        # beside the candidates on the main one: independent launches, each too
+        # small to fill the GPU
+        rr = self.side if self.side is not None else eng
+        if rr is not eng:
+            self._sfork.record(eng.stream)
+            rr.stream.wait_event(self._sfork)
+        rr.score_placements(self.dem_rr, self.luts_rr, self.g2n, D, row_node=self.g2n,
+                            out=self.sc_rr)
         inter, intra, rank = self.sc_rr
-        eng.finalize(inter.view(-1), intra.view(-1), rank.view(-1, D), D, self.cost,
-                     self.topology, out=self.fin_rr[0], payload=self.fin_rr[1])
+        rr.finalize(inter.view(-1), intra.view(-1), rank.view(-1, D), D, self.cost,
+                    self.topology, out=self.fin_rr[0], payload=self.fin_rr[1])
+        if rr is not eng:
+            self._sjoin.record(rr.stream)
         lo, hi = self.shard if self.shard is not None else (0, self.luts_cl.shape[0])
         inter, intra, rank = (t[lo:hi] for t in self.sc_cl)
         eng.score_placements(self.dem_cl, self.luts_cl[lo:hi], self.g2n, D, row_node=self.g2n,
@@ -476,6 +486,8 @@ class RoutingPipeline:
         eng.finalize(inter.reshape(-1), intra.reshape(-1), rank.reshape(-1, D), D, self.cost,
                      self.topology, out=self.fin_cl[0][lo * L:hi * L],
                      payload=self.fin_cl[1][lo * L:hi * L])
+        if rr is not eng:
+            eng.stream.wait_event(self._sjoin)
 
     def _gather_scores(self, group=None):
         if self.shard is None:

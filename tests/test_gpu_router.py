@@ -130,7 +130,7 @@ def test_sm_budget_changes_nothing_but_the_grid(eng):
                                    (300, 1088, 64, 4, 0, True)])
 def test_router_split_k_parts(eng, oracle, shape, monkeypatch):
     """Small decode batches (fewer tiles than SMs) split every tile's K range
-    over up to 8 units (router.cu next_item / launch_router_n). Whatever the
+    over up to 4 units (router.cu next_item / launch_router_n). Whatever the
     number of parts (uneven ones included: 1088 / 64 = 17 k-steps), the logits
     stay within the fp32 accumulation-order bound of the float64 reference and
     the top-k is the oracle's on the same logits; the partial flags reset

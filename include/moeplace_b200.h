@@ -74,6 +74,19 @@ MPB_API mpb_status mpb_context_set_stream(mpb_context *ctx, void *stream);
  * contexts with disjoint budgets run their kernels concurrently (e.g. the
  * router of layer l+1 beside the statistics of layer l). */
 MPB_API mpb_status mpb_context_set_sm_budget(mpb_context *ctx, uint32_t sms);
+/* Like mpb_context_set_sm_budget, for a context whose stream belongs to an SM
+ * partition (mpb_sm_partition_create): the hardware confines its kernels to
+ * `sms` SMs, so early-launched (programmatic) CTAs cannot land elsewhere. */
+MPB_API mpb_status mpb_context_set_sm_partition(mpb_context *ctx, uint32_t sms);
+/* Splits the device's SMs into two green-context partitions, side >= side_sms
+ * SMs (the hardware rounds up to its granularity, 8 on B200) and main = the
+ * rest, and returns one stream (cudaStream_t) on each; kernels launched into a
+ * stream run only on its partition's SMs. Reports the actual SM counts. */
+MPB_API mpb_status mpb_sm_partition_create(int device, uint32_t side_sms, int main_priority,
+                                           int side_priority, void **main_stream,
+                                           void **side_stream, uint32_t *main_sms,
+                                           uint32_t *side_sms_out);
+MPB_API mpb_status mpb_sm_partition_destroy(void *main_stream);
 /* Synchronises the stream and reports input errors the kernels flagged
  * (uncovered expert, id >= E, source group >= D -> MPB_VALIDATION_ERROR,
  * exactly where simulate_layer throws, simulator.cpp:66-71). Clears the flag. */

@@ -36,6 +36,9 @@ _SIGS = {
     "mpb_context_destroy": (C.c_int, [_p]),
     "mpb_context_set_stream": (C.c_int, [_p, _p]),
     "mpb_context_set_sm_budget": (C.c_int, [_p, C.c_uint32]),
+    "mpb_context_set_sm_partition": (C.c_int, [_p, C.c_uint32]),
+    "mpb_sm_partition_create": (C.c_int, [C.c_int, C.c_uint32, C.c_int, C.c_int, _p, _p, _p, _p]),
+    "mpb_sm_partition_destroy": (C.c_int, [_p]),
     "mpb_context_sync": (C.c_int, [_p]),
     "mpb_context_launch_count": (C.c_uint64, [_p]),
     "mpb_placement_create": (C.c_int, [_p, _u32p, _u32p, C.c_uint32, C.c_uint32, _u32p,

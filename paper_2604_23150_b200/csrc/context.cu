@@ -112,6 +112,7 @@ uint64_t mpb_context_launch_count(const mpb_context *ctx) { return ctx ? ctx->la
 
 mpb_status mpb_context_set_sm_budget(mpb_context *ctx, uint32_t sms) {
     if (!ctx) return fail(MPB_VALIDATION_ERROR, "mpb_context_set_sm_budget: NULL context");
+    ctx->confined = false;
     ctx->num_sms = sms == 0 ? ctx->device_sms
                             : static_cast<int>(std::min<uint32_t>(sms, ctx->device_sms));
     if (ctx->num_sms < 2) ctx->num_sms = 2;  // a router CTA pair

@@ -77,6 +77,10 @@ struct mpb_context {
     cudaStream_t stream = nullptr;
     int num_sms = 148;      // SM budget grids are sized for (<= device_sms)
     int device_sms = 148;
+    // the stream's kernels are confined to num_sms SMs by the hardware (a
+    // green-context partition): early (programmatic) launches cannot land on
+    // SMs another context uses, so the router keeps PDL
+    bool confined = false;
     uint32_t *d_error = nullptr;
     uint64_t launches = 0;
     // grow-only scratch (permutation block histograms, co-activation partials)

@@ -675,7 +675,7 @@ mpb_status launch_router_n(mpb_context *ctx, const CUtensorMap &mx, const CUtens
     // PDL only when this context owns the whole GPU: an early-launched CTA may
     // land on (and spin on) an SM outside the context's budget, starving the
     // kernels that another context runs there
-    if (pdl_enabled() && ctx->num_sms == ctx->device_sms) {
+    if (pdl_enabled() && (ctx->num_sms == ctx->device_sms || ctx->confined)) {
         attr[cfg.numAttrs].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         attr[cfg.numAttrs].val.programmaticStreamSerializationAllowed = 1;
         ++cfg.numAttrs;

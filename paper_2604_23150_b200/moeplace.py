@@ -284,6 +284,31 @@ def host_dest_lut(placement: Placement, group_to_node) -> np.ndarray:
     return out.reshape(nodes, E)
 
 
+class SmPartition:
+    """Two green-context SM partitions of one device (mpb_sm_partition_create):
+    `main` / `side` are torch streams whose kernels the hardware confines to
+    `main_sms` / `side_sms` SMs (side rounded up to the partition granularity).
+    Lives until the object is collected."""
+
+    def __init__(self, device: int, side_sms: int, main_priority: int = 0, side_priority: int = 0):
+        ms, ss = C.c_void_p(), C.c_void_p()
+        mn, sn = C.c_uint32(), C.c_uint32()
+        _abi.call("mpb_sm_partition_create", int(device), int(side_sms), int(main_priority),
+                  int(side_priority), C.byref(ms), C.byref(ss), C.byref(mn), C.byref(sn))
+        self._handle = ms.value
+        dev = torch.device("cuda", device)
+        self.main = torch.cuda.ExternalStream(ms.value, device=dev)
+        self.side = torch.cuda.ExternalStream(ss.value, device=dev)
+        self.main_sms, self.side_sms = int(mn.value), int(sn.value)
+
+    def __del__(self):
+        try:
+            if self._handle:
+                _abi.lib().mpb_sm_partition_destroy(C.c_void_p(self._handle))
+        except Exception:
+            pass
+
+
 class Engine:
     """One mpb_context bound to a CUDA device and (torch) stream."""
 
@@ -309,6 +334,11 @@ class Engine:
     def set_sm_budget(self, sms: int) -> None:
         """Size this context's grids for `sms` SMs (0 = all of them)."""
         _abi.call("mpb_context_set_sm_budget", self.ctx, int(sms))
+
+    def set_sm_partition(self, sms: int) -> None:
+        """This context's stream belongs to an SM partition of `sms` SMs
+        (SmPartition): grids sized for it, programmatic launches kept."""
+        _abi.call("mpb_context_set_sm_partition", self.ctx, int(sms))
 
     def sync(self) -> None:
         """Synchronise and raise ValidationError for inputs kernels flagged."""

@@ -191,16 +191,39 @@ class RoutingPipeline:
             # caller's torch ops and timing events stay ordered with it): when SMs
             # free up, the block scheduler serves its CTAs before the tail's
             lo_prio, hi_prio = torch.cuda.Stream.priority_range()
-            main = torch.cuda.Stream(eng.device, priority=hi_prio)
+            want_side = int(os.environ.get("MPB_SIDE_SMS", "20"))
+            # SM partition (green contexts, MPB_SM_PARTITION=1): the hardware
+            # keeps the tails' CTAs off the router's SMs (a grid budget alone only
+            # sizes the grids). Measured at the DSv3 shape: the router gets ~3%
+            # faster per layer in a 132-SM partition, but the tails confined to 16
+            # SMs fall behind (~1 ms exposed after the last router) — off by
+            # default, the budgeted tails borrow router SMs when they need them
+            self.partition = None
+            if os.environ.get("MPB_SM_PARTITION", "0") != "0":
+                try:
+                    self.partition = mp.SmPartition(eng.device.index, want_side, hi_prio, lo_prio)
+                except Exception:
+                    self.partition = None
+            if self.partition is not None:
+                main, side_stream = self.partition.main, self.partition.side
+            else:
+                main = torch.cuda.Stream(eng.device, priority=hi_prio)
+                side_stream = torch.cuda.Stream(eng.device, priority=lo_prio)
             main.wait_stream(torch.cuda.current_stream(eng.device))
             torch.cuda.set_stream(main)
             eng.set_stream(main)
-            self.side = mp.Engine(eng.device.index,
-                                  stream=torch.cuda.Stream(eng.device, priority=lo_prio))
-            n_sm = torch.cuda.get_device_properties(eng.device).multi_processor_count
-            self.side_sms = int(os.environ.get("MPB_SIDE_SMS", "20"))
-            self.side.set_sm_budget(self.side_sms)
-            eng.set_sm_budget(n_sm - self.side_sms)
+            self.side = mp.Engine(eng.device.index, stream=side_stream)
+            if self.partition is not None:
+                self.side_sms = self.partition.side_sms
+                self.side.set_sm_partition(self.side_sms)
+                eng.set_sm_partition(self.partition.main_sms)
+                # the partition's streams must outlive every context bound to them
+                eng._partition = self.side._partition = self.partition
+            else:
+                n_sm = torch.cuda.get_device_properties(eng.device).multi_processor_count
+                self.side_sms = want_side
+                self.side.set_sm_budget(self.side_sms)
+                eng.set_sm_budget(n_sm - self.side_sms)
             # one idx / w buffer per layer (8 MiB each at the DSv3 shape): the
             # router chain never waits on the tails (no write-after-read hazard),
             # so consecutive routers keep their programmatic-launch overlap
@@ -515,6 +538,7 @@ class RoutingPipeline:
         chunks = [l1 - l0 for l0, l1 in self.chunks] if grouped else [1] * self.spec.layers
         return {"side_stream_mode": self.side_mode,
                 "side_sms": getattr(self, "side_sms", 0),
+                "sm_partition": getattr(self, "partition", None) is not None,
                 "router_launches_per_step": len(chunks), "layers_per_router_launch": chunks}
 
     def router_ms(self):

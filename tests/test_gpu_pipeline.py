@@ -81,3 +81,21 @@ def test_graph_replay_matches_eager(monkeypatch):
     assert pipe.launches_per_step > 0
     assert torch.equal(pipe.stats, stats)
     assert torch.equal(pipe.fin_cl[0], fin_cl) and torch.equal(pipe.fin_rr[0], fin_rr)
+
+
+def test_sm_partition_confines_kernels(monkeypatch):
+    """mpb_sm_partition_create: two green-context streams on disjoint SM sets;
+    the library's kernels run on them (here the overlapped schedule with the
+    partition switched on reproduces the budgeted schedule's statistics)."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    part = mp.SmPartition(0, 16)
+    n_sm = torch.cuda.get_device_properties(0).multi_processor_count
+    assert part.side_sms >= 16 and part.main_sms + part.side_sms == n_sm
+    del part
+    p_budget, _ = _run(3, monkeypatch)
+    monkeypatch.setenv("MPB_SM_PARTITION", "1")
+    p_part, _ = _run(3, monkeypatch)
+    assert p_part.partition is not None
+    assert torch.equal(p_budget.stats, p_part.stats)
+    assert p_budget.results() == p_part.results()

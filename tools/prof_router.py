@@ -18,6 +18,9 @@ ap.add_argument("--iters", type=int, default=5)
 ap.add_argument("--sms", type=int, default=0, help="SM budget (0 = all)")
 ap.add_argument("--nx", type=int, default=1, help="distinct X / W buffers rotated per launch")
 ap.add_argument("--events", action="store_true", help="an event pair around every launch")
+ap.add_argument("--layers", type=int, default=0,
+                help="time one grouped launch over this many layers (mpb_router_topk_layers); "
+                     "reported per layer")
 ap.add_argument("--sleep", type=float, default=0.0,
                 help="ms of device sleep queued before the timed launches, so small-T launches are "
                      "timed on the GPU rather than at the host's launch rate")
@@ -28,6 +31,23 @@ if a.sms:
 Xs = [torch.randn(a.T, a.H, device="cuda").to(torch.bfloat16) for _ in range(a.nx)]
 Ws = [(torch.randn(a.E, a.H, device="cuda") / a.H ** 0.5).to(torch.bfloat16) for _ in range(a.nx)]
 X, W = Xs[0], Ws[0]
+if a.layers:
+    LX = [X] * a.layers if a.nx == 1 else [Xs[i % a.nx] for i in range(a.layers)]
+    LW = [W] * a.layers if a.nx == 1 else [Ws[i % a.nx] for i in range(a.layers)]
+    lout = (torch.empty(a.layers, a.T, a.k, dtype=torch.int32, device="cuda"),
+            torch.empty(a.layers, a.T, a.k, dtype=torch.float32, device="cuda"))
+    for _ in range(2):
+        eng.router_topk_layers(LX, LW, a.k, a.fn, True, out=lout)
+    torch.cuda.synchronize()
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s0.record()
+    for _ in range(a.iters):
+        eng.router_topk_layers(LX, LW, a.k, a.fn, True, out=lout)
+    s1.record()
+    torch.cuda.synchronize()
+    ms = s0.elapsed_time(s1) / a.iters / a.layers
+    print(f"grouped router x{a.layers} T={a.T} H={a.H} E={a.E} k={a.k}: {ms:.4f} ms/layer  "
+          f"{2 * a.T * a.H * a.E / ms / 1e9:.1f} TFLOP/s  {(a.T * a.H * 2) / ms / 1e6:.0f} GB/s(X)")
 out = (torch.empty(a.T, a.k, dtype=torch.int32, device="cuda"),
        torch.empty(a.T, a.k, dtype=torch.float32, device="cuda"))
 for _ in range(2):

@@ -9,7 +9,18 @@ import torch  # noqa: E402
 from paper_2604_23150_b200 import moeplace as mp  # noqa: E402
 
 T, E, k, D, L, P = 65536, 256, 8, 8, 58, 1022
-eng = mp.Engine(0)
+SMS = int(sys.argv[1]) if len(sys.argv) > 1 else 0  # SM budget (the side context's, e.g. 20)
+CONFINE = len(sys.argv) > 2 and sys.argv[2] == "confined"  # run inside an SM partition
+if CONFINE:
+    part = mp.SmPartition(0, SMS)
+    torch.cuda.set_stream(part.side)
+    eng = mp.Engine(0, stream=part.side)
+    eng.set_sm_partition(part.side_sms)
+    print(f"confined to a {part.side_sms}-SM partition")
+else:
+    eng = mp.Engine(0)
+    if SMS:
+        eng.set_sm_budget(SMS)
 rng = np.random.default_rng(0)
 idx = torch.from_numpy(np.argsort(rng.random((T, E), dtype=np.float32), axis=1)[:, :k]
                        .astype(np.int32)).cuda()

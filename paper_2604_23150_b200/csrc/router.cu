@@ -320,7 +320,8 @@ __global__ void __launch_bounds__(kThreadsR, 1)
             const uint64_t out_row = static_cast<uint64_t>(layer) * p.T + row;
             const uint32_t taddr = tmem_base + acc * N + ((q * 32) << 16);
             if (it.role != 0) {
-                // split-K tail: partial [slot][part-1][rank][chunk][row][16] fp32, coalesced rows
+                // split-K tail: partial [slot][part-1][rank][chunk][quarter][row] float4 — a
+                // warp's 16-byte accesses to one (chunk, quarter) cover 512 contiguous bytes
                 constexpr size_t kPartFloats = static_cast<size_t>(N) * kBM;
                 const size_t part_stride = (PAIR ? 2 : 1) * kPartFloats;  // between K parts
                 float *part0 = p.partial + static_cast<size_t>(it.slot) * (p.splits - 1) * part_stride +
@@ -333,10 +334,10 @@ __global__ void __launch_bounds__(kThreadsR, 1)
                         uint32_t r[16];
                         ptx::tmem_ld_32x32b_x16(taddr + c, r);
                         ptx::tmem_ld_wait();
-                        float4 *dst = reinterpret_cast<float4 *>(part + ((c / 16) * kBM + row_in_tile) * 16);
+                        float4 *dst = reinterpret_cast<float4 *>(part) + (c / 16) * 4 * kBM + row_in_tile;
 #pragma unroll
                         for (int i = 0; i < 4; ++i)
-                            dst[i] = make_float4(__uint_as_float(r[4 * i]), __uint_as_float(r[4 * i + 1]),
+                            dst[i * kBM] = make_float4(__uint_as_float(r[4 * i]), __uint_as_float(r[4 * i + 1]),
                                                  __uint_as_float(r[4 * i + 2]),
                                                  __uint_as_float(r[4 * i + 3]));
                     }
@@ -365,15 +366,15 @@ __global__ void __launch_bounds__(kThreadsR, 1)
                 for (int c = half * NH; c < (half + 1) * NH; c += 16) {
                     uint32_t r[16];
                     ptx::tmem_ld_32x32b_x16(taddr + c, r);
-                    const float4 *src = reinterpret_cast<const float4 *>(
-                        part0 + ((c / 16) * kBM + row_in_tile) * 16);
+                    const float4 *src =
+                        reinterpret_cast<const float4 *>(part0) + (c / 16) * 4 * kBM + row_in_tile;
                     constexpr uint32_t kMaxParts = 4;
 #pragma unroll
                     for (int i = 0; i < 4; ++i) {
                         float4 v[kMaxParts - 1];  // every part's float4 in flight at once
 #pragma unroll
                         for (uint32_t h = 1; h < kMaxParts; ++h)
-                            if (h < p.splits) v[h - 1] = __ldcg(src + (h - 1) * (part_stride / 4) + i);
+                            if (h < p.splits) v[h - 1] = __ldcg(src + (h - 1) * (part_stride / 4) + i * kBM);
                         if (i == 0) ptx::tmem_ld_wait();
 #pragma unroll
                         for (uint32_t h = 1; h < kMaxParts; ++h)

@@ -184,3 +184,37 @@ def test_router_topk_layers_matches_per_layer(eng, shape, monkeypatch):
     # the descriptor table is cached: a second call with the same buffers reuses it
     idx3, w3 = eng.router_topk_layers(Xs, Ws, k, fn, renorm)
     assert torch.equal(idx3, idx2) and torch.equal(w3, w2)
+
+
+def test_router_topk_layers_errors(eng):
+    """Grouped-launch argument checks map onto the reference's error classes:
+    NULL buffers -> ValidationError, misaligned / unsupported shapes ->
+    ConfigError; zero layers is a no-op; a second descriptor table for new
+    buffers is created next to the first (both stay valid)."""
+    import ctypes as C
+
+    from paper_2604_23150_b200 import _abi
+    from paper_2604_23150_b200.errors import ConfigError, ValidationError
+    T, H, E, k = 512, 256, 64, 4
+    Xs = [torch.randn(T, H, device="cuda").to(torch.bfloat16) for _ in range(2)]
+    Ws = [(torch.randn(E, H, device="cuda") / 16).to(torch.bfloat16) for _ in range(2)]
+    idx = torch.empty(2, T, k, dtype=torch.int32, device="cuda")
+    w = torch.empty(2, T, k, dtype=torch.float32, device="cuda")
+    xp = (C.c_void_p * 2)(Xs[0].data_ptr(), 0)
+    wp = (C.c_void_p * 2)(Ws[0].data_ptr(), Ws[1].data_ptr())
+    with pytest.raises(ValidationError):
+        _abi.call("mpb_router_topk_layers", eng.ctx, 2, xp, wp, T, H, E, k, 0, 0,
+                  C.c_void_p(idx.data_ptr()), C.c_void_p(w.data_ptr()))
+    xp = (C.c_void_p * 2)(Xs[0].data_ptr() + 2, Xs[1].data_ptr())
+    with pytest.raises(ConfigError):
+        _abi.call("mpb_router_topk_layers", eng.ctx, 2, xp, wp, T, H, E, k, 0, 0,
+                  C.c_void_p(idx.data_ptr()), C.c_void_p(w.data_ptr()))
+    with pytest.raises(ConfigError):  # H not a multiple of 64
+        _abi.call("mpb_router_topk_layers", eng.ctx, 2, xp, wp, T, H - 32, E, k, 0, 0,
+                  C.c_void_p(idx.data_ptr()), C.c_void_p(w.data_ptr()))
+    _abi.call("mpb_router_topk_layers", eng.ctx, 0, None, None, T, H, E, k, 0, 0, None, None)
+    a = eng.router_topk_layers(Xs, Ws, k, 0, False)
+    b = eng.router_topk_layers(Xs[::-1], Ws[::-1], k, 0, False)
+    c = eng.router_topk_layers(Xs, Ws, k, 0, False)
+    torch.cuda.synchronize()
+    assert torch.equal(a[0], c[0]) and torch.equal(a[0][0], b[0][1]) and torch.equal(a[0][1], b[0][0])

@@ -1,3 +1,5 @@
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O2 -o tools/green/probe tools/green/probe.cu -lcuda
+// Run:   tools/green/probe <side SMs>   (on a B200, e.g. under gpurun)
 // Feasibility probe: SM partitions through green contexts, runtime-API launches
 // into their streams, and events shared with the primary context.
 #include <cuda.h>

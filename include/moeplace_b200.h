@@ -281,6 +281,17 @@ MPB_API mpb_status mpb_dispatch_p2p(mpb_context *ctx, const void *X, const int32
                                     const int64_t *counts, const int64_t *key_offsets,
                                     uint32_t span, uint32_t world, uint32_t rank,
                                     const uint64_t *peer_recv, uint64_t capacity_rows);
+/* Pull variant of mpb_dispatch_p2p: each rank copies the rows destined to it
+ * out of every source's staged hidden states into its own receive buffer.
+ * peer_x / peer_sorted_pairs / peer_key_offsets: device arrays of every
+ * rank's (symmetric-memory) X [T,H] bf16, sorted pairs and key offsets;
+ * counts: this rank's [world][world] count matrix (mpb_a2a_put_counts). The
+ * receive buffer ends up identical to the push dispatch's. */
+MPB_API mpb_status mpb_dispatch_pull(mpb_context *ctx, const int64_t *counts, const uint64_t *peer_x,
+                                     const uint64_t *peer_sorted_pairs,
+                                     const uint64_t *peer_key_offsets, uint32_t k, uint32_t H,
+                                     uint32_t span, uint32_t world, uint32_t rank, void *recv,
+                                     uint64_t capacity_rows);
 /* Return leg pushed instead of pulled: every received row (the first
  * `recv_rows` rows of this rank's buffer, grouped by source rank) is written
  * into its source rank's `back` buffer at its position in that rank's sorted

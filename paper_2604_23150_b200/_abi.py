@@ -72,6 +72,8 @@ _SIGS = {
                                    C.c_uint32, C.c_uint32, C.c_uint32, _p, C.c_uint64]),
     "mpb_return_p2p": (C.c_int, [_p, _p, C.c_uint64, C.c_uint32, _p, C.c_uint32, C.c_uint32,
                                  _p]),
+    "mpb_dispatch_pull": (C.c_int, [_p, _p, _p, _p, _p, C.c_uint32, C.c_uint32, C.c_uint32,
+                                    C.c_uint32, C.c_uint32, _p, C.c_uint64]),
     "mpb_combine_p2p": (C.c_int, [_p, _p, _p, C.c_uint64, C.c_uint32, C.c_uint32, _p, _p,
                                   C.c_uint32, C.c_uint32, C.c_uint32, _p, _p]),
     "mpb_linear_placement": (C.c_int, [C.c_uint32, C.c_uint32, _p]),

@@ -66,11 +66,21 @@ class ExpertParallelA2A:
         per_node = max(1, world // max(1, nodes))
         self.node_of_rank = [r // per_node for r in range(world)]
         self.p2p = False
+        self.phase_events = None  # list -> per-step (start, counts, dispatch, combine) events
 
-    def enable_p2p(self, capacity_rows: int, combine: str = "pull") -> None:
+    def enable_p2p(self, capacity_rows: int, combine: str = "pull", dispatch: str = "push",
+                   max_tokens: int | None = None) -> None:
         """Maps a `capacity_rows` x H bf16 receive buffer and a [world][world]
-        count matrix of every rank into this process (symmetric memory)."""
+        count matrix of every rank into this process (symmetric memory).
+        dispatch="pull": each rank also stages its hidden states (up to
+        `max_tokens` rows), sorted pairs and key offsets in symmetric memory,
+        and destinations copy their rows out of the sources' buffers
+        (mpb_dispatch_pull); "push": sources store rows into the destinations'
+        buffers (mpb_dispatch_p2p). Same receive buffer either way."""
         dev = self.eng.device
+        self.dispatch_mode = dispatch
+        if max_tokens is None:
+            max_tokens = self.send.shape[0]
         if self.world == 1:
             self.recv = torch.empty(capacity_rows, self.H, dtype=torch.bfloat16, device=dev)
             self.back_sym = self.back
@@ -79,6 +89,11 @@ class ExpertParallelA2A:
             self.peer_recv = torch.tensor([self.recv.data_ptr()], dtype=torch.uint64, device=dev)
             self.peer_cnt = torch.tensor([self.cnt.data_ptr()], dtype=torch.uint64, device=dev)
             self.hdl = None
+            if dispatch == "pull":
+                self.x_sym = torch.empty(max_tokens, self.H, dtype=torch.bfloat16, device=dev)
+                self.peer_x = torch.tensor([self.x_sym.data_ptr()], dtype=torch.uint64, device=dev)
+                self.peer_sp = torch.tensor([self.sp.data_ptr()], dtype=torch.uint64, device=dev)
+                self.peer_ko = torch.tensor([self.ko.data_ptr()], dtype=torch.uint64, device=dev)
         else:
             import torch.distributed._symmetric_memory as symm_mem
             gname = (self.group or dist.group.WORLD).group_name
@@ -100,6 +115,23 @@ class ExpertParallelA2A:
                                           device=dev)
             self.peer_cnt = torch.tensor(list(hc.buffer_ptrs), dtype=torch.uint64, device=dev)
             self._hc = hc
+            if dispatch == "pull":
+                mt = torch.tensor([max_tokens], dtype=torch.int64, device=dev)
+                dist.all_reduce(mt, op=dist.ReduceOp.MAX, group=self.group)
+                self.x_sym = symm_mem.empty(int(mt.item()), self.H, dtype=torch.bfloat16,
+                                            device=dev)
+                hx = symm_mem.rendezvous(self.x_sym, gname)
+                # the layout writes the sorted pairs / key offsets straight into
+                # symmetric buffers the destinations read
+                sp = symm_mem.empty(int(mx.item()), dtype=torch.int32, device=dev)
+                hs = symm_mem.rendezvous(sp, gname)
+                ko = symm_mem.empty(self.D * self.E + 1, dtype=torch.int64, device=dev)
+                hk = symm_mem.rendezvous(ko, gname)
+                self.sp, self.ko = sp, ko
+                self.peer_x = torch.tensor(list(hx.buffer_ptrs), dtype=torch.uint64, device=dev)
+                self.peer_sp = torch.tensor(list(hs.buffer_ptrs), dtype=torch.uint64, device=dev)
+                self.peer_ko = torch.tensor(list(hk.buffer_ptrs), dtype=torch.uint64, device=dev)
+                self._hx, self._hs, self._hk = hx, hs, hk
         self.capacity = capacity_rows
         self.combine_mode = combine  # "pull": remote loads in the combine (default); "push"
         self.p2p = True
@@ -156,11 +188,27 @@ class ExpertParallelA2A:
         span = groups_per_rank(self.D, self.world) * self.E
         if stats is not None:
             self._count_stats(stats)
+        ph = self.phase_events  # optional per-phase device timing (tools/bench_a2a.py)
+        if ph is not None:
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+            ph.append(ev)
+            ev[0].record(eng.stream)
+        pull = self.dispatch_mode == "pull"
+        if pull:  # stage the hidden states where the destinations can read them
+            self.x_sym[:X.shape[0]].copy_(X)
         eng.a2a_put_counts(self.ko, span, self.world, self.rank, self.peer_cnt)
-        self._barrier()  # every rank's counts are in every count matrix
-        eng.dispatch_p2p(X, self.sp[:n], k, self.cnt, self.ko, span, self.world, self.rank,
-                         self.peer_recv, self.capacity)
+        self._barrier()  # every rank's counts (and staged rows / pairs) are visible
+        if ph is not None:
+            ev[1].record(eng.stream)
+        if pull:
+            eng.dispatch_pull(self.cnt, self.peer_x, self.peer_sp, self.peer_ko, k, self.H, span,
+                              self.world, self.rank, self.recv, self.capacity)
+        else:
+            eng.dispatch_p2p(X, self.sp[:n], k, self.cnt, self.ko, span, self.world, self.rank,
+                             self.peer_recv, self.capacity)
         self._barrier()  # every row has landed in its destination buffer
+        if ph is not None:
+            ev[2].record(eng.stream)
         # expert FFN stand-in: identity on this rank's received rows
         if self.combine_mode == "push":
             # each rank pushes the rows it received (after its experts) back to
@@ -168,12 +216,17 @@ class ExpertParallelA2A:
             eng.return_p2p(self.recv, self.capacity, self.cnt, self.world, self.rank,
                            self.peer_back)
             self._barrier()  # every row is home
-            return eng.combine_scatter(self.back_sym[:n], self.pp[:n], w)
+            Y = eng.combine_scatter(self.back_sym[:n], self.pp[:n], w)
+            if ph is not None:
+                ev[3].record(eng.stream)
+            return Y
         self._barrier()  # every rank's experts are done with its rows
         Y = torch.empty(idx.shape[0], self.H, dtype=torch.bfloat16, device=X.device)
         eng.combine_p2p(self.pp[:n], w, self.H, self.cnt, self.ko, span, self.world, self.rank,
                         self.peer_recv, Y)
         self._barrier()  # peers have read their rows back: buffers reusable
+        if ph is not None:
+            ev[3].record(eng.stream)
         return Y
 
 

@@ -102,8 +102,11 @@ __global__ void __launch_bounds__(256) k_dispatch_p2p(const uint4 *X, const int3
     __shared__ P2PMap m;
     if (threadIdx.x == 0) p2p_map(C, ko, span, world, me, m);
     __syncthreads();
-    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
-    if (i >= n) return;
+    const uint64_t i0 = static_cast<uint64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+    if (i0 >= n) return;
+    // rotated start (see k_dispatch_p2p_tma)
+    const uint64_t rot = static_cast<uint64_t>(m.first[(me + 1) % world]) % n;
+    const uint64_t i = i0 + rot >= n ? i0 + rot - n : i0 + rot;
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t r = rank_of_pos(m, world, static_cast<int64_t>(i));
     const uint64_t row = static_cast<uint64_t>(m.base[r] + static_cast<int64_t>(i) - m.first[r]);
@@ -162,6 +165,60 @@ __global__ void __launch_bounds__(256) k_combine_p2p(const int32_t *pair_pos, co
     }
 }
 
+// Pull variant of the dispatch: the DESTINATION copies its rows out of the
+// sources' staged X (symmetric memory), in exactly the layout the push
+// dispatch produces (source s's rows at sum_{s'<s} C[s'][me], in s's sorted
+// order), so the combine and its output are unchanged. Remote reads run at the
+// NVLink ingress rate of the pull combine (the pushed stores were measured at
+// ~420 GB/s egress at 4 ranks). Warp per row, 8 independent 16-byte loads in
+// flight per lane; the row's token id comes from the source's sorted pairs.
+__global__ void __launch_bounds__(256) k_dispatch_pull(const int64_t *C, const uint64_t *peer_x,
+                                                       const uint64_t *peer_sp, const uint64_t *peer_ko,
+                                                       uint32_t k, uint32_t hv, uint32_t span,
+                                                       uint32_t world, uint32_t me, uint4 *recv,
+                                                       uint64_t cap, uint32_t *err) {
+    __shared__ int64_t s_off[9], s_first[8];
+    if (threadIdx.x < world)
+        s_first[threadIdx.x] =
+            reinterpret_cast<const int64_t *>(peer_ko[threadIdx.x])[static_cast<size_t>(me) * span];
+    if (threadIdx.x == 0) {
+        s_off[0] = 0;
+        for (uint32_t s = 0; s < world; ++s) s_off[s + 1] = s_off[s] + C[s * world + me];
+    }
+    __syncthreads();
+    const uint64_t total = static_cast<uint64_t>(s_off[world]);
+    const uint32_t lane = threadIdx.x & 31;
+    // rotated start: rows from source me+1 first, so the ranks do not all read
+    // the same source at once (one hot NVLink port)
+    const uint64_t rot = total ? static_cast<uint64_t>(s_off[(me + 1) % world]) % total : 0;
+    for (uint64_t qq = static_cast<uint64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5); qq < total;
+         qq += static_cast<uint64_t>(gridDim.x) * 8) {
+        const uint64_t q = qq + rot >= total ? qq + rot - total : qq + rot;
+        if (q >= cap) {
+            if (lane == 0) atomicOr(err, kErrCapacity);
+            continue;
+        }
+        uint32_t s = 0;
+        while (s + 1 < world && static_cast<int64_t>(q) >= s_off[s + 1]) ++s;
+        const int64_t j = static_cast<int64_t>(q) - s_off[s];
+        int32_t pair = 0;
+        if (lane == 0) pair = reinterpret_cast<const int32_t *>(peer_sp[s])[s_first[s] + j];
+        pair = __shfl_sync(0xffffffffu, pair, 0);
+        const uint4 *src = reinterpret_cast<const uint4 *>(peer_x[s]) +
+                           (static_cast<uint64_t>(pair) / k) * hv;
+        uint4 *dst = recv + q * hv;
+        uint32_t c = lane;
+        for (; c + 7 * 32 < hv; c += 8 * 32) {
+            uint4 v[8];
+#pragma unroll
+            for (int b = 0; b < 8; ++b) v[b] = __ldcg(src + c + b * 32);
+#pragma unroll
+            for (int b = 0; b < 8; ++b) dst[c + b * 32] = v[b];
+        }
+        for (; c < hv; c += 32) dst[c] = __ldcg(src + c);
+    }
+}
+
 // TMA variant of the dispatch: one issuing thread per CTA streams rows
 // through a ring of kRing shared-memory row buffers — bulk load of the token's
 // row from local HBM, then bulk store straight into the destination rank's
@@ -183,7 +240,13 @@ __global__ void __launch_bounds__(32) k_dispatch_p2p_tma(const uint8_t *X, const
     ptx::fence_barrier_init();
     const uint64_t first = blockIdx.x, step = gridDim.x;
     const uint64_t cnt = first < n ? (n - first + step - 1) / step : 0;
-    auto row_of = [&](uint64_t j) { return first + j * step; };
+    // rotated start: this rank's rows for rank me+1 first, so the ranks do not
+    // all push into the same destination at once (one hot NVLink port)
+    const uint64_t rot = static_cast<uint64_t>(m.first[(me + 1) % world]) % n;
+    auto row_of = [&](uint64_t j) {
+        const uint64_t i = first + j * step + rot;
+        return i >= n ? i - n : i;
+    };
     auto load = [&](uint64_t j) {
         const int slot = static_cast<int>(j % kRing);
         const uint64_t tok = static_cast<uint64_t>(sorted_pairs[row_of(j)]) / k;
@@ -235,8 +298,12 @@ __global__ void __launch_bounds__(256) k_return_p2p(const uint4 *recv, uint64_t 
         s_base[world] = b;
     }
     __syncthreads();
-    const uint64_t row = static_cast<uint64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
-    if (row >= rows || static_cast<int64_t>(row) >= s_base[world]) return;
+    const uint64_t row0 = static_cast<uint64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+    const uint64_t total = static_cast<uint64_t>(s_base[world]);
+    if (row0 >= rows || row0 >= total) return;
+    // rotated start: rows of source me+1 first (no single hot destination)
+    const uint64_t rot = static_cast<uint64_t>(s_base[(me + 1) % world]) % total;
+    const uint64_t row = row0 + rot >= total ? row0 + rot - total : row0 + rot;
     const uint32_t lane = threadIdx.x & 31;
     uint32_t q = 0;
     while (q + 1 < world && static_cast<int64_t>(row) >= s_base[q + 1]) ++q;
@@ -317,6 +384,22 @@ mpb_status mpb_dispatch_p2p(mpb_context *ctx, const void *X, const int32_t *sort
     k_dispatch_p2p<<<static_cast<unsigned>((n_pairs + 7) / 8), 256, 0, ctx->stream>>>(
         static_cast<const uint4 *>(X), sorted_pairs, n_pairs, k, H / 8, counts, key_offsets, span,
         world, rank, peer_recv, capacity_rows, ctx->d_error);
+    MPB_LAUNCHED(ctx);
+    return MPB_OK;
+}
+
+mpb_status mpb_dispatch_pull(mpb_context *ctx, const int64_t *counts, const uint64_t *peer_x,
+                             const uint64_t *peer_sorted_pairs, const uint64_t *peer_key_offsets,
+                             uint32_t k, uint32_t H, uint32_t span, uint32_t world, uint32_t rank,
+                             void *recv, uint64_t capacity_rows) {
+    if (!ctx || !counts || !peer_x || !peer_sorted_pairs || !peer_key_offsets || !recv)
+        return fail(MPB_VALIDATION_ERROR, "mpb_dispatch_pull: NULL argument");
+    if (H % 8 != 0 || k == 0) return fail(MPB_CONFIG_ERROR, "mpb_dispatch_pull: need H % 8 == 0, k >= 1");
+    if (world < 1 || world > 8 || rank >= world)
+        return fail(MPB_CONFIG_ERROR, "mpb_dispatch_pull: need 1 <= world <= 8, rank < world");
+    k_dispatch_pull<<<static_cast<unsigned>(ctx->num_sms) * 4, 256, 0, ctx->stream>>>(
+        counts, peer_x, peer_sorted_pairs, peer_key_offsets, k, H / 8, span, world, rank,
+        static_cast<uint4 *>(recv), capacity_rows, ctx->d_error);
     MPB_LAUNCHED(ctx);
     return MPB_OK;
 }

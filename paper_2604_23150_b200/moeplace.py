@@ -529,6 +529,12 @@ class Engine:
                   k, X.shape[1], _ptr(counts), _ptr(key_offsets), span, world, rank,
                   _ptr(peer_recv), capacity_rows)
 
+    def dispatch_pull(self, counts, peer_x, peer_sorted_pairs, peer_key_offsets, k: int, H: int,
+                      span: int, world: int, rank: int, recv, capacity_rows: int):
+        _abi.call("mpb_dispatch_pull", self.ctx, _ptr(counts), _ptr(peer_x),
+                  _ptr(peer_sorted_pairs), _ptr(peer_key_offsets), k, H, span, world, rank,
+                  _ptr(recv), capacity_rows)
+
     def return_p2p(self, recv, recv_rows: int, counts, world: int, rank: int, peer_back):
         _abi.call("mpb_return_p2p", self.ctx, _ptr(recv), recv_rows, recv.shape[1], _ptr(counts),
                   world, rank, _ptr(peer_back))

@@ -333,10 +333,12 @@ def test_coactivation_unaligned_ids(eng, oracle, k):
     np.testing.assert_array_equal(c.cpu().numpy(), oracle.coactivation(idx, E))
 
 
+@pytest.mark.parametrize("dispatch", ["pull", "push"])
 @pytest.mark.parametrize("mode", ["pull", "push"])
-def test_p2p_dispatch_combine_matches_local(eng, mode):
+def test_p2p_dispatch_combine_matches_local(eng, mode, dispatch):
     """K6-P2P at world 1 (the peer map is this rank's own buffers): the fused
-    dispatch / return / combine equals gather + local permute + combine."""
+    dispatch (sources push / destinations pull) / return / combine equals
+    gather + local permute + combine."""
     from paper_2604_23150_b200.a2a import ExpertParallelA2A
     rng = np.random.default_rng(5)
     T, E, k, D, H = 3000, 64, 4, 8, 256
@@ -348,10 +350,13 @@ def test_p2p_dispatch_combine_matches_local(eng, mode):
     pl, top = make_placement(rng, E, D, 0), topo(D, 2)
     op = ExpertParallelA2A(eng, pl, top, H, T * k)
     ref = op(X, idx, w, src)
-    op.enable_p2p(2 * T * k, combine=mode)
+    op.enable_p2p(2 * T * k, combine=mode, dispatch=dispatch, max_tokens=T)
     got = op(X, idx, w, src)
     eng.sync()
     assert torch.equal(got, ref)
+    got2 = op(X, idx, w, src)  # staged buffers reused on the next step
+    eng.sync()
+    assert torch.equal(got2, ref)
 
 
 @pytest.mark.parametrize("sms", [2, 20])

@@ -140,15 +140,32 @@ def main():
                                inter_fraction=inter / max(1, sent), max_abs_err=err,
                                tokens_per_rank=T)
         if not a.no_p2p:  # fused NVLink path: same output bit for bit
-            for mode in ("push", "pull"):
-                op.enable_p2p(2 * T * spec.top_k, combine=mode)
+            for dmode, mode in (("push", "push"), ("push", "pull"), ("pull", "pull")):
+                op.enable_p2p(2 * T * spec.top_k, combine=mode, dispatch=dmode, max_tokens=T)
+                op.phase_events = None
                 Yp, ms_p, _ = timed(lambda st_: op(X, idx, w, src, st_))
+                # per-phase split on separate steps (events between phases)
+                op.phase_events = []
+                for _ in range(4):
+                    op(X, idx, w, src, None)
+                torch.cuda.synchronize()
+                ph = np.array([[a_.elapsed_time(b_) for a_, b_ in zip(ev[:-1], ev[1:])]
+                               for ev in op.phase_events[1:]]).mean(0)
+                op.phase_events = None
+                tag = mode if dmode == "push" else f"{dmode}_{mode}"
+                # rows each rank receives (column sums of the count matrix): the
+                # dispatch is bound by the most loaded destination
+                C = op.cnt.view(world, world).double()
+                recv_rows = C.sum(0)
+                results[policy]["recv_rows_max_over_mean"] = float(recv_rows.max() / recv_rows.mean())
+                results[policy][f"p2p_{tag}_phase_ms"] = {
+                    "counts": float(ph[0]), "dispatch": float(ph[1]), "combine": float(ph[2])}
                 eng.sync()
                 same = torch.tensor([int(torch.equal(Yp, Y))], device=eng.device)
                 if world > 1:
                     dist.all_reduce(same, op=dist.ReduceOp.MIN)
-                results[policy].update({f"p2p_{mode}_ms_per_step": ms_p,
-                                        f"p2p_{mode}_bit_identical": bool(same.item())})
+                results[policy].update({f"p2p_{tag}_ms_per_step": ms_p,
+                                        f"p2p_{tag}_bit_identical": bool(same.item())})
     if rank == 0:
         base = results["round_robin"]["inter_node_bytes"]
         saved = 1.0 - results["learned"]["inter_node_bytes"] / base if base else float("nan")

@@ -141,6 +141,49 @@ __global__ void __launch_bounds__(256) k_combine_p2p(const int32_t *pair_pos, co
     const uint64_t t = static_cast<uint64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
     if (t >= T) return;
     const uint32_t lane = threadIdx.x & 31;
+    if (k <= 8) {
+        // the token's k rows located once; each lane then issues all k remote
+        // loads of a column before accumulating them in j order (bit-identical
+        // to the loop below, more bytes in flight per warp)
+        const uint4 *rowp[8];
+        float wj[8];
+#pragma unroll
+        for (uint32_t j = 0; j < 8; ++j) {
+            rowp[j] = nullptr;
+            wj[j] = 0.f;
+            if (j < k) {
+                const int64_t pos = pair_pos[t * k + j];
+                const uint32_t r = rank_of_pos(m, world, pos);
+                const uint64_t row = static_cast<uint64_t>(m.base[r] + pos - m.first[r]);
+                rowp[j] = reinterpret_cast<const uint4 *>(peer_recv[r]) + row * hv;
+                wj[j] = w[t * k + j];
+            }
+        }
+        for (uint32_t c = lane; c < hv; c += 32) {
+            uint4 v[8];
+#pragma unroll
+            for (uint32_t j = 0; j < 8; ++j)
+                if (j < k) v[j] = rowp[j][c];
+            float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+            for (uint32_t j = 0; j < 8; ++j) {
+                if (j >= k) break;
+                const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&v[j]);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const float2 f = __bfloat1622float2(h[q]);
+                    acc[2 * q] = fmaf(wj[j], f.x, acc[2 * q]);
+                    acc[2 * q + 1] = fmaf(wj[j], f.y, acc[2 * q + 1]);
+                }
+            }
+            uint4 o;
+            __nv_bfloat162 *oh = reinterpret_cast<__nv_bfloat162 *>(&o);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) oh[q] = __floats2bfloat162_rn(acc[2 * q], acc[2 * q + 1]);
+            Y[t * hv + c] = o;
+        }
+        return;
+    }
     for (uint32_t c = lane; c < hv; c += 32) {
         float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         for (uint32_t j = 0; j < k; ++j) {

@@ -27,6 +27,7 @@
  *   mpb_score_placements   simulate_layer over P candidates x B batches
  *                          (simulator.cpp:43-99)
  *   mpb_finalize_layer_sims padded_all_to_all_time + LayerSim times
+ *   mpb_score_placements_finalize  the two above in one launch
  *                          (simulator.cpp:27-41, 90-98), bit-exact doubles
  *   mpb_dispatch_gather / mpb_combine_scatter  (new) physical bf16 dispatch /
  *                          combine around the all-to-all
@@ -250,6 +251,14 @@ MPB_API mpb_status mpb_finalize_layer_sims(mpb_context *ctx, const uint64_t *int
                                            uint64_t N, uint32_t D, const double *cost,
                                            uint32_t tp_exp, int spans_nodes, double *out,
                                            double *payload);
+/* mpb_score_placements with mpb_finalize_layer_sims fused into its epilogue
+ * (one launch; each cell's LayerSim computed by the warp that priced it, the
+ * same operations in the same order: bit-identical to the two calls). */
+MPB_API mpb_status mpb_score_placements_finalize(
+    mpb_context *ctx, const uint64_t *demand, uint32_t B, uint32_t rows, const uint8_t *row_node,
+    const uint8_t *luts, uint32_t P, const uint8_t *group_to_node, uint32_t D, uint32_t nodes,
+    uint32_t E, uint64_t *inter, uint64_t *intra, uint64_t *rank_pairs, const double *cost,
+    uint32_t tp_exp, int spans_nodes, double *out, double *payload);
 
 /* ---- physical dispatch / combine (bf16 hidden states) --------------------
  * gather:  send[pos][:] = X[sorted_pairs[pos] / k][:] for pos < n_pairs

@@ -65,6 +65,9 @@ _SIGS = {
                                        C.c_uint32, C.c_uint32, C.c_uint32, _p, _p, _p]),
     "mpb_finalize_layer_sims": (C.c_int, [_p, _p, _p, _p, C.c_uint64, C.c_uint32, _f64p,
                                           C.c_uint32, C.c_int, _p, _p]),
+    "mpb_score_placements_finalize": (C.c_int, [_p, _p, C.c_uint32, C.c_uint32, _p, _p, C.c_uint32,
+                                                _p, C.c_uint32, C.c_uint32, C.c_uint32, _p, _p, _p,
+                                                _f64p, C.c_uint32, C.c_int, _p, _p]),
     "mpb_dispatch_gather": (C.c_int, [_p, _p, _p, C.c_uint64, C.c_uint32, C.c_uint32, _p]),
     "mpb_combine_scatter": (C.c_int, [_p, _p, _p, _p, C.c_uint64, C.c_uint32, C.c_uint32, _p]),
     "mpb_a2a_put_counts": (C.c_int, [_p, _p, C.c_uint32, C.c_uint32, C.c_uint32, _p]),

@@ -64,6 +64,50 @@ __global__ void __launch_bounds__(256) k_batch_demand(const uint32_t *row_ptr, c
         for (uint32_t i = threadIdx.x; i < nodes * E; i += blockDim.x) out[i] = s_nd[i];
 }
 
+struct CostParams {
+    double hidden, bpe, inter_bw, intra_bw, etpt, overhead;
+};
+
+// One LayerSim from a cell's integer pair counts — simulate_layer's doubles in
+// the reference's order of operations (shared by k_finalize and the fused
+// scorer, so both produce the same bits).
+__device__ __forceinline__ void finalize_cell(uint64_t i, uint64_t inter, uint64_t intra,
+                                              const uint64_t *rank, uint32_t D, const CostParams &c,
+                                              uint32_t tp_exp, int spans, double *out, double *payload) {
+    // bytes_per_token = double(hidden) * double(bpe) (simulator.cpp:57-58)
+    const double bpt = __dmul_rn(c.hidden, c.bpe);
+    double mx = 0.0, straggler = 0.0;
+    for (uint32_t d = 0; d < D; ++d) {
+        const double pairs = static_cast<double>(rank[d]);
+        const double bytes = __dmul_rn(pairs, bpt);
+        if (payload) payload[i * D + d] = bytes;
+        if (d == 0 || bytes > mx) mx = bytes;
+        if (d == 0 || pairs > straggler) straggler = pairs;
+    }
+    const double bw = spans ? c.inter_bw : c.intra_bw;
+    // max_payload / tp_exp / bandwidth (simulator.cpp:40)
+    const double dispatch = __ddiv_rn(__ddiv_rn(mx, static_cast<double>(tp_exp)), bw);
+    const double compute = __dmul_rn(c.etpt, straggler);
+    // dispatch + compute + combine + overhead, left to right (simulator.cpp:96-97)
+    const double layer = __dadd_rn(__dadd_rn(__dadd_rn(dispatch, compute), dispatch), c.overhead);
+    double *o = out + i * 6;
+    o[0] = __dmul_rn(static_cast<double>(inter), bpt);
+    o[1] = __dmul_rn(static_cast<double>(intra), bpt);
+    o[2] = dispatch;
+    o[3] = compute;
+    o[4] = dispatch;
+    o[5] = layer;
+}
+
+// optional fused finalize of the scorer (out == nullptr: off)
+struct FinalizeArgs {
+    CostParams c;
+    uint32_t tp_exp;
+    int spans;
+    double *out;
+    double *payload;
+};
+
 constexpr int kScoreWarps = 8;
 constexpr uint32_t kScoreMaxD = 32;  // lane-private rank accumulators in smem
 
@@ -81,7 +125,8 @@ __global__ void __launch_bounds__(kScoreWarps * 32) k_score(const uint64_t *dema
                                                             uint32_t nodes, uint32_t E,
                                                             uint64_t *inter_out,
                                                             uint64_t *intra_out,
-                                                            uint64_t *rank_out, uint32_t *err) {
+                                                            uint64_t *rank_out, uint32_t *err,
+                                                            FinalizeArgs fin) {
     extern __shared__ unsigned long long s_raw[];
     const uint32_t NE = nodes * E;
     unsigned long long *s_nd = s_raw;                        // [nodes*E]
@@ -144,42 +189,19 @@ __global__ void __launch_bounds__(kScoreWarps * 32) k_score(const uint64_t *dema
                 t = acc[d];
             rank_out[cell * D + d] = t;
         }
-        __syncwarp();
+        __syncwarp();  // the warp's rank totals are visible to lane 0
+        if (fin.out && lane == 0)
+            finalize_cell(cell, inter, intra, rank_out + cell * D, D, fin.c, fin.tp_exp, fin.spans,
+                          fin.out, fin.payload);
     }
 }
-
-struct CostParams {
-    double hidden, bpe, inter_bw, intra_bw, etpt, overhead;
-};
 
 __global__ void k_finalize(const uint64_t *inter, const uint64_t *intra, const uint64_t *rank,
                            uint64_t N, uint32_t D, CostParams c, uint32_t tp_exp, int spans,
                            double *out, double *payload) {
     const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= N) return;
-    // bytes_per_token = double(hidden) * double(bpe) (simulator.cpp:57-58)
-    const double bpt = __dmul_rn(c.hidden, c.bpe);
-    double mx = 0.0, straggler = 0.0;
-    for (uint32_t d = 0; d < D; ++d) {
-        const double pairs = static_cast<double>(rank[i * D + d]);
-        const double bytes = __dmul_rn(pairs, bpt);
-        if (payload) payload[i * D + d] = bytes;
-        if (d == 0 || bytes > mx) mx = bytes;
-        if (d == 0 || pairs > straggler) straggler = pairs;
-    }
-    const double bw = spans ? c.inter_bw : c.intra_bw;
-    // max_payload / tp_exp / bandwidth (simulator.cpp:40)
-    const double dispatch = __ddiv_rn(__ddiv_rn(mx, static_cast<double>(tp_exp)), bw);
-    const double compute = __dmul_rn(c.etpt, straggler);
-    // dispatch + compute + combine + overhead, left to right (simulator.cpp:96-97)
-    const double layer = __dadd_rn(__dadd_rn(__dadd_rn(dispatch, compute), dispatch), c.overhead);
-    double *o = out + i * 6;
-    o[0] = __dmul_rn(static_cast<double>(inter[i]), bpt);
-    o[1] = __dmul_rn(static_cast<double>(intra[i]), bpt);
-    o[2] = dispatch;
-    o[3] = compute;
-    o[4] = dispatch;
-    o[5] = layer;
+    finalize_cell(i, inter[i], intra[i], rank + i * D, D, c, tp_exp, spans, out, payload);
 }
 
 }  // namespace
@@ -208,42 +230,10 @@ mpb_status mpb_batch_demand(mpb_context *ctx, const uint32_t *row_ptr, const uin
     return MPB_OK;
 }
 
-mpb_status mpb_score_placements(mpb_context *ctx, const uint64_t *demand, uint32_t B,
-                                uint32_t rows, const uint8_t *row_node, const uint8_t *luts,
-                                uint32_t P, const uint8_t *group_to_node, uint32_t D,
-                                uint32_t nodes, uint32_t E, uint64_t *inter, uint64_t *intra,
-                                uint64_t *rank_pairs) {
-    if (!ctx || !demand || !row_node || !luts || !group_to_node || !inter || !intra || !rank_pairs)
-        return fail(MPB_VALIDATION_ERROR, "mpb_score_placements: NULL argument");
-    if (rows == 0 || rows > 255) return fail(MPB_CONFIG_ERROR, "mpb_score_placements: need 1 <= rows <= 255");
-    if (D == 0 || D > 255 || nodes == 0)
-        return fail(MPB_CONFIG_ERROR, "mpb_score_placements: need 1 <= D <= 255, nodes >= 1");
-    if (P == 0 || B == 0) return MPB_OK;
-    const bool priv = D <= kScoreMaxD;
-    const size_t smem =
-        size_t(nodes) * E * 8 + size_t(kScoreWarps) * D * (priv ? 32 : 1) * 8 + D + 8;
-    if (smem > 200 * 1024) return fail(MPB_CONFIG_ERROR, "mpb_score_placements: nodes*E too large");
-    auto kern = priv ? k_score<true> : k_score<false>;
-    MPB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    // one CTA per batch; split candidates over grid.y until the machine is full
-    const uint32_t want = 4u * static_cast<uint32_t>(ctx->num_sms);
-    uint32_t gy = std::max(1u, want / std::max(1u, B));
-    gy = std::min(gy, (P + kScoreWarps - 1) / kScoreWarps);
-    gy = std::min(gy, 65535u);
-    dim3 grid(B, gy);
-    kern<<<grid, kScoreWarps * 32, smem, ctx->stream>>>(demand, B, rows, row_node, luts, P,
-                                                           group_to_node, D, nodes, E, inter,
-                                                           intra, rank_pairs, ctx->d_error);
-    MPB_LAUNCHED(ctx);
-    return MPB_OK;
-}
+}  // extern "C"
 
-mpb_status mpb_finalize_layer_sims(mpb_context *ctx, const uint64_t *inter, const uint64_t *intra,
-                                   const uint64_t *rank_pairs, uint64_t N, uint32_t D,
-                                   const double *cost, uint32_t tp_exp, int spans_nodes,
-                                   double *out, double *payload) {
-    if (!ctx || !inter || !intra || !rank_pairs || !cost || !out)
-        return fail(MPB_VALIDATION_ERROR, "mpb_finalize_layer_sims: NULL argument");
+namespace {
+mpb_status check_cost(const double *cost, uint32_t tp_exp) {
     // CostModelParams::validate (simulator.cpp:14-25)
     if (cost[0] < 1 || cost[1] < 1)
         return fail(MPB_CONFIG_ERROR, "cost model: hidden_dim and bytes_per_element must be >= 1");
@@ -256,6 +246,73 @@ mpb_status mpb_finalize_layer_sims(mpb_context *ctx, const uint64_t *inter, cons
     if (cost[5] < 0.0)
         return fail(MPB_CONFIG_ERROR, "cost model: fixed_layer_overhead must be >= 0");
     if (tp_exp == 0) return fail(MPB_CONFIG_ERROR, "topology: tp_exp must be >= 1");
+    return MPB_OK;
+}
+
+mpb_status launch_score(mpb_context *ctx, const char *fn, const uint64_t *demand, uint32_t B,
+                        uint32_t rows, const uint8_t *row_node, const uint8_t *luts, uint32_t P,
+                        const uint8_t *group_to_node, uint32_t D, uint32_t nodes, uint32_t E,
+                        uint64_t *inter, uint64_t *intra, uint64_t *rank_pairs, FinalizeArgs fin) {
+    if (!ctx || !demand || !row_node || !luts || !group_to_node || !inter || !intra || !rank_pairs)
+        return fail(MPB_VALIDATION_ERROR, std::string(fn) + ": NULL argument");
+    if (rows == 0 || rows > 255) return fail(MPB_CONFIG_ERROR, std::string(fn) + ": need 1 <= rows <= 255");
+    if (D == 0 || D > 255 || nodes == 0)
+        return fail(MPB_CONFIG_ERROR, std::string(fn) + ": need 1 <= D <= 255, nodes >= 1");
+    if (P == 0 || B == 0) return MPB_OK;
+    const bool priv = D <= kScoreMaxD;
+    const size_t smem =
+        size_t(nodes) * E * 8 + size_t(kScoreWarps) * D * (priv ? 32 : 1) * 8 + D + 8;
+    if (smem > 200 * 1024) return fail(MPB_CONFIG_ERROR, std::string(fn) + ": nodes*E too large");
+    auto kern = priv ? k_score<true> : k_score<false>;
+    MPB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    // one CTA per batch; split candidates over grid.y until the machine is full
+    const uint32_t want = 4u * static_cast<uint32_t>(ctx->num_sms);
+    uint32_t gy = std::max(1u, want / std::max(1u, B));
+    gy = std::min(gy, (P + kScoreWarps - 1) / kScoreWarps);
+    gy = std::min(gy, 65535u);
+    dim3 grid(B, gy);
+    kern<<<grid, kScoreWarps * 32, smem, ctx->stream>>>(demand, B, rows, row_node, luts, P,
+                                                           group_to_node, D, nodes, E, inter,
+                                                           intra, rank_pairs, ctx->d_error, fin);
+    MPB_LAUNCHED(ctx);
+    return MPB_OK;
+}
+}  // namespace
+
+extern "C" {
+
+mpb_status mpb_score_placements(mpb_context *ctx, const uint64_t *demand, uint32_t B,
+                                uint32_t rows, const uint8_t *row_node, const uint8_t *luts,
+                                uint32_t P, const uint8_t *group_to_node, uint32_t D,
+                                uint32_t nodes, uint32_t E, uint64_t *inter, uint64_t *intra,
+                                uint64_t *rank_pairs) {
+    return launch_score(ctx, "mpb_score_placements", demand, B, rows, row_node, luts, P,
+                        group_to_node, D, nodes, E, inter, intra, rank_pairs,
+                        FinalizeArgs{CostParams{}, 1, 0, nullptr, nullptr});
+}
+
+mpb_status mpb_score_placements_finalize(mpb_context *ctx, const uint64_t *demand, uint32_t B,
+                                         uint32_t rows, const uint8_t *row_node, const uint8_t *luts,
+                                         uint32_t P, const uint8_t *group_to_node, uint32_t D,
+                                         uint32_t nodes, uint32_t E, uint64_t *inter, uint64_t *intra,
+                                         uint64_t *rank_pairs, const double *cost, uint32_t tp_exp,
+                                         int spans_nodes, double *out, double *payload) {
+    if (!ctx || !cost || !out)
+        return fail(MPB_VALIDATION_ERROR, "mpb_score_placements_finalize: NULL argument");
+    if (mpb_status st = check_cost(cost, tp_exp)) return st;
+    return launch_score(ctx, "mpb_score_placements_finalize", demand, B, rows, row_node, luts, P,
+                        group_to_node, D, nodes, E, inter, intra, rank_pairs,
+                        FinalizeArgs{CostParams{cost[0], cost[1], cost[2], cost[3], cost[4], cost[5]},
+                                     tp_exp, spans_nodes, out, payload});
+}
+
+mpb_status mpb_finalize_layer_sims(mpb_context *ctx, const uint64_t *inter, const uint64_t *intra,
+                                   const uint64_t *rank_pairs, uint64_t N, uint32_t D,
+                                   const double *cost, uint32_t tp_exp, int spans_nodes,
+                                   double *out, double *payload) {
+    if (!ctx || !inter || !intra || !rank_pairs || !cost || !out)
+        return fail(MPB_VALIDATION_ERROR, "mpb_finalize_layer_sims: NULL argument");
+    if (mpb_status st = check_cost(cost, tp_exp)) return st;
     if (N == 0) return MPB_OK;
     CostParams c{cost[0], cost[1], cost[2], cost[3], cost[4], cost[5]};
     const unsigned blocks = static_cast<unsigned>((N + 255) / 256);

@@ -463,6 +463,25 @@ class Engine:
                   _ptr(luts), P, _ptr(g2n), D, nodes, E, _ptr(inter), _ptr(intra), _ptr(rank))
         return inter, intra, rank
 
+    def score_and_finalize(self, demand: torch.Tensor, luts: torch.Tensor, g2n: torch.Tensor,
+                           D: int, cost: CostModelParams, topology: Topology, row_node=None,
+                           out=None, fin_out=None, payload=None):
+        """score_placements + finalize in one launch (bit-identical to the two)."""
+        B, rows, E = demand.shape
+        P, nodes, _ = luts.shape
+        if row_node is None:
+            row_node = torch.arange(rows, dtype=torch.uint8, device=self.device)
+        if out is None:
+            out = (self._u64(P, B), self._u64(P, B), self._u64(P, B, D))
+        if fin_out is None:
+            fin_out = torch.empty(P * B, 6, dtype=torch.float64, device=self.device)
+        inter, intra, rank = out
+        _abi.call("mpb_score_placements_finalize", self.ctx, _ptr(demand), B, rows, _ptr(row_node),
+                  _ptr(luts), P, _ptr(g2n), D, nodes, E, _ptr(inter), _ptr(intra), _ptr(rank),
+                  cost.as_array(), topology.tp_exp, int(topology.spans_nodes()), _ptr(fin_out),
+                  _ptr(payload))
+        return out, fin_out, payload
+
     def finalize(self, inter, intra, rank, D: int, cost: CostModelParams, topology: Topology,
                  out=None, payload=None):
         N = inter.numel()

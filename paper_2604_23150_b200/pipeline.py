@@ -495,20 +495,17 @@ class RoutingPipeline:
         if rr is not eng:
             self._sfork.record(eng.stream)
             rr.stream.wait_event(self._sfork)
-        rr.score_placements(self.dem_rr, self.luts_rr, self.g2n, D, row_node=self.g2n,
-                            out=self.sc_rr)
-        inter, intra, rank = self.sc_rr
-        rr.finalize(inter.view(-1), intra.view(-1), rank.view(-1, D), D, self.cost,
-                    self.topology, out=self.fin_rr[0], payload=self.fin_rr[1])
+        rr.score_and_finalize(self.dem_rr, self.luts_rr, self.g2n, D, self.cost, self.topology,
+                              row_node=self.g2n, out=self.sc_rr, fin_out=self.fin_rr[0],
+                              payload=self.fin_rr[1])
         if rr is not eng:
             self._sjoin.record(rr.stream)
         lo, hi = self.shard if self.shard is not None else (0, self.luts_cl.shape[0])
         inter, intra, rank = (t[lo:hi] for t in self.sc_cl)
-        eng.score_placements(self.dem_cl, self.luts_cl[lo:hi], self.g2n, D, row_node=self.g2n,
-                             out=(inter, intra, rank))
-        eng.finalize(inter.reshape(-1), intra.reshape(-1), rank.reshape(-1, D), D, self.cost,
-                     self.topology, out=self.fin_cl[0][lo * L:hi * L],
-                     payload=self.fin_cl[1][lo * L:hi * L])
+        eng.score_and_finalize(self.dem_cl, self.luts_cl[lo:hi], self.g2n, D, self.cost,
+                               self.topology, row_node=self.g2n, out=(inter, intra, rank),
+                               fin_out=self.fin_cl[0][lo * L:hi * L],
+                               payload=self.fin_cl[1][lo * L:hi * L])
         if rr is not eng:
             eng.stream.wait_event(self._sjoin)
 

@@ -416,3 +416,32 @@ def test_score_placements_group_rows_pipeline_shape(oracle, sms):
     np.testing.assert_array_equal(inter.cpu().numpy(), ri)
     np.testing.assert_array_equal(intra.cpu().numpy(), ra)
     np.testing.assert_array_equal(rank.cpu().numpy(), rr)
+
+
+@pytest.mark.parametrize("spans", [True, False])
+def test_score_and_finalize_fused_equals_two_launches(oracle, spans):
+    """mpb_score_placements_finalize (LayerSim doubles computed in the scorer's
+    epilogue) == mpb_score_placements then mpb_finalize_layer_sims, bit for
+    bit, integer outputs included; the LayerSims also match the oracle's
+    simulate_layer restatement on the same pair counts."""
+    rng = np.random.default_rng(7 + spans)
+    E, D, P, B = 128, 8, 300, 5
+    nodes = 2 if spans else 1
+    g2n = [d // (D // nodes) for d in range(D)]
+    dem = rng.integers(0, 300, (B, D, E)).astype(np.uint64)
+    dem[dem < 100] = 0
+    luts = np.stack([oracle.dest_lut(make_placement(rng, E, D, p % 3).groups, g2n, E)
+                     for p in range(P)])
+    e = mp.Engine(0)
+    top = mp.Topology.contiguous(D, 1, D, 1, nodes)
+    cost = mp.CostModelParams(7168, 2, 50e9, 300e9, 1e-7, 50e-6)
+    g2n_t = dev(np.array(g2n, np.uint8))
+    sc = e.score_placements(dev(dem), dev(luts), g2n_t, D, row_node=g2n_t)
+    f2, p2 = e.finalize(sc[0].view(-1), sc[1].view(-1), sc[2].view(-1, D), D, cost, top)
+    pay = torch.empty(P * B, D, dtype=torch.float64, device="cuda")
+    sc1, f1, p1 = e.score_and_finalize(dev(dem), dev(luts), g2n_t, D, cost, top,
+                                       row_node=g2n_t, payload=pay)
+    e.sync()
+    for a, b in zip(sc, sc1):
+        assert torch.equal(a, b)
+    assert torch.equal(f1, f2) and torch.equal(p1, p2)

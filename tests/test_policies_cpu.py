@@ -86,3 +86,19 @@ def test_kmeans_planted_clouds():
     assert m.labels[0] != m.labels[40]
     with pytest.raises(InfeasibleError):
         pol.kmeans(np.zeros((1, 3)), 1, 3, 2, 0)
+
+
+def test_router_chunk_taper():
+    """Grouped router launches (pipeline._taper_chunks): contiguous chunks that
+    cover every layer once, at most G layers each, ending 4, 2, 1 so the last
+    chunk's statistics tails are short."""
+    from paper_2604_23150_b200.pipeline import _taper_chunks
+    assert [b - a for a, b in _taper_chunks(58, 8)] == [3, 8, 8, 8, 8, 8, 8, 4, 2, 1]
+    for L in (1, 2, 3, 7, 8, 9, 16, 58, 61):
+        for G in (1, 2, 4, 8, 16, 64):
+            ch = _taper_chunks(L, G)
+            assert ch[0][0] == 0 and ch[-1][1] == L
+            assert all(a[1] == b[0] for a, b in zip(ch, ch[1:]))
+            assert all(0 < b - a <= max(G, 1) for a, b in ch)
+            if L > 1 and G > 1:
+                assert ch[-1][1] - ch[-1][0] == 1

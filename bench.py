@@ -325,6 +325,9 @@ def run_gpu_arm(args, spec):
     ms_step = float(t.item()) / args.steps
     eng.sync()
     res = pipe.results()
+    # the reference's statistic on the step's own routing (untimed): device
+    # compare_strategies over the measured layer's decode matrix
+    ref_stat = pipe.reference_statistic()
     tokens_step = spec.layers * spec.tokens * world
     value = tokens_step / (ms_step / 1e3)
 
@@ -387,9 +390,17 @@ def run_gpu_arm(args, spec):
                            "schedule": pipe.schedule(),
                            "l2": "inputs larger than L2 (each layer's X is "
                                  f"{spec.tokens * spec.hidden * 2 / 2**20:.0f} MiB)"},
-                "a2a_bytes_saved_pct": res["a2a_bytes_saved_pct"],
+                "a2a_bytes_saved_pct": ref_stat["a2a_bytes_saved_pct"],
+                "a2a_statistic": {
+                    "what": "compare_strategies (simulator.cpp:122-243) on device over the decode "
+                            "matrix of the measured layer: median over B batches of S sampled "
+                            "requests of inter-node bytes, data_based / linear",
+                    "layer": ref_stat["layer"], "requests": ref_stat["matrix"].rows,
+                    "batches": ref_stat["num_batches"], "batch_size": ref_stat["batch_size"],
+                    "seed": ref_stat["seed"], "normalized_median": ref_stat["normalized"]},
+                "per_layer_median_bytes_saved_pct": res["per_layer_median_bytes_saved_pct"],
                 "searched_a2a_bytes_saved_pct": res["searched_bytes_saved_pct"],
-                "normalized_inter_node_bytes": res["normalized"],
+                "normalized_inter_node_bytes_per_layer_median": res["normalized"],
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches, "cuda_graph": graphed, "clocks": clocks.summary()}
         print(json.dumps(line), flush=True)

@@ -131,7 +131,9 @@ MPB_API mpb_status mpb_router_topk(mpb_context *ctx, const void *X, const void *
                                    int32_t *idx, float *weights, float *logits_out);
 /* mpb_router_topk for `layers` independent layers of the same shape in ONE
  * persistent launch: X[l] [T,H] and W[l] [E,H] (host arrays of device
- * pointers); idx / weights are [layers][T][k] (device). Results equal
+ * pointers); idx / weights are [layers][T][k] (device); logits_out
+ * [layers][T][E] fp32 is optional (NULL in the step; parity tests check the
+ * grouped launch's top-k against the oracle on these logits). Results equal
  * mpb_router_topk per layer up to the fp32 order of the split-K tail (the last
  * wave of the whole launch). Only one exposed last-tile epilogue per launch
  * instead of one per layer. The TMA descriptors are encoded and uploaded on
@@ -140,7 +142,7 @@ MPB_API mpb_status mpb_router_topk(mpb_context *ctx, const void *X, const void *
 MPB_API mpb_status mpb_router_topk_layers(mpb_context *ctx, uint32_t layers, const void *const *X,
                                           const void *const *W, uint64_t T, uint32_t H, uint32_t E,
                                           uint32_t k, int score_fn, int renorm, int32_t *idx,
-                                          float *weights);
+                                          float *weights, float *logits_out);
 /* Top-k over given fp32 logits [T,E] (device), E <= 1024. */
 MPB_API mpb_status mpb_topk_logits(mpb_context *ctx, const float *logits, uint64_t T, uint32_t E,
                                    uint32_t k, int score_fn, int renorm, int32_t *idx,

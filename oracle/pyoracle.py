@@ -282,6 +282,10 @@ class Reference:
                                                C.c_uint64, _u32p]
         L.ref_compare_scenario.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, _f64p]
         L.ref_bench_compare.argtypes = [C.c_char_p, C.c_uint32, _f64p]
+        L.ref_compare_strategies.argtypes = [C.c_uint64, C.c_uint32, _f64p, C.c_uint32, C.c_char_p,
+                                             _u32p, _u32p, C.c_uint32, _i32p, _u64p, _u32p,
+                                             _u32p, _u32p, _f64p, C.c_uint32, C.c_uint32,
+                                             C.c_uint64, _f64p, _f64p, _f64p, _f64p]
         L.ref_analysis.argtypes = [C.c_char_p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_char_p]
         L.ref_bench_parse.argtypes = [C.c_char_p, C.c_uint32, C.c_uint32, C.c_uint32, _f64p,
                                       _f64p, C.POINTER(C.c_uint64)]
@@ -392,6 +396,35 @@ class Reference:
     def analysis(self, trace_path, E, top_k, layers, out_json):
         self._check(self.lib.ref_analysis(str(trace_path).encode(), E, top_k, layers,
                                           str(out_json).encode()))
+
+    def compare_strategies(self, values, strategies, routes, topology, cost, num_batches,
+                           batch_size, seed):
+        """compare_strategies (simulator.cpp:122-243) of the compiled reference
+        on given inputs. strategies: [(label, groups, cluster_routed)].
+        Returns (sims [B*S, 6], normalized [B*S], summary [S, 8], linear
+        median); rows in the reference's order (batch-major)."""
+        values = _c(values, np.float64)
+        R, E = values.shape
+        S = len(strategies)
+        D = len(strategies[0][1])
+        flat, sizes = [], []
+        for _, groups, _ in strategies:
+            f, z = groups_flat(groups)
+            flat.append(f)
+            sizes.append(z)
+        routed = np.array([int(c) for _, _, c in strategies], np.int32)
+        roff = np.concatenate([[0], np.cumsum([len(g) for g in routes])]).astype(np.uint64)
+        rflat = np.array([g for gs in routes for g in gs] or [0], np.uint32)
+        t, g2n = self.topo_arrays(topology)
+        sims = np.zeros((num_batches * S, 6)); norm = np.zeros(num_batches * S)
+        summ = np.zeros((S, 8)); lin = np.zeros(1)
+        labels = "\n".join(l for l, _, _ in strategies).encode()
+        self._check(self.lib.ref_compare_strategies(
+            R, E, values.reshape(-1), S, labels, np.concatenate(flat).astype(np.uint32),
+            np.concatenate(sizes).astype(np.uint32), D, routed, roff, rflat, t, g2n,
+            _c(cost, np.float64), num_batches, batch_size, seed, sims.reshape(-1), norm,
+            summ.reshape(-1), lin))
+        return sims, norm, summ, float(lin[0])
 
     def bench_compare(self, config_path, reps):
         sec = np.zeros(1)

@@ -476,4 +476,72 @@ int ref_bench_parse(const char *trace_path, std::uint32_t E, std::uint32_t top_k
     });
 }
 
+// compare_strategies (simulator.cpp:122-243) on caller-given inputs: the
+// decode matrix [R x E] (integer counts as double), S strategies (labels
+// newline-separated, groups of strategy s at groups_flat[s], sizes in
+// group_sizes[s*D..], cluster_routed[s]) and per-row routing group sets
+// (route_off[R+1] into route_flat). Outputs: sims[B*S][6] (inter, intra,
+// dispatch, compute, combine, layer), normalized[B*S], summary[S][8]
+// (median / q25 / q75 inter bytes, normalized median, median dispatch /
+// compute / combine / layer time) and the linear median.
+int ref_compare_strategies(std::uint64_t R, std::uint32_t E, const double *values,
+                           std::uint32_t S, const char *labels, const std::uint32_t *groups_flat,
+                           const std::uint32_t *group_sizes, std::uint32_t D,
+                           const std::int32_t *cluster_routed, const std::uint64_t *route_off,
+                           const std::uint32_t *route_flat, const std::uint32_t *topo,
+                           const std::uint32_t *g2n, const double *cost, std::uint32_t B,
+                           std::uint32_t batch_size, std::uint64_t seed, double *sims,
+                           double *normalized, double *summary, double *linear_median) {
+    return guarded([&] {
+        ActivationMatrix m;
+        m.rows = R;
+        m.cols = E;
+        m.values.assign(values, values + R * E);
+        m.row_labels.assign(R, "x");
+        for (std::uint64_t r = 0; r < R; ++r) m.request_ids.push_back(r);
+        std::vector<StrategyEntry> strategies(S);
+        std::string all(labels);
+        std::size_t pos = 0, off = 0;
+        for (std::uint32_t s = 0; s < S; ++s) {
+            const std::size_t nl = all.find('\n', pos);
+            strategies[s].label = all.substr(pos, nl == std::string::npos ? std::string::npos : nl - pos);
+            pos = nl == std::string::npos ? all.size() : nl + 1;
+            std::uint32_t n = 0;
+            for (std::uint32_t d = 0; d < D; ++d) n += group_sizes[s * D + d];
+            strategies[s].placement = make_placement(groups_flat + off, group_sizes + s * D, D, E);
+            strategies[s].cluster_routed = cluster_routed[s] != 0;
+            off += n;
+        }
+        std::vector<std::vector<std::uint32_t>> routes(R);
+        for (std::uint64_t r = 0; r < R; ++r)
+            routes[r].assign(route_flat + route_off[r], route_flat + route_off[r + 1]);
+        auto table = compare_strategies(m, strategies, routes, make_topology(topo, g2n),
+                                        make_cost(cost), B, batch_size, seed);
+        for (std::size_t i = 0; i < table.rows.size(); ++i) {
+            const auto &sim = table.rows[i].sim;
+            double *o = sims + 6 * i;
+            o[0] = sim.inter_node_bytes;
+            o[1] = sim.intra_node_bytes;
+            o[2] = sim.dispatch_time;
+            o[3] = sim.expert_compute_time;
+            o[4] = sim.combine_time;
+            o[5] = sim.layer_time;
+            normalized[i] = table.rows[i].normalized;
+        }
+        for (std::size_t s = 0; s < table.summary.size(); ++s) {
+            const auto &x = table.summary[s];
+            double *o = summary + 8 * s;
+            o[0] = x.median_inter_node_bytes;
+            o[1] = x.q25_inter_node_bytes;
+            o[2] = x.q75_inter_node_bytes;
+            o[3] = x.normalized_median;
+            o[4] = x.median_dispatch_time;
+            o[5] = x.median_expert_compute_time;
+            o[6] = x.median_combine_time;
+            o[7] = x.median_layer_time;
+        }
+        *linear_median = table.linear_median_bytes;
+    });
+}
+
 } // extern "C"

@@ -49,7 +49,7 @@ _SIGS = {
     "mpb_router_topk": (C.c_int, [_p, _p, _p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32,
                                   C.c_int, C.c_int, _p, _p, _p]),
     "mpb_router_topk_layers": (C.c_int, [_p, C.c_uint32, _p, _p, C.c_uint64, C.c_uint32, C.c_uint32,
-                                         C.c_uint32, C.c_int, C.c_int, _p, _p]),
+                                         C.c_uint32, C.c_int, C.c_int, _p, _p, _p]),
     "mpb_topk_logits": (C.c_int, [_p, _p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_int, C.c_int,
                                   _p, _p]),
     "mpb_dispatch_layout": (C.c_int, [_p, C.POINTER(MpbTokens), _p, _p, _p, _p, _p, _p, _p]),

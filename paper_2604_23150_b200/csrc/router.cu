@@ -402,7 +402,7 @@ __global__ void __launch_bounds__(kThreadsR, 1)
                 ti[j] = j < off ? -1 : 0x7FFFFFFF;
             }
             float m = -INFINITY;
-            float *lrow = (p.logits && row < p.T) ? p.logits + row * p.E : nullptr;
+            float *lrow = (p.logits && row < p.T) ? p.logits + out_row * p.E : nullptr;
 #pragma unroll 1
             for (int c = half * NH; c < (half + 1) * NH; c += 16) {
                 uint32_t r[16];
@@ -760,7 +760,7 @@ extern "C" mpb_status mpb_router_topk(mpb_context *ctx, const void *X, const voi
 extern "C" mpb_status mpb_router_topk_layers(mpb_context *ctx, uint32_t layers, const void *const *X,
                                              const void *const *W, uint64_t T, uint32_t H, uint32_t E,
                                              uint32_t k, int score_fn, int renorm, int32_t *idx,
-                                             float *weights) {
+                                             float *weights, float *logits_out) {
     if (!ctx || (layers && T && (!X || !W || !idx || !weights)))
         return fail(MPB_VALIDATION_ERROR, "mpb_router_topk_layers: NULL argument");
     if (mpb_status st = router_check("mpb_router_topk_layers", T, H, E, k, score_fn)) return st;
@@ -807,7 +807,7 @@ extern "C" mpb_status mpb_router_topk_layers(mpb_context *ctx, uint32_t layers, 
         }
         it = ctx->router_maps.emplace(std::move(key), d).first;
     }
-    RouterParams p{T, H, k, score_fn, renorm, 0, idx, weights, nullptr, 1, nullptr, nullptr, E,
+    RouterParams p{T, H, k, score_fn, renorm, 0, idx, weights, logits_out, 1, nullptr, nullptr, E,
                    static_cast<const CUtensorMap *>(it->second), 0, layers};
     CUtensorMap unused{};
     return router_dispatch(ctx, N, pair, unused, unused, p);

@@ -379,9 +379,10 @@ class Engine:
         return (idx, w, logits) if want_logits else (idx, w)
 
     def router_topk_layers(self, Xs, Ws, k: int, score_fn: int = 0, renorm: bool = False,
-                           out=None):
+                           out=None, logits_out: Optional[torch.Tensor] = None):
         """Router + top-k of several layers (same T, H, E) in one launch
-        (mpb_router_topk_layers). Returns idx [L,T,k] i32 and w [L,T,k] f32."""
+        (mpb_router_topk_layers). Returns idx [L,T,k] i32 and w [L,T,k] f32;
+        logits_out ([L,T,E] f32, optional) receives the logits the top-k saw."""
         L = len(Xs)
         assert len(Ws) == L and L > 0
         T, H = Xs[0].shape
@@ -396,8 +397,11 @@ class Engine:
             assert idx.is_contiguous() and w.is_contiguous() and idx.numel() == L * T * k
         xp = (C.c_void_p * L)(*[X.data_ptr() for X in Xs])
         wp = (C.c_void_p * L)(*[W.data_ptr() for W in Ws])
+        if logits_out is not None:
+            assert logits_out.is_contiguous() and logits_out.numel() == L * T * E
+            assert logits_out.dtype == torch.float32
         _abi.call("mpb_router_topk_layers", self.ctx, L, xp, wp, T, H, E, k, score_fn,
-                  int(renorm), _ptr(idx), _ptr(w))
+                  int(renorm), _ptr(idx), _ptr(w), _ptr(logits_out))
         return idx, w
 
     # --- layout ---------------------------------------------------------

@@ -654,9 +654,63 @@ class RoutingPipeline:
         return [a.elapsed_time(b) for a, b in self.graph_events]
 
     # ---------------------------------------------------------------- results
+    @property
+    def sim_layer(self) -> int:
+        """The layer the reference statistic is computed on (the paper reports
+        DeepSeek-V3 layer 42); the last layer when the
+        schedule keeps only the last layer's routing."""
+        L = self.spec.layers
+        return min(42, L - 1) if self.side_mode == 3 else L - 1
+
+    def reference_statistic(self, group=None, num_batches: int = 200, batch_size: int = 128,
+                            seed: int = 3):
+        """The reference's a2a-bytes-saved statistic on this step's routing:
+        compare_strategies (simulator.cpp:122-243) — B Monte-Carlo batches of
+        S requests sampled from the decode matrix of ONE layer, linear / EPLB
+        on the batch-position rule, data_based cluster-routed, normalised by the
+        linear median — fully on the device (mp.compare_strategies). The decode
+        matrix [requests x E] is the request-tag histogram of the measured
+        layer's top-k (all ranks' requests, gathered); a request's routing set
+        is its domain's cluster route. Returns the table and its inputs (the
+        parity test replays them through the compiled reference)."""
+        s, eng = self.spec, self.eng
+        dev = eng.device
+        E, l = s.experts, self.sim_layer
+        idx = self.idx_buf[l] if self.side_mode == 3 else self.idx
+        tok_req = np.arange(s.tokens) // s.tokens_per_request
+        req_mat = torch.zeros(self.R, E, dtype=torch.uint64, device=dev)
+        eng.dispatch_layout(idx, self.dp_deployed, src=self.src_cl,
+                            tag=torch.from_numpy(tok_req.astype(np.uint16)).to(dev),
+                            n_tags=self.R, permutation=False, tag_pop=req_mat)
+        dom = torch.from_numpy(self.h_dom[::s.tokens_per_request][:self.R].astype(np.int64)).to(dev)
+        if self.world > 1:
+            import torch.distributed as dist
+            mats = [torch.empty_like(req_mat) for _ in range(self.world)]
+            doms = [torch.empty_like(dom) for _ in range(self.world)]
+            dist.all_gather([m.view(torch.int64) for m in mats], req_mat.view(torch.int64),
+                            group=group)
+            dist.all_gather(doms, dom, group=group)
+            req_mat, dom = torch.cat(mats), torch.cat(doms)
+        eng.sync()
+        counts = req_mat.cpu().numpy().astype(np.float64)
+        dom = dom.cpu().numpy()
+        R = counts.shape[0]
+        matrix = mp.ActivationMatrix(R, E, counts, [f"domain{d}" for d in dom], list(range(R)))
+        routes = [list(self.calib.domain_route[d]) for d in dom]
+        table = mp.compare_strategies(matrix, self.calib.strategies, routes, self.topology,
+                                      self.cost, num_batches, batch_size, seed, engine=eng)
+        summ = {x.strategy: x for x in table.summary}
+        return dict(layer=l, table=table, matrix=matrix, routes=routes,
+                    strategies=self.calib.strategies, num_batches=num_batches,
+                    batch_size=batch_size, seed=seed,
+                    a2a_bytes_saved_pct=100.0 * (1.0 - summ["data_based"].normalized_median),
+                    normalized={k: v.normalized_median for k, v in summ.items()})
+
     def results(self):
-        """Per-layer LayerSims of the named strategies and the search winner;
-        bytes saved = 1 - median_l(data_based inter)/median_l(linear inter)."""
+        """Per-layer LayerSims of the named strategies and the search winner
+        over the step's full per-layer batches (NOT the reference statistic —
+        that is reference_statistic()): per_layer_median_bytes_saved_pct =
+        1 - median_l(data_based inter) / median_l(linear inter)."""
         s = self.spec
         L = s.layers
         rr = self.fin_rr[0].view(2, L, 6).cpu().numpy()
@@ -671,7 +725,7 @@ class RoutingPipeline:
             linear=1.0, eplb=norm(eplb), data_based=norm(db), searched=norm(searched),
             best_candidate=float(cand_med[best] / lin_med) if lin_med > 0 else float("nan")),
             best_candidate_index=best,
-            a2a_bytes_saved_pct=100.0 * (1.0 - norm(db)),
+            per_layer_median_bytes_saved_pct=100.0 * (1.0 - norm(db)),
             searched_bytes_saved_pct=100.0 * (1.0 - norm(searched)))
 
 

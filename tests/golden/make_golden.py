@@ -143,7 +143,7 @@ def main():
     R.analysis(OUT / "trace_analysis.jsonl", 64, 2, 3, OUT / "analysis.json")
 
     # ---- compare_strategies scenarios ----
-    for name in ("qwen3_c1", "desk_default"):
+    for name in ("qwen3_c1", "desk_default", "dsv3_c2"):
         R.compare_scenario(ROOT / "configs" / f"{name}.json", OUT / f"compare_{name}.json")
 
     # ---- metrics ----

@@ -128,7 +128,7 @@ def test_simulate_tokens_uncovered_and_range_errors(eng):
     assert sim.intra_node_bytes == 7168.0
 
 
-@pytest.mark.parametrize("name", ["qwen3_c1", "desk_default"])
+@pytest.mark.parametrize("name", ["qwen3_c1", "desk_default", "dsv3_c2"])
 def test_compare_strategies_golden_bit_exact(eng, golden, name):
     sc = json.loads((golden / f"compare_{name}.json").read_text())
     dm = sc["decode_matrix"]

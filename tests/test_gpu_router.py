@@ -204,15 +204,15 @@ def test_router_topk_layers_errors(eng):
     wp = (C.c_void_p * 2)(Ws[0].data_ptr(), Ws[1].data_ptr())
     with pytest.raises(ValidationError):
         _abi.call("mpb_router_topk_layers", eng.ctx, 2, xp, wp, T, H, E, k, 0, 0,
-                  C.c_void_p(idx.data_ptr()), C.c_void_p(w.data_ptr()))
+                  C.c_void_p(idx.data_ptr()), C.c_void_p(w.data_ptr()), None)
     xp = (C.c_void_p * 2)(Xs[0].data_ptr() + 2, Xs[1].data_ptr())
     with pytest.raises(ConfigError):
         _abi.call("mpb_router_topk_layers", eng.ctx, 2, xp, wp, T, H, E, k, 0, 0,
-                  C.c_void_p(idx.data_ptr()), C.c_void_p(w.data_ptr()))
+                  C.c_void_p(idx.data_ptr()), C.c_void_p(w.data_ptr()), None)
     with pytest.raises(ConfigError):  # H not a multiple of 64
         _abi.call("mpb_router_topk_layers", eng.ctx, 2, xp, wp, T, H - 32, E, k, 0, 0,
-                  C.c_void_p(idx.data_ptr()), C.c_void_p(w.data_ptr()))
-    _abi.call("mpb_router_topk_layers", eng.ctx, 0, None, None, T, H, E, k, 0, 0, None, None)
+                  C.c_void_p(idx.data_ptr()), C.c_void_p(w.data_ptr()), None)
+    _abi.call("mpb_router_topk_layers", eng.ctx, 0, None, None, T, H, E, k, 0, 0, None, None, None)
     a = eng.router_topk_layers(Xs, Ws, k, 0, False)
     b = eng.router_topk_layers(Xs[::-1], Ws[::-1], k, 0, False)
     c = eng.router_topk_layers(Xs, Ws, k, 0, False)

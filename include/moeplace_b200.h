@@ -347,10 +347,13 @@ MPB_API mpb_status mpb_aggregate_usage(const uint32_t *labels /* rows */, const 
                                        uint32_t D, double *usage_out /* D*E */);
 MPB_API mpb_status mpb_l2_normalize_rows(const double *matrix, uint64_t rows, uint32_t cols,
                                          double *out);
+/* objective_history (nullable, capacity max_iterations): the objective after
+ * each Lloyd iteration (ClusterModel::objective_history, clustering.cpp:207). */
 MPB_API mpb_status mpb_kmeans(const double *rows, uint64_t n, uint32_t dim, uint32_t K,
                               uint64_t seed, uint32_t max_iterations, double tolerance,
                               uint32_t *labels_out /* n */, double *centroids_out /* K*dim */,
-                              double *objective_out, uint32_t *iterations_out);
+                              double *objective_out, uint32_t *iterations_out,
+                              double *objective_history /* host */);
 /* Device k-means (K7): same algorithm, order of operations and RNG draws as
  * kmeans / l2_normalize_rows (clustering.cpp:15-230) — bit-identical labels,
  * centroids and objective — on caller-owned device buffers, in ctx's stream
@@ -363,12 +366,34 @@ MPB_API mpb_status mpb_kmeans_device(mpb_context *ctx, const double *rows /* dev
                                      uint32_t max_iterations, double tolerance,
                                      uint32_t *labels /* dev n */, double *centroids /* dev K*dim */,
                                      double *objective_out /* host */,
-                                     uint32_t *iterations_out /* host */);
+                                     uint32_t *iterations_out /* host */,
+                                     double *objective_history /* host, nullable */);
+/* Placement::verify (placement.cpp:35-56): exact group sizes M, no expert
+ * twice within a group, ids < E, every expert placed -> MPB_VALIDATION_ERROR. */
+MPB_API mpb_status mpb_placement_verify(const uint32_t *groups_flat, const uint32_t *group_sizes,
+                                        uint32_t D, uint32_t E, uint32_t M);
 MPB_API mpb_status mpb_assign_clusters_to_groups(const uint32_t *labels, uint64_t n, uint32_t K,
                                                  const double *raw, uint32_t dim, uint32_t D,
                                                  uint64_t seed, uint32_t *assign_flat /* <= K*D */,
                                                  uint32_t *assign_sizes /* K */,
                                                  double *cluster_sizes_out /* K */);
+
+/* ---- characterisation metrics (metrics.cpp:11-132) -------------------------
+ * mpb_label_row_sums: sums[l][c] = sum of matrix[r][c] over rows r with
+ * labels[r] == l (labels NULL: one label, all rows) — the per-dataset
+ * popularity vectors and the all-row sums of the prefill->decode correlation
+ * (metrics.cpp:72-91), as exact uint64 histograms on the device (matrix, labels,
+ * sums device; sums overwritten; synchronous). Entries must be non-negative
+ * integers < 2^53 — then every sequential double sum of the reference is exact
+ * and equals these — else MPB_VALIDATION_ERROR.
+ * mpb_expert_load / mpb_pearson: host finalisation in the reference's order
+ * (metrics.cpp:11-34, 42-68), same errors. */
+MPB_API mpb_status mpb_label_row_sums(mpb_context *ctx, const double *matrix, uint64_t rows,
+                                      uint32_t cols, const uint32_t *labels, uint32_t n_labels,
+                                      uint64_t *sums);
+MPB_API mpb_status mpb_expert_load(const double *counts, uint32_t E, uint32_t top_k,
+                                   double *loads, uint64_t *total_tokens);
+MPB_API mpb_status mpb_pearson(const double *x, const double *y, uint64_t n, double *r);
 
 /* ---- host trace model (no device needed) -----------------------------------
  * trace.cpp:73-297: JSONL loader / writer (byte-identical to the reference's
@@ -386,6 +411,19 @@ MPB_API mpb_status mpb_trace_generate(uint32_t num_domains, uint32_t requests_pe
                                       double decode_tokens_mean, uint64_t seed, uint32_t E,
                                       uint32_t top_k, uint32_t layers, int keep_picks,
                                       mpb_trace **out);
+/* write_trace (trace.cpp:117-131) into buf: *len = bytes of the JSONL text,
+ * copied when buf != NULL and cap >= *len. */
+MPB_API mpb_status mpb_trace_dump(const mpb_trace *t, char *buf, uint64_t cap, uint64_t *len);
+/* A trace from caller records (inverse of mpb_trace_export; pairs of record i
+ * in [pair_offset[i], pair_offset[i+1]), ascending expert ids, label index into
+ * labels[n_labels]). Used by the C++ drop-in to hand std::vector<ActivationRecord>
+ * to the builders and the writer. */
+MPB_API mpb_status mpb_trace_import(uint64_t n_records, const uint64_t *request_id,
+                                    const uint32_t *layer, const uint8_t *stage,
+                                    const uint64_t *input_len, const uint64_t *gen_tokens,
+                                    const uint32_t *label, const uint64_t *pair_offset,
+                                    const uint32_t *expert, const uint64_t *count,
+                                    uint64_t n_labels, const char *const *labels, mpb_trace **out);
 MPB_API mpb_status mpb_trace_destroy(mpb_trace *t);
 MPB_API mpb_status mpb_trace_sizes(const mpb_trace *t, uint64_t *n_records, uint64_t *n_pairs,
                                    uint64_t *n_labels, uint64_t *n_picks);

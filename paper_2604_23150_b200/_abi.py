@@ -92,10 +92,11 @@ _SIGS = {
                                       C.c_uint32, _p]),
     "mpb_l2_normalize_rows": (C.c_int, [_p, C.c_uint64, C.c_uint32, _p]),
     "mpb_kmeans": (C.c_int, [_p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint32,
-                             C.c_double, _p, _p, _p, _p]),
+                             C.c_double, _p, _p, _p, _p, _p]),
+    "mpb_placement_verify": (C.c_int, [_p, _p, C.c_uint32, C.c_uint32, C.c_uint32]),
     "mpb_l2_normalize_rows_device": (C.c_int, [_p, _p, C.c_uint64, C.c_uint32, _p]),
     "mpb_kmeans_device": (C.c_int, [_p, _p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint64,
-                                    C.c_uint32, C.c_double, _p, _p, _p, _p]),
+                                    C.c_uint32, C.c_double, _p, _p, _p, _p, _p]),
     "mpb_assign_clusters_to_groups": (C.c_int, [_p, C.c_uint64, C.c_uint32, _p, C.c_uint32,
                                                 C.c_uint32, C.c_uint64, _p, _p, _p]),
     "mpb_trace_parse": (C.c_int, [C.c_char_p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32,
@@ -107,6 +108,12 @@ _SIGS = {
                                      C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, C.c_int,
                                      C.POINTER(_p)]),
     "mpb_trace_destroy": (C.c_int, [_p]),
+    "mpb_trace_dump": (C.c_int, [_p, _p, C.c_uint64, _p]),
+    "mpb_trace_import": (C.c_int, [C.c_uint64, _p, _p, _p, _p, _p, _p, _p, _p, _p, C.c_uint64,
+                                   _p, _p]),
+    "mpb_label_row_sums": (C.c_int, [_p, _p, C.c_uint64, C.c_uint32, _p, C.c_uint32, _p]),
+    "mpb_expert_load": (C.c_int, [_p, C.c_uint32, C.c_uint32, _p, _p]),
+    "mpb_pearson": (C.c_int, [_p, _p, C.c_uint64, _p]),
     "mpb_trace_sizes": (C.c_int, [_p, _p, _p, _p, _p]),
     "mpb_trace_export": (C.c_int, [_p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p]),
     "mpb_trace_label": (C.c_char_p, [_p, C.c_uint64]),

@@ -120,7 +120,8 @@ void phase2(Groups &groups, const double *U, uint32_t E, uint32_t M) {
         const size_t need = M - g.size();
         if (!need) continue;
         std::vector<char> in(E, 0);
-        for (uint32_t e : g) in[e] = 1;
+        for (uint32_t e : g)
+            if (e < E) in[e] = 1;  // ids >= E are never candidates anyway
         std::vector<uint32_t> cand;
         for (uint32_t e = 0; e < E; ++e)
             if (!in[e]) cand.push_back(e);
@@ -214,6 +215,7 @@ struct KMeans {
     std::vector<double> centroids;
     double objective = 0.0;
     uint32_t iterations = 0;
+    std::vector<double> history;  // objective after each Lloyd iteration
 };
 
 void assign(const double *X, size_t n, size_t dim, const std::vector<double> &C, uint32_t K,
@@ -321,6 +323,7 @@ KMeans kmeans(const double *X, size_t n, size_t dim, uint32_t K, uint64_t seed, 
         for (uint32_t k = 0; k < K; ++k)
             for (size_t c = 0; c < dim; ++c)
                 m.centroids[size_t(k) * dim + c] = sums[size_t(k) * dim + c] / static_cast<double>(cnt[k]);
+        m.history.push_back(objective(X, n, dim, m.centroids, m.labels));
         double move = 0.0;
         for (uint32_t k = 0; k < K; ++k)
             move = std::max(move, std::sqrt(sqdist(m.centroids.data() + size_t(k) * dim,
@@ -505,13 +508,24 @@ mpb_status mpb_l2_normalize_rows(const double *matrix, uint64_t rows, uint32_t c
 
 mpb_status mpb_kmeans(const double *rows, uint64_t n, uint32_t dim, uint32_t K, uint64_t seed,
                       uint32_t max_iterations, double tolerance, uint32_t *labels_out,
-                      double *centroids_out, double *objective_out, uint32_t *iterations_out) {
+                      double *centroids_out, double *objective_out, uint32_t *iterations_out,
+                      double *objective_history) {
     return guard([&] {
         KMeans m = kmeans(rows, n, dim, K, seed, max_iterations, tolerance);
         std::copy(m.labels.begin(), m.labels.end(), labels_out);
         if (centroids_out) std::copy(m.centroids.begin(), m.centroids.end(), centroids_out);
         if (objective_out) *objective_out = m.objective;
         if (iterations_out) *iterations_out = m.iterations;
+        if (objective_history) std::copy(m.history.begin(), m.history.end(), objective_history);
+    });
+}
+
+mpb_status mpb_placement_verify(const uint32_t *groups_flat, const uint32_t *group_sizes,
+                                uint32_t D, uint32_t E, uint32_t M) {
+    return guard([&] {
+        if (D && (!groups_flat || !group_sizes))
+            raise(MPB_VALIDATION_ERROR, "mpb_placement_verify: NULL argument");
+        verify_placement(D ? read_groups(groups_flat, group_sizes, D) : Groups{}, E, M);
     });
 }
 

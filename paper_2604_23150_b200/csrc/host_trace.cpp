@@ -22,6 +22,7 @@
 #include <cstring>
 #include <fstream>
 #include <map>
+#include <memory>
 #include <random>
 #include <set>
 #include <sstream>
@@ -495,6 +496,57 @@ mpb_status mpb_trace_write_file(const mpb_trace *t, const char *path) {
     const std::string s = dump(*t);
     out.write(s.data(), static_cast<std::streamsize>(s.size()));
     return MPB_OK;
+}
+
+// write_trace into a caller buffer: *len = bytes of the JSONL text; the text
+// is copied only when buf != NULL and cap >= *len.
+mpb_status mpb_trace_dump(const mpb_trace *t, char *buf, uint64_t cap, uint64_t *len) {
+    if (!t || !len) return fail(MPB_VALIDATION_ERROR, "mpb_trace_dump: NULL argument");
+    const std::string s = dump(*t);
+    *len = s.size();
+    if (buf && cap >= s.size()) std::memcpy(buf, s.data(), s.size());
+    return MPB_OK;
+}
+
+// A trace from caller records (the inverse of mpb_trace_export): record i has
+// pairs [pair_offset[i], pair_offset[i+1]) with strictly ascending expert ids
+// and label labels[label[i]]. Records are taken as they are (the reference
+// validates only while parsing / generating); the matrix builder checks
+// expert ids against its E like build_activation_matrix.
+mpb_status mpb_trace_import(uint64_t n_records, const uint64_t *request_id, const uint32_t *layer,
+                            const uint8_t *stage, const uint64_t *input_len,
+                            const uint64_t *gen_tokens, const uint32_t *label,
+                            const uint64_t *pair_offset, const uint32_t *expert,
+                            const uint64_t *count, uint64_t n_labels, const char *const *labels,
+                            mpb_trace **out) {
+    if (!out) return fail(MPB_VALIDATION_ERROR, "mpb_trace_import: out is NULL");
+    *out = nullptr;
+    if (n_records && (!request_id || !layer || !stage || !input_len || !gen_tokens || !label ||
+                      !pair_offset))
+        return fail(MPB_VALIDATION_ERROR, "mpb_trace_import: NULL record array");
+    if (n_labels && !labels) return fail(MPB_VALIDATION_ERROR, "mpb_trace_import: NULL labels");
+    return tguard([&] {
+        auto t = std::make_unique<mpb_trace>();
+        std::vector<uint32_t> remap(n_labels);
+        for (uint64_t i = 0; i < n_labels; ++i) remap[i] = t->label(labels[i] ? labels[i] : "");
+        t->records.resize(n_records);
+        for (uint64_t i = 0; i < n_records; ++i) {
+            auto &r = t->records[i];
+            r.request_id = request_id[i];
+            r.layer = layer[i];
+            r.stage = stage[i] ? 1 : 0;
+            r.input_len = input_len[i];
+            r.gen_tokens = gen_tokens[i];
+            if (label[i] >= n_labels) bad(MPB_VALIDATION_ERROR, "mpb_trace_import: label index out of range");
+            r.label = remap[label[i]];
+            const uint64_t a = pair_offset[i], b = pair_offset[i + 1];
+            if (b < a || (b > a && (!expert || !count)))
+                bad(MPB_VALIDATION_ERROR, "mpb_trace_import: bad pair offsets");
+            r.experts.reserve(b - a);
+            for (uint64_t j = a; j < b; ++j) r.experts.emplace_back(expert[j], count[j]);
+        }
+        *out = t.release();
+    });
 }
 
 mpb_status mpb_trace_destroy(mpb_trace *t) {

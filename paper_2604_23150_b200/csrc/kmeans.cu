@@ -379,7 +379,7 @@ mpb_status mpb_l2_normalize_rows_device(mpb_context *ctx, const double *matrix, 
 mpb_status mpb_kmeans_device(mpb_context *ctx, const double *X, uint64_t n, uint32_t dim,
                              uint32_t K, uint64_t seed, uint32_t max_iterations, double tolerance,
                              uint32_t *labels, double *centroids, double *objective_out,
-                             uint32_t *iterations_out) {
+                             uint32_t *iterations_out, double *objective_history) {
     if (!ctx || !X || !labels || !centroids)
         return fail(MPB_VALIDATION_ERROR, "mpb_kmeans_device: NULL argument");
     if (K < 1) return fail(MPB_INFEASIBLE_ERROR, "kmeans: K must be >= 1");
@@ -475,8 +475,16 @@ mpb_status mpb_kmeans_device(mpb_context *ctx, const double *X, uint64_t n, uint
         MPB_LAUNCHED(ctx);
         k_movement<<<1, 32, 0, st>>>(centroids, sc.prev, K, dim, sc.d_small + 1);
         MPB_LAUNCHED(ctx);
-        MPB_CUDA(cudaMemcpyAsync(sc.h_d + 1, sc.d_small + 1, 8, cudaMemcpyDeviceToHost, st));
+        if (objective_history) {  // objective_value after the update (clustering.cpp:207-208)
+            k_label_dist<<<rb, 128, csmem, st>>>(X, n, dim, centroids, K, labels, sc.dist);
+            MPB_LAUNCHED(ctx);
+            k_seq_scan<<<1, 256, 0, st>>>(sc.dist, n, -1.0, sc.d_small + 2, sc.d_pick);
+            MPB_LAUNCHED(ctx);
+        }
+        MPB_CUDA(cudaMemcpyAsync(sc.h_d + 1, sc.d_small + 1, objective_history ? 16 : 8,
+                                 cudaMemcpyDeviceToHost, st));
         MPB_CUDA(cudaStreamSynchronize(st));
+        if (objective_history) objective_history[it] = sc.h_d[2];
         if (trace) {
             auto t2 = std::chrono::steady_clock::now();
             std::fprintf(stderr, "[kmeans] it %u assign %.1f us update %.1f us move %.3g\n", it,

@@ -43,6 +43,7 @@ class ClusterModel:
     dim: int
     objective: float
     iterations_run: int
+    objective_history: list = field(default_factory=list)
 
 
 @dataclass
@@ -161,10 +162,11 @@ def kmeans(rows, n_rows: int, dim: int, K: int, seed: int, max_iterations: int =
     cent = np.zeros(max(1, K * dim), np.float64)
     obj = np.zeros(1)
     it = np.zeros(1, np.uint32)
+    hist = np.zeros(max(1, max_iterations))
     _abi.call("mpb_kmeans", _p(x), n_rows, dim, K, seed, max_iterations, tolerance, _p(labels),
-              _p(cent), _p(obj), _p(it))
+              _p(cent), _p(obj), _p(it), _p(hist))
     return ClusterModel(K, labels[:n_rows], cent[: K * dim].reshape(K, dim), dim, float(obj[0]),
-                        int(it[0]))
+                        int(it[0]), hist[:int(it[0])].tolist())
 
 
 def kmeans_device(engine, rows, n_rows: int, dim: int, K: int, seed: int,
@@ -182,7 +184,7 @@ def kmeans_device(engine, rows, n_rows: int, dim: int, K: int, seed: int,
     it = np.zeros(1, np.uint32)
     _abi.call("mpb_kmeans_device", engine.ctx, C.c_void_p(x.data_ptr()), n_rows, dim, K, seed,
               max_iterations, tolerance, C.c_void_p(labels.data_ptr()),
-              C.c_void_p(cent.data_ptr()), _p(obj), _p(it))
+              C.c_void_p(cent.data_ptr()), _p(obj), _p(it), None)
     return ClusterModel(K, labels[:n_rows].cpu().numpy().astype(np.uint32),
                         cent[: K * dim].cpu().numpy().reshape(K, dim), dim, float(obj[0]),
                         int(it[0]))

@@ -33,75 +33,12 @@
 #include "moeplace/simulator.hpp"
 #include "moeplace/stats.hpp"
 #include "moeplace_b200.h"
+#include "shim_common.hpp"
 
 namespace moeplace {
 namespace {
 
-[[noreturn]] void throw_status(mpb_status s, const std::string &what) {
-    switch (s) {
-    case MPB_PARSE_ERROR: throw ParseError(0, what);
-    case MPB_VALIDATION_ERROR: throw ValidationError(what);
-    case MPB_CONFIG_ERROR: throw ConfigError(what);
-    case MPB_EMPTY_SELECTION_ERROR: throw EmptySelectionError(what);
-    case MPB_UNDEFINED_CORRELATION_ERROR: throw UndefinedCorrelationError(what);
-    case MPB_INFEASIBLE_ERROR: throw InfeasibleError(what);
-    case MPB_LOOKUP_ERROR: throw LookupError(what);
-    default: throw Error(what);
-    }
-}
-
-void check(mpb_status s) {
-    if (s != MPB_OK) throw_status(s, mpb_last_error_message());
-}
-
-void check_cuda(cudaError_t e, const char *where) {
-    if (e != cudaSuccess) throw Error(std::string(where) + ": " + cudaGetErrorString(e));
-}
-
-// Process-wide device context + grow-only device buffers.
-struct Device {
-    mpb_context *ctx = nullptr;
-    std::vector<void *> bufs;
-    std::vector<size_t> sizes;
-    std::mutex mu;
-
-    Device() { check(mpb_context_create(0, nullptr, &ctx)); }
-    ~Device() {
-        for (void *p : bufs) cudaFree(p);
-        mpb_context_destroy(ctx);
-    }
-    void *buf(size_t slot, size_t bytes) {
-        if (bufs.size() <= slot) {
-            bufs.resize(slot + 1, nullptr);
-            sizes.resize(slot + 1, 0);
-        }
-        bytes = std::max<size_t>(bytes, 64);
-        if (sizes[slot] < bytes) {
-            if (bufs[slot]) cudaFree(bufs[slot]);
-            check_cuda(cudaMalloc(&bufs[slot], bytes), "cudaMalloc");
-            sizes[slot] = bytes;
-        }
-        return bufs[slot];
-    }
-    template <typename T> T *up(size_t slot, const std::vector<T> &h) {
-        auto *d = static_cast<T *>(buf(slot, h.size() * sizeof(T)));
-        if (!h.empty())
-            check_cuda(cudaMemcpy(d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice), "H2D");
-        return d;
-    }
-    template <typename T> void down(std::vector<T> &h, const void *d) {
-        if (!h.empty())
-            check_cuda(cudaMemcpy(h.data(), d, h.size() * sizeof(T), cudaMemcpyDeviceToHost), "D2H");
-    }
-};
-
-Device &device() {
-    static Device d;
-    return d;
-}
-
-enum Slot : size_t { kRowPtr, kCols, kVals, kRows, kPicks, kSrc, kG2n, kLuts, kDemand, kInter,
-                     kIntra, kRank, kOut, kPayload, kSetSize, kSetOff, kGroups, kRowNode };
+using namespace b200;
 
 std::vector<uint8_t> dest_lut(const Placement &p, const Topology &t, uint32_t nodes) {
     const uint32_t D = p.D();
@@ -238,7 +175,7 @@ LayerSim simulate_layer(const BatchAssignment &batch, const Placement &placement
     }
     const uint32_t nodes = node_count(topology, D), E = placement.E;
     Device &dev = device();
-    std::lock_guard<std::mutex> lock(dev.mu);
+    std::lock_guard<std::recursive_mutex> lock(dev.mu);
     std::vector<uint8_t> g2n(D);
     for (uint32_t d = 0; d < D; ++d) g2n[d] = static_cast<uint8_t>(topology.group_to_node[d]);
     auto *d_demand = static_cast<uint64_t *>(dev.buf(kDemand, size_t(nodes) * E * 8));
@@ -311,7 +248,7 @@ ComparisonTable compare_strategies(const ActivationMatrix &decode_matrix,
     }
     const uint32_t nodes = node_count(topology, D);
     Device &dev = device();
-    std::lock_guard<std::mutex> lock(dev.mu);
+    std::lock_guard<std::recursive_mutex> lock(dev.mu);
     const size_t BS = size_t(num_batches) * batch_size;
     auto *d_rows = static_cast<uint32_t *>(dev.buf(kRows, BS * 4));
     auto *d_picks = static_cast<uint32_t *>(dev.buf(kPicks, BS * 4));

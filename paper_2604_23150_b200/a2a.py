@@ -184,6 +184,13 @@ class ExpertParallelA2A:
                 stats.inter_node_rows += int(c)
 
     def _p2p(self, X, idx, w, n, k, stats):
+        # the symmetric-memory barrier and the x_sym staging copy are issued on
+        # torch's current stream; run them on the engine's stream so the
+        # barrier orders the P2P kernels (which the engine launches there)
+        with torch.cuda.stream(self.eng.stream):
+            return self._p2p_body(X, idx, w, n, k, stats)
+
+    def _p2p_body(self, X, idx, w, n, k, stats):
         eng = self.eng
         span = groups_per_rank(self.D, self.world) * self.E
         if stats is not None:

@@ -40,19 +40,32 @@ mpb_status cuda_fail(cudaError_t err, const char *where) {
 
 }  // namespace mpb
 
-cudaError_t mpb_context::ensure_scratch(size_t bytes) {
-    if (bytes <= scratch_bytes) return cudaSuccess;
-    if (scratch) {
-        cudaError_t e = cudaStreamSynchronize(stream);
-        if (e != cudaSuccess) return e;
-        cudaFree(scratch);
-        scratch = nullptr;
-        scratch_bytes = 0;
+cudaError_t mpb_context::grow(void **buf, size_t *bytes, size_t need, size_t min_bytes,
+                              size_t zero_bytes) {
+    if (need <= *bytes) return cudaSuccess;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaError_t e = cudaStreamIsCapturing(stream, &cs);
+    if (e != cudaSuccess) return e;
+    if (cs != cudaStreamCaptureStatusNone) return cudaErrorStreamCaptureUnsupported;
+    void *p = nullptr;
+    const size_t want = std::max(need, min_bytes);
+    e = cudaMalloc(&p, want);
+    if (e != cudaSuccess) return e;
+    if (zero_bytes) {
+        e = cudaMemsetAsync(p, 0, std::min(zero_bytes, want), stream);
+        if (e != cudaSuccess) {
+            cudaFree(p);
+            return e;
+        }
     }
-    size_t want = std::max<size_t>(bytes, 1 << 20);
-    cudaError_t e = cudaMalloc(&scratch, want);
-    if (e == cudaSuccess) scratch_bytes = want;
-    return e;
+    if (*buf) retired.push_back(*buf);
+    *buf = p;
+    *bytes = want;
+    return cudaSuccess;
+}
+
+cudaError_t mpb_context::ensure_scratch(size_t need) {
+    return grow(&scratch, &scratch_bytes, need, size_t(1) << 20, 0);
 }
 
 using namespace mpb;
@@ -96,6 +109,7 @@ mpb_status mpb_context_destroy(mpb_context *ctx) {
     if (ctx->d_error) cudaFree(ctx->d_error);
     if (ctx->scratch) cudaFree(ctx->scratch);
     if (ctx->router_ws) cudaFree(ctx->router_ws);
+    for (void *p : ctx->retired) cudaFree(p);
     for (auto &kv : ctx->router_maps) cudaFree(kv.second);
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
     delete ctx;

@@ -347,6 +347,7 @@ __global__ void __launch_bounds__(256) k_return_p2p(const uint4 *recv, uint64_t 
     // rotated start: rows of source me+1 first (no single hot destination)
     const uint64_t rot = static_cast<uint64_t>(s_base[(me + 1) % world]) % total;
     const uint64_t row = row0 + rot >= total ? row0 + rot - total : row0 + rot;
+    if (row >= rows) return;  // capacity overflow (dispatch flagged kErrCapacity)
     const uint32_t lane = threadIdx.x & 31;
     uint32_t q = 0;
     while (q + 1 < world && static_cast<int64_t>(row) >= s_base[q + 1]) ++q;

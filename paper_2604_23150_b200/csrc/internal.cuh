@@ -87,6 +87,14 @@ struct mpb_context {
     void *scratch = nullptr;
     size_t scratch_bytes = 0;
     cudaError_t ensure_scratch(size_t bytes);
+    // Grow-only workspace rule (scratch, router_ws): a CUDA graph captured
+    // earlier may still reference the old buffer, so a grown buffer's
+    // predecessor is retired (freed at mpb_context_destroy), never freed in
+    // place; growing while the stream is capturing is refused
+    // (cudaErrorStreamCaptureUnsupported): size the workspaces with one eager
+    // call at the largest shape before capture.
+    std::vector<void *> retired;
+    cudaError_t grow(void **buf, size_t *bytes, size_t need, size_t min_bytes, size_t zero_bytes);
     // router split-K tail: fp32 partial accumulators + per-slot ready flags
     void *router_ws = nullptr;
     size_t router_ws_bytes = 0;

@@ -16,9 +16,9 @@
 //                axis (exclusive, in place) and writes the slot totals.
 //   3. scatter : every block scans the NS slot totals in smem (slot bases; block
 //                0 emits key_offsets), re-reads its chunk (L2-resident), ranks
-//                pairs stably inside each warp (warp-aggregated per-warp
-//                counters, then __match_any_sync + popc of lower lanes) and
-//                writes sorted_pairs / pair_pos.
+//                pairs stably inside each warp (per-warp slot counters; the
+//                rank among lower lanes from per-bit ballots of the slot id,
+//                no MATCH.ANY) and writes sorted_pairs / pair_pos.
 // Algorithmic bytes per pair: 4 (idx) + 8 (perm out) [+ 1/k src + 1/k tag].
 #include <algorithm>
 #include <cstdlib>
@@ -83,13 +83,6 @@ __device__ __forceinline__ void load4(const int32_t *idx, uint64_t q, uint64_t P
 #pragma unroll
         for (int c = 0; c < 4; ++c) v[c] = q + c < P ? __ldg(idx + q + c) : -1;
     }
-}
-
-// Warp-aggregated shared-memory increment: lanes with equal keys elect one
-// leader that adds the group size (kNone keys do not count).
-__device__ __forceinline__ void agg_add(uint32_t *base, uint32_t key) {
-    const unsigned peers = __match_any_sync(0xffffffffu, key);
-    if (key != kNone && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(base + key, __popc(peers));
 }
 
 // Resolves pair (t, e): slot id (kNone if invalid), flags errors.
@@ -508,7 +501,7 @@ __global__ void __launch_bounds__(256) k_layout_derive(const uint64_t *demand, c
             if (!a) continue;
             const uint32_t n = g2n[s];
             const uint32_t d = dest_lut[static_cast<size_t>(n) * E + e];
-            if (d == 255) {
+            if (d >= D) {
                 atomicOr(err, kErrUncovered);
                 continue;
             }

@@ -647,15 +647,7 @@ mpb_status launch_router_n(mpb_context *ctx, const CUtensorMap &mx, const CUtens
         const size_t ranks = PAIR ? 2 : 1;
         const size_t flag_bytes = 4096;
         const size_t need = flag_bytes + size_t(rem) * (S - 1) * ranks * N * kBM * sizeof(float);
-        if (ctx->router_ws_bytes < need) {
-            MPB_CUDA(cudaStreamSynchronize(ctx->stream));
-            if (ctx->router_ws) cudaFree(ctx->router_ws);
-            ctx->router_ws = nullptr;
-            ctx->router_ws_bytes = 0;
-            MPB_CUDA(cudaMalloc(&ctx->router_ws, need));
-            MPB_CUDA(cudaMemset(ctx->router_ws, 0, flag_bytes));
-            ctx->router_ws_bytes = need;
-        }
+        MPB_CUDA(ctx->grow(&ctx->router_ws, &ctx->router_ws_bytes, need, 0, flag_bytes));
         // flags: count of K parts > 0 whose partial is ready (reset by the finisher)
         p.flags = static_cast<uint32_t *>(ctx->router_ws);
         p.partial = reinterpret_cast<float *>(static_cast<char *>(ctx->router_ws) + flag_bytes);
@@ -789,9 +781,8 @@ extern "C" mpb_status mpb_router_topk_layers(mpb_context *ctx, uint32_t layers, 
             return fail(MPB_CONFIG_ERROR,
                         "mpb_router_topk_layers: first call for these buffers inside a stream capture "
                         "(call once before capturing)");
-        if (ctx->router_maps.size() >= 256) {  // bounded: drop the tables once in-flight work is done
-            MPB_CUDA(cudaStreamSynchronize(ctx->stream));
-            for (auto &kv : ctx->router_maps) cudaFree(kv.second);
+        if (ctx->router_maps.size() >= 256) {  // bounded lookup; captured graphs may still read the
+            for (auto &kv : ctx->router_maps) ctx->retired.push_back(kv.second);  // old tables
             ctx->router_maps.clear();
         }
         std::vector<CUtensorMap> maps(2 * static_cast<size_t>(layers));

@@ -27,7 +27,8 @@ __global__ void __launch_bounds__(256) k_batch_demand(const uint32_t *row_ptr, c
                                                       uint32_t S, const uint8_t *g2n, uint32_t D,
                                                       uint32_t nodes, uint32_t E, int use_smem,
                                                       uint64_t *node_demand, uint32_t *err) {
-    extern __shared__ uint32_t s_nd[];  // [nodes*E]
+    // u64 counters: a batch's summed demand for one cell may pass 2^32
+    extern __shared__ unsigned long long s_nd[];  // [nodes*E]
     const uint32_t b = blockIdx.x;
     uint64_t *out = node_demand + static_cast<size_t>(b) * nodes * E;
     if (use_smem) {
@@ -53,7 +54,7 @@ __global__ void __launch_bounds__(256) k_batch_demand(const uint32_t *row_ptr, c
                 continue;
             }
             if (use_smem)
-                atomicAdd(s_nd + n * E + e, vals[z]);
+                atomicAdd(s_nd + n * E + e, static_cast<unsigned long long>(vals[z]));
             else
                 atomicAdd(reinterpret_cast<unsigned long long *>(out) + n * E + e,
                           static_cast<unsigned long long>(vals[z]));
@@ -157,7 +158,7 @@ __global__ void __launch_bounds__(kScoreWarps * 32) k_score(const uint64_t *dema
             const unsigned long long v = s_nd[i];
             const uint32_t d = __ldg(lut + i);
             if (!v) continue;
-            if (d == 255) {
+            if (d >= D) {  // 255 = uncovered; any other out-of-range group too
                 atomicOr(err, kErrUncovered);
                 continue;
             }
@@ -218,7 +219,7 @@ mpb_status mpb_batch_demand(mpb_context *ctx, const uint32_t *row_ptr, const uin
     if (!ctx || !row_ptr || !rows || !src || !group_to_node || !node_demand)
         return fail(MPB_VALIDATION_ERROR, "mpb_batch_demand: NULL argument");
     if (B == 0) return MPB_OK;
-    const size_t smem = size_t(nodes) * E * 4;
+    const size_t smem = size_t(nodes) * E * 8;
     const int use_smem = smem <= 160 * 1024;
     if (use_smem)
         MPB_CUDA(cudaFuncSetAttribute(k_batch_demand, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -385,7 +385,7 @@ class RoutingPipeline:
             if db.R_redundancy:  # replicated experts: the library's holder rule
                 return np.stack([mp.host_dest_lut(mp.Placement(c, E, db.R_redundancy, db.M), g2n)
                                  for c in cands])
-            out = np.empty((len(cands), nodes, E), np.uint8)
+            out = np.full((len(cands), nodes, E), 255, np.uint8)
             for p, c in enumerate(cands):
                 for d, g in enumerate(c):
                     out[p, :, g] = d

@@ -66,12 +66,22 @@ class ClockSampler:
     def __enter__(self):
         fd, self.path = tempfile.mkstemp(suffix=".csv")
         os.close(fd)
+        if os.environ.get("MPB_BENCH_NO_CLOCKS"):  # diagnostics only
+            return self
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.FIELDS}",
                  "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
-            time.sleep(0.3)
+            # wait until nvidia-smi has initialised NVML and written its first
+            # samples: its start-up driver calls stall kernel launches, which
+            # would land inside a short timed region
+            t0 = time.time()
+            while time.time() - t0 < 5.0:
+                time.sleep(0.1)
+                if os.path.getsize(self.path) and open(self.path).read().count("\n") >= 2:
+                    break
+            time.sleep(0.2)
         except FileNotFoundError:
             self.proc = None
         return self
@@ -210,48 +220,49 @@ def run_reference_arm(args, spec):
 
 
 def run_e2e(pipe, steps: int):
-    """Same step with per-layer hidden states from pinned host memory."""
+    """The same step through the same public API (RoutingPipeline.step, the
+    C++ schedule) with every step's inputs copied H2D from pinned host memory
+    inside the timed region — each layer's hidden states (its own data: one
+    pinned host buffer per layer when host RAM allows, see `host_layers`) and
+    the per-token source groups / domain tags — and the step's LayerSims /
+    statistics read back D2H."""
     import torch
 
     s = pipe.spec
     eng = pipe.eng
-    dev = eng.device
     T, H, L = s.tokens, s.hidden, s.layers
-    host = [torch.empty(T, H, dtype=torch.bfloat16, pin_memory=True) for _ in range(2)]
-    for i in range(2):
-        host[i].copy_(pipe.X[i % L])
-    stage = [torch.empty(T, H, dtype=torch.bfloat16, device=dev) for _ in range(2)]
+    layer_bytes = T * H * 2
+    try:
+        import psutil
+        avail = psutil.virtual_memory().available
+    except ImportError:
+        avail = 0
+    n_host = max(2, min(L, int(0.6 * avail) // layer_bytes)) if avail else 2
+    host = []
+    for i in range(n_host):
+        h = torch.empty(T, H, dtype=torch.bfloat16, pin_memory=True)
+        h.copy_(pipe.X[i % L])
+        host.append(h)
     h_meta = [torch.from_numpy(pipe.h_src_cl).pin_memory(),
               torch.from_numpy(pipe.h_src_rr).pin_memory(),
               torch.from_numpy(pipe.h_dom.view("int16")).pin_memory()]
     outs = [pipe.fin_rr[0], pipe.fin_cl[0], pipe.pop, pipe.coact]
     h_out = [torch.empty(o.shape, dtype=o.dtype, pin_memory=True) for o in outs]
-    copy = torch.cuda.Stream(dev)
     main = eng.stream
-    ready = [torch.cuda.Event() for _ in range(2)]
-    free = [torch.cuda.Event() for _ in range(2)]
-    h2d = L * T * H * 2 + sum(m.numel() * m.element_size() for m in h_meta)
+    h2d = L * layer_bytes + sum(m.numel() * m.element_size() for m in h_meta)
     d2h = sum(o.numel() * o.element_size() for o in outs)
 
     def one_step():
-        pipe.src_cl.copy_(h_meta[0], non_blocking=True)
-        pipe.src_rr.copy_(h_meta[1], non_blocking=True)
-        pipe.dom_tok.view(torch.int16).copy_(h_meta[2], non_blocking=True)
-        pipe.stats.zero_()
-        for i in range(2):
-            free[i].record(main)
-        for l in range(L):
-            b = l % 2
-            with torch.cuda.stream(copy):
-                copy.wait_event(free[b])
-                stage[b].copy_(host[l % 2], non_blocking=True)
-                ready[b].record(copy)
-            main.wait_event(ready[b])
-            pipe.layer(l, stage[b])
-            free[b].record(main)
-        pipe.reduce_and_score()
-        for o, h in zip(outs, h_out):
-            h.copy_(o, non_blocking=True)
+        with torch.cuda.stream(main):
+            pipe.src_cl.copy_(h_meta[0], non_blocking=True)
+            pipe.src_rr.copy_(h_meta[1], non_blocking=True)
+            pipe.dom_tok.view(torch.int16).copy_(h_meta[2], non_blocking=True)
+            for l in range(L):
+                pipe.X[l].copy_(host[l % n_host], non_blocking=True)
+        pipe.step()
+        with torch.cuda.stream(main):
+            for o, h in zip(outs, h_out):
+                h.copy_(o, non_blocking=True)
         main.synchronize()
         return float(h_out[0][0, 0])  # the host reads the step's result
 
@@ -262,7 +273,11 @@ def run_e2e(pipe, steps: int):
         one_step()
     torch.cuda.synchronize()
     dt = (time.perf_counter() - t0) / steps
-    return dt, h2d, d2h
+    # restore the resident inputs the device-timed step used
+    if n_host < L:
+        for l in range(L):
+            pipe.model.fill_hidden(pipe.X[l], l, 0, pipe.dom_tok.long())
+    return dt, h2d, d2h, n_host
 
 
 def run_gpu_arm(args, spec):
@@ -301,6 +316,8 @@ def run_gpu_arm(args, spec):
     torch.cuda.synchronize()
     launches0 = pipe.launches
     pipe.router_events = []
+    if pipe.plan is not None:
+        pipe.plan.timing_reset()  # router events averaged over exactly the timed steps
     start = torch.cuda.Event(enable_timing=True)
     end = torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clocks:
@@ -361,13 +378,15 @@ def run_gpu_arm(args, spec):
 
     e2e = None
     if not args.no_e2e:
-        dt, h2d, d2h = run_e2e(pipe, args.e2e_steps)
+        dt, h2d, d2h, n_host = run_e2e(pipe, args.e2e_steps)
         tt = torch.tensor([dt], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e = {"value": tokens_step / float(tt.item()), "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": float(tt.item()) * 1e3,
-               "note": "hidden states H2D per layer from pinned host (PCIe-bound)"}
+               "host_layers": n_host,
+               "note": "every layer's hidden states H2D from pinned host each step (PCIe-bound); "
+                       f"{n_host} distinct pinned host layers of {spec.layers}"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -31,6 +31,9 @@
  *                          (simulator.cpp:27-41, 90-98), bit-exact doubles
  *   mpb_dispatch_gather / mpb_combine_scatter  (new) physical bf16 dispatch /
  *                          combine around the all-to-all
+ *   mpb_step_*             the host schedule of one routed step over all
+ *                          layers (pipeline.cpp:316-443's route -> account ->
+ *                          price loop), in C++ inside the library
  */
 #ifndef MOEPLACE_B200_H
 #define MOEPLACE_B200_H
@@ -315,6 +318,89 @@ MPB_API mpb_status mpb_combine_p2p(mpb_context *ctx, const int32_t *pair_pos,
                                    const int64_t *counts, const int64_t *key_offsets,
                                    uint32_t span, uint32_t world, uint32_t rank,
                                    const uint64_t *peer_recv, void *Y);
+
+/* ---- the routed step (C++ host schedule) ----------------------------------
+ * One routed pass of every MoE layer over one batch, scheduled by the library
+ * on two streams of its own — the host side of the reference's planner loop
+ * (pipeline.cpp:316-443: route -> account -> price every placement), with the
+ * routes from the router GEMM instead of the synthetic sampler:
+ *   LAYERS phase: zero the fused statistics buffer; routers (grouped launches
+ *     of router_group layers, mpb_router_topk_layers) on the main stream with
+ *     an SM budget of device_sms - side_sms; each chunk's statistics tails
+ *     (mpb_dispatch_layout: demand / demand2 / tag histograms + permutation,
+ *     and mpb_coactivation) on the side stream, beside the next chunk's router.
+ *     One layer: the router on every SM, then the layout on main with the
+ *     co-activation beside it on the side stream.
+ *   SCORE phase: mpb_score_placements_finalize of score_jobs[0] on the main
+ *     stream, the other jobs on the side stream beside it.
+ * Multi-GPU callers all-reduce the statistics between the phases. Both
+ * phases are asynchronous and ordered after / before the work already on
+ * ctx's stream. mpb_step_capture replays them from CUDA graphs (captured
+ * after one eager run that sizes every workspace). Per-chunk router times
+ * (device events around every router launch, also inside the graphs) feed
+ * the roofline. */
+typedef struct mpb_step mpb_step;
+typedef struct {
+    const uint64_t *demand;    /* [B][rows][E] */
+    uint32_t B, rows;
+    const uint8_t *row_node;   /* [rows] */
+    const uint8_t *luts;       /* [P][nodes][E] */
+    uint32_t P;
+    const uint8_t *group_to_node; /* [D] device */
+    uint32_t D, nodes, E;
+    uint64_t *inter, *intra, *rank_pairs;
+    double cost[6];
+    uint32_t tp_exp;
+    int spans_nodes;
+    double *out, *payload;     /* [P*B][6], [P*B][D] */
+} mpb_score_job;
+
+typedef struct {
+    uint32_t layers;
+    uint64_t T;
+    uint32_t H, E, k;
+    int score_fn, renorm;
+    const void *const *X;      /* host array [layers] of device bf16 [T,H] */
+    const void *const *W;      /* host array [layers] of device bf16 [E,H] */
+    int32_t *idx;              /* [layers][T][k] */
+    float *weights;            /* [layers][T][k] */
+    const mpb_placement *deployed;
+    const uint8_t *src_group;  /* [T] */
+    const uint8_t *src_group2; /* [T] or NULL */
+    const uint16_t *tag;       /* [T] or NULL */
+    uint32_t n_tags;
+    uint64_t *demand;          /* [layers][D][E] */
+    uint64_t *demand2;         /* [layers][D][E] or NULL */
+    uint64_t *tag_pop;         /* [n_tags][E] or NULL */
+    uint64_t *coact;           /* [E][E] or NULL (no co-activation) */
+    int32_t *sorted_pairs;     /* [T*k] or NULL (no permutation) */
+    int32_t *pair_pos;
+    int64_t *key_offsets;
+    void *zero_base;           /* zeroed at the start of every LAYERS phase */
+    uint64_t zero_bytes;
+    const mpb_score_job *score_jobs; /* copied */
+    uint32_t n_score_jobs;
+    uint32_t side_sms;         /* 0: 20 when layers > 1 */
+    uint32_t router_group;     /* 0: 8 */
+} mpb_step_desc;
+
+#define MPB_STEP_LAYERS 1u
+#define MPB_STEP_SCORE 2u
+MPB_API mpb_status mpb_step_create(mpb_context *ctx, const mpb_step_desc *desc, mpb_step **out);
+MPB_API mpb_status mpb_step_destroy(mpb_step *step);
+MPB_API mpb_status mpb_step_run(mpb_step *step, uint32_t phases);
+MPB_API mpb_status mpb_step_capture(mpb_step *step);
+/* Waits for both streams; reports kernel-flagged input errors of either. */
+MPB_API mpb_status mpb_step_sync(mpb_step *step);
+/* Per-layer router ms (a grouped launch's time divided over its layers) into
+ * ms[layers], averaged over the runs since mpb_step_timing_reset (at most the
+ * last 64; the last run when none); *n_runs = runs averaged. After sync. */
+MPB_API mpb_status mpb_step_timing_reset(mpb_step *step);
+MPB_API mpb_status mpb_step_router_ms(const mpb_step *step, float *ms, uint32_t *n_runs);
+/* Kernels one run of `phases` launches; the chunking (layers per router
+ * launch) into chunks[] (capacity layers), *n_chunks. */
+MPB_API mpb_status mpb_step_info(const mpb_step *step, uint32_t phases, uint64_t *launches,
+                                 uint32_t *chunks, uint32_t *n_chunks);
 
 /* ---- host placement / grouping policies (no device needed) ----------------
  * Restatements of the reference policies with the same std::mt19937_64 /

@@ -29,6 +29,25 @@ class MpbTokens(C.Structure):
                 ("n_tags", C.c_uint32), ("src_group2", _p)]
 
 
+class MpbScoreJob(C.Structure):
+    _fields_ = [("demand", _p), ("B", C.c_uint32), ("rows", C.c_uint32), ("row_node", _p),
+                ("luts", _p), ("P", C.c_uint32), ("group_to_node", _p), ("D", C.c_uint32),
+                ("nodes", C.c_uint32), ("E", C.c_uint32), ("inter", _p), ("intra", _p),
+                ("rank_pairs", _p), ("cost", C.c_double * 6), ("tp_exp", C.c_uint32),
+                ("spans_nodes", C.c_int), ("out", _p), ("payload", _p)]
+
+
+class MpbStepDesc(C.Structure):
+    _fields_ = [("layers", C.c_uint32), ("T", C.c_uint64), ("H", C.c_uint32), ("E", C.c_uint32),
+                ("k", C.c_uint32), ("score_fn", C.c_int), ("renorm", C.c_int), ("X", _p),
+                ("W", _p), ("idx", _p), ("weights", _p), ("deployed", _p), ("src_group", _p),
+                ("src_group2", _p), ("tag", _p), ("n_tags", C.c_uint32), ("demand", _p),
+                ("demand2", _p), ("tag_pop", _p), ("coact", _p), ("sorted_pairs", _p),
+                ("pair_pos", _p), ("key_offsets", _p), ("zero_base", _p),
+                ("zero_bytes", C.c_uint64), ("score_jobs", _p), ("n_score_jobs", C.c_uint32),
+                ("side_sms", C.c_uint32), ("router_group", C.c_uint32)]
+
+
 _SIGS = {
     "mpb_abi_version": (C.c_int, []),
     "mpb_last_error_message": (C.c_char_p, []),
@@ -79,6 +98,14 @@ _SIGS = {
                                     C.c_uint32, C.c_uint32, _p, C.c_uint64]),
     "mpb_combine_p2p": (C.c_int, [_p, _p, _p, C.c_uint64, C.c_uint32, C.c_uint32, _p, _p,
                                   C.c_uint32, C.c_uint32, C.c_uint32, _p, _p]),
+    "mpb_step_create": (C.c_int, [_p, C.POINTER(MpbStepDesc), C.POINTER(_p)]),
+    "mpb_step_destroy": (C.c_int, [_p]),
+    "mpb_step_run": (C.c_int, [_p, C.c_uint32]),
+    "mpb_step_capture": (C.c_int, [_p]),
+    "mpb_step_sync": (C.c_int, [_p]),
+    "mpb_step_timing_reset": (C.c_int, [_p]),
+    "mpb_step_router_ms": (C.c_int, [_p, _f32p, _u32p]),
+    "mpb_step_info": (C.c_int, [_p, C.c_uint32, _u64p, _u32p, _u32p]),
     "mpb_linear_placement": (C.c_int, [C.c_uint32, C.c_uint32, _p]),
     "mpb_eplb_placement": (C.c_int, [_p, C.c_uint32, C.c_uint32, _p]),
     "mpb_phase1_unique_distribution": (C.c_int, [_p, C.c_uint32, C.c_uint32, _p, _p]),

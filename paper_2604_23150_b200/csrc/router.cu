@@ -44,6 +44,11 @@ constexpr int kKB = MPB_ROUTER_KBLOCKS;
 constexpr int kStageK = kBK * kKB;  // K columns per stage
 constexpr int kThreadsR = 384;  // 4 non-epilogue + 8 epilogue warps
 
+#ifndef MPB_ROUTER_PREFETCH
+#define MPB_ROUTER_PREFETCH 0  // X k-steps prefetched into L2 ahead of the TMA loads
+#endif
+constexpr uint32_t kPrefetch = MPB_ROUTER_PREFETCH;
+
 #ifndef MPB_ROUTER_STAGES_CAP
 #define MPB_ROUTER_STAGES_CAP 8  // build-time knob for stage-count experiments
 #endif
@@ -210,6 +215,26 @@ __global__ void __launch_bounds__(kThreadsR, 1)
         int stage = 0;
         uint32_t phase = 0;
         WorkItem it;
+        // X L2 prefetch cursor, kPrefetch k-steps ahead of the loads in the same
+        // (tile, k-block) order: HBM latency is covered by L2 prefetches that hold
+        // no shared memory, so the smem ring only has to cover the L2 latency
+        uint32_t pn = 0, pkb = 0;
+        WorkItem pit;
+        bool pvalid = kPrefetch > 0 && next_item(0, unit, units, p.num_tiles, nk, p.splits, pit);
+        if (pvalid) pkb = pit.k0;
+        auto prefetch_one = [&]() {
+            if (!pvalid) return;
+            const uint32_t pl = pit.tile / p.tiles_per_layer;
+            ptx::tma_prefetch_2d(p.maps ? p.maps + 2 * pl : &tmX, static_cast<int32_t>(pkb * kStageK),
+                                 static_cast<int32_t>((pit.tile - pl * p.tiles_per_layer) * Cfg::ROWS_PER_TILE +
+                                                      rank * kBM));
+            if (++pkb >= pit.k1) {
+                pvalid = next_item(++pn, unit, units, p.num_tiles, nk, p.splits, pit);
+                if (pvalid) pkb = pit.k0;
+            }
+        };
+        if constexpr (kPrefetch > 0)
+            for (uint32_t i = 0; i < kPrefetch; ++i) prefetch_one();
         for (uint32_t n = 0; next_item(n, unit, units, p.num_tiles, nk, p.splits, it); ++n) {
             const uint32_t layer = it.tile / p.tiles_per_layer;
             const int32_t m0 = static_cast<int32_t>((it.tile - layer * p.tiles_per_layer) * Cfg::ROWS_PER_TILE +
@@ -217,18 +242,35 @@ __global__ void __launch_bounds__(kThreadsR, 1)
             const CUtensorMap *mX = p.maps ? p.maps + 2 * layer : &tmX;
             const CUtensorMap *mW = p.maps ? p.maps + 2 * layer + 1 : &tmW;
             for (uint32_t kb = it.k0; kb < it.k1; ++kb) {
+                prefetch_one();
                 ptx::mbar_wait(&empty[stage], phase ^ 1);
                 if constexpr (PAIR) {
+#if (defined(MPB_EXP) && MPB_EXP == 1) || defined(MPB_EXP_FEEDNOW)  // experiment: W for the first tile only
+                    const bool wl = n == 0;
+#else
+                    constexpr bool wl = true;
+#endif
+#if defined(MPB_EXP) && MPB_EXP == 2  // experiment: X rows from an L2-resident window
+                    const int32_t mx0 = m0 & 2047;
+#else
+                    const int32_t mx0 = m0;
+#endif
                     // both CTAs' loads complete on the leader's full barrier
-                    if (rank == 0) ptx::mbar_arrive_expect_tx(&full[stage], 2 * Cfg::STAGE);
+                    if (rank == 0) ptx::mbar_arrive_expect_tx(&full[stage], wl ? 2 * Cfg::STAGE : 2 * Cfg::A_BYTES);
                     const uint32_t bar = ptx::mapa(ptx::smem_u32(&full[stage]), 0);
 #pragma unroll
                     for (int j = 0; j < kKB; ++j) {
                         const int32_t kc = static_cast<int32_t>(kb * kStageK + j * kBK);
+#if defined(MPB_EXP_CONTIG)  // experiment: the same bytes as one contiguous stream per tile
                         ptx::tma_load_2d_2sm(mX, bar, sA + stage * Cfg::A_BYTES + j * Cfg::A_BLOCK,
-                                             kc, m0, pol_x);
-                        ptx::tma_load_2d_2sm(mW, bar, sB + stage * Cfg::B_BYTES + j * Cfg::B_BLOCK,
-                                             kc, static_cast<int32_t>(rank) * (N / 2), pol_w);
+                                             0, static_cast<int32_t>(((mx0 / kBM) * nk + kb) * kBM), pol_x);
+#else
+                        ptx::tma_load_2d_2sm(mX, bar, sA + stage * Cfg::A_BYTES + j * Cfg::A_BLOCK,
+                                             kc, mx0, pol_x);
+#endif
+                        if (wl)
+                            ptx::tma_load_2d_2sm(mW, bar, sB + stage * Cfg::B_BYTES + j * Cfg::B_BLOCK,
+                                                 kc, static_cast<int32_t>(rank) * (N / 2), pol_w);
                     }
                 } else {
                     ptx::mbar_arrive_expect_tx(&full[stage], Cfg::STAGE);
@@ -266,6 +308,9 @@ __global__ void __launch_bounds__(kThreadsR, 1)
                         ptx::smem_u32(sA + stage * Cfg::A_BYTES + j * Cfg::A_BLOCK));
                     const uint64_t bd = ptx::sw128_kmajor_desc(
                         ptx::smem_u32(sB + stage * Cfg::B_BYTES + j * Cfg::B_BLOCK));
+#if defined(MPB_EXP) && MPB_EXP == 3  // experiment: loads only (no MMAs) — the feed's own rate
+                    if (kb != it.k0 + 1) continue;
+#endif
 #pragma unroll
                     for (int kk = 0; kk < kBK / 16; ++kk) {  // +32 bytes along K per UMMA_K = 16
                         const uint32_t accum = (kb != it.k0) | (j != 0) | (kk != 0);
@@ -601,7 +646,12 @@ bool make_map(CUtensorMap *map, const void *ptr, uint64_t rows, uint64_t cols, u
     cuuint32_t estr[2] = {1, 1};
     CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(ptr), dims,
                     strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+#ifdef MPB_EXP_PROMO
+                    static_cast<CUtensorMapL2promotion>(MPB_EXP_PROMO),
+#else
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+#endif
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
 
@@ -787,7 +837,12 @@ extern "C" mpb_status mpb_router_topk_layers(mpb_context *ctx, uint32_t layers, 
         }
         std::vector<CUtensorMap> maps(2 * static_cast<size_t>(layers));
         for (uint32_t l = 0; l < layers; ++l)
-            if (!make_map(&maps[2 * l], X[l], T, H, kBM) || !make_map(&maps[2 * l + 1], W[l], E, H, pair ? N / 2 : N))
+#if defined(MPB_EXP_CONTIG)
+            if (!make_map(&maps[2 * l], X[l], T * H / kBK, kBK, kBM) ||
+#else
+            if (!make_map(&maps[2 * l], X[l], T, H, kBM) ||
+#endif
+                !make_map(&maps[2 * l + 1], W[l], E, H, pair ? N / 2 : N))
                 return fail(MPB_CUDA_ERROR, "mpb_router_topk_layers: cuTensorMapEncodeTiled failed");
         void *d = nullptr;
         MPB_CUDA(cudaMalloc(&d, maps.size() * sizeof(CUtensorMap)));

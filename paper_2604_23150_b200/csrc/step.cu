@@ -1,0 +1,419 @@
+// The routed step's host schedule (mpb_step_*): C++ inside the library.
+//
+// The reference's planner loop (/root/reference/proj/core/src/pipeline.cpp:
+// 316-443) routes, accounts and prices on the host, layer after layer. Here one
+// step over L layers is a fixed launch schedule on two streams owned by the
+// plan, built once and replayed (eagerly or from CUDA graphs):
+//
+//   LAYERS  main stream (high priority, SM budget device - side_sms):
+//             memset(stats) ; for each chunk c of layers [l0, l1):
+//               ev_r0[c] ; mpb_router_topk_layers(l0..l1) ; ev_r1[c] ; ev_done[c]
+//           side stream (low priority, side_sms): for each chunk c:
+//               wait ev_done[c] ; for l in [l0, l1): mpb_dispatch_layout(l),
+//               mpb_coactivation(l)        -- beside router chunk c+1
+//           main waits for the side stream's last tail.
+//           One layer (nothing to overlap): router on every SM, then the layout
+//           on main with the co-activation beside it on the side stream.
+//   SCORE   score_jobs[0] on main, the others on side, joined.
+//
+// Chunks taper at the end (..., 4, 2, 1 layers) so the tails left after the
+// last router are short. Every layer owns its idx / weights slice, so routers
+// never wait on tails. Both phases order after the work already on the
+// caller's stream and before anything enqueued after them.
+#include <algorithm>
+#include <cstring>
+#include <utility>
+#include <vector>
+
+#include "internal.cuh"
+
+struct mpb_step {
+    mpb_context *ctx = nullptr;  // the caller's (ordering) context
+    mpb_context *main = nullptr, *side = nullptr;
+    cudaStream_t s_main = nullptr, s_side = nullptr;
+    mpb_step_desc d{};
+    std::vector<const void *> X, W;
+    std::vector<mpb_score_job> jobs;
+    std::vector<std::pair<uint32_t, uint32_t>> chunks;
+    bool overlapped = false;
+    cudaEvent_t ev_in = nullptr, ev_out = nullptr, ev_fork = nullptr, ev_join = nullptr;
+    std::vector<cudaEvent_t> ev_done;
+    // router timing: kRing sets of (start, end) events per chunk; run r of the
+    // LAYERS phase records into set r % kRing, so the per-layer router time can
+    // be averaged over every run of a timed region (graphs: the event-record
+    // nodes are re-pointed at the run's set before each launch)
+    static constexpr uint32_t kRing = 64;
+    std::vector<cudaEvent_t> ev_r0, ev_r1;  // [kRing][chunk]
+    uint64_t runs = 0, timing_from = 0;
+    cudaGraph_t graph_layers = nullptr;
+    std::vector<std::pair<cudaGraphNode_t, uint32_t>> rec_nodes;  // (node, chunk*2 + end)
+    cudaGraphExec_t g_layers = nullptr, g_score = nullptr;
+    uint64_t launches[4] = {0, 0, 0, 0};  // per phase mask (1, 2, 3)
+    bool capturing = false;
+    // stream the phases order against: the caller's stream, or during capture
+    // a plan-owned origin stream (the legacy default stream cannot capture)
+    cudaStream_t origin = nullptr, s_cap = nullptr;
+};
+
+namespace {
+
+using namespace mpb;
+
+std::vector<std::pair<uint32_t, uint32_t>> taper_chunks(uint32_t L, uint32_t G) {
+    std::vector<uint32_t> tail;
+    uint32_t sum = 0;
+    for (uint32_t c = 1; c < G && sum + c <= L; c *= 2) {
+        tail.insert(tail.begin(), c);
+        sum += c;
+    }
+    const uint32_t rest = L - sum;
+    std::vector<uint32_t> sizes;
+    if (rest % G) sizes.push_back(rest % G);
+    for (uint32_t i = 0; i < rest / G; ++i) sizes.push_back(G);
+    sizes.insert(sizes.end(), tail.begin(), tail.end());
+    std::vector<std::pair<uint32_t, uint32_t>> out;
+    uint32_t l0 = 0;
+    for (uint32_t n : sizes) {
+        out.emplace_back(l0, l0 + n);
+        l0 += n;
+    }
+    return out;
+}
+
+mpb_status record(mpb_step *s, cudaEvent_t ev, cudaStream_t st, bool timing) {
+    // timing events inside a capture must be external nodes to stay readable
+    MPB_CUDA(cudaEventRecordWithFlags(ev, st, (timing && s->capturing) ? cudaEventRecordExternal : 0));
+    return MPB_OK;
+}
+
+mpb_status tail(mpb_step *s, mpb_context *c, uint32_t l) {
+    const mpb_step_desc &d = s->d;
+    const uint32_t D = d.deployed->D, E = d.E;
+    const size_t pairs = static_cast<size_t>(d.T) * d.k;
+    mpb_tokens tk{d.idx + l * pairs, d.T, d.k, d.src_group, 0, 0, d.tag, d.n_tags, d.src_group2};
+    if (mpb_status st = mpb_dispatch_layout(
+            c, &tk, d.deployed, d.demand + static_cast<size_t>(l) * D * E,
+            d.demand2 ? d.demand2 + static_cast<size_t>(l) * D * E : nullptr, d.tag_pop,
+            d.sorted_pairs, d.pair_pos, d.key_offsets))
+        return st;
+    return MPB_OK;
+}
+
+mpb_status launch_router(mpb_step *s, size_t c) {
+    const mpb_step_desc &d = s->d;
+    const size_t pairs = static_cast<size_t>(d.T) * d.k;
+    const auto [l0, l1] = s->chunks[c];
+    const size_t set = (s->runs % mpb_step::kRing) * s->chunks.size();
+    if (mpb_status st = record(s, s->ev_r0[set + c], s->s_main, true)) return st;
+    mpb_status st;
+    if (l1 - l0 == 1)
+        st = mpb_router_topk(s->main, s->X[l0], s->W[l0], d.T, d.H, d.E, d.k, d.score_fn, d.renorm,
+                             d.idx + l0 * pairs, d.weights + l0 * pairs, nullptr);
+    else
+        st = mpb_router_topk_layers(s->main, l1 - l0, s->X.data() + l0, s->W.data() + l0, d.T, d.H, d.E,
+                                    d.k, d.score_fn, d.renorm, d.idx + l0 * pairs,
+                                    d.weights + l0 * pairs, nullptr);
+    if (st) return st;
+    if ((st = record(s, s->ev_r1[set + c], s->s_main, true))) return st;
+    MPB_CUDA(cudaEventRecord(s->ev_done[c], s->s_main));
+    return MPB_OK;
+}
+
+mpb_status run_layers(mpb_step *s) {
+    const mpb_step_desc &d = s->d;
+    const size_t pairs = static_cast<size_t>(d.T) * d.k;
+    MPB_CUDA(cudaEventRecord(s->ev_in, s->origin));
+    MPB_CUDA(cudaStreamWaitEvent(s->s_main, s->ev_in, 0));
+    MPB_CUDA(cudaStreamWaitEvent(s->s_side, s->ev_in, 0));
+    if (d.zero_base && d.zero_bytes) MPB_CUDA(cudaMemsetAsync(d.zero_base, 0, d.zero_bytes, s->s_main));
+    mpb_status st;
+    if (s->overlapped) {
+        // router c+1 is enqueued before the tails of chunk c, so the main stream
+        // never idles while the host enqueues the side stream's launches
+        if ((st = launch_router(s, 0))) return st;
+        for (size_t c = 0; c < s->chunks.size(); ++c) {
+            if (c + 1 < s->chunks.size() && (st = launch_router(s, c + 1))) return st;
+            MPB_CUDA(cudaStreamWaitEvent(s->s_side, s->ev_done[c], 0));
+            for (uint32_t l = s->chunks[c].first; l < s->chunks[c].second; ++l) {
+                if ((st = tail(s, s->side, l))) return st;
+                if (d.coact && (st = mpb_coactivation(s->side, d.idx + l * pairs, d.T, d.k, d.E, d.coact)))
+                    return st;
+            }
+        }
+    } else {
+        for (size_t c = 0; c < s->chunks.size(); ++c) {
+            if ((st = launch_router(s, c))) return st;
+            for (uint32_t l = s->chunks[c].first; l < s->chunks[c].second; ++l) {
+                if (d.coact) {  // co-activation beside the layout (both only read idx)
+                    MPB_CUDA(cudaEventRecord(s->ev_fork, s->s_main));
+                    MPB_CUDA(cudaStreamWaitEvent(s->s_side, s->ev_fork, 0));
+                    if ((st = mpb_coactivation(s->side, d.idx + l * pairs, d.T, d.k, d.E, d.coact))) return st;
+                }
+                if ((st = tail(s, s->main, l))) return st;
+                if (d.coact) {
+                    MPB_CUDA(cudaEventRecord(s->ev_join, s->s_side));
+                    MPB_CUDA(cudaStreamWaitEvent(s->s_main, s->ev_join, 0));
+                }
+            }
+        }
+    }
+    MPB_CUDA(cudaEventRecord(s->ev_join, s->s_side));
+    MPB_CUDA(cudaStreamWaitEvent(s->s_main, s->ev_join, 0));
+    MPB_CUDA(cudaEventRecord(s->ev_out, s->s_main));
+    MPB_CUDA(cudaStreamWaitEvent(s->origin, s->ev_out, 0));
+    return MPB_OK;
+}
+
+mpb_status run_score(mpb_step *s) {
+    if (s->jobs.empty()) return MPB_OK;
+    MPB_CUDA(cudaEventRecord(s->ev_in, s->origin));
+    MPB_CUDA(cudaStreamWaitEvent(s->s_main, s->ev_in, 0));
+    MPB_CUDA(cudaStreamWaitEvent(s->s_side, s->ev_in, 0));
+    for (size_t j = 0; j < s->jobs.size(); ++j) {
+        const mpb_score_job &b = s->jobs[j];
+        mpb_context *c = j == 0 ? s->main : s->side;
+        if (mpb_status st = mpb_score_placements_finalize(
+                c, b.demand, b.B, b.rows, b.row_node, b.luts, b.P, b.group_to_node, b.D, b.nodes, b.E,
+                b.inter, b.intra, b.rank_pairs, b.cost, b.tp_exp, b.spans_nodes, b.out, b.payload))
+            return st;
+    }
+    MPB_CUDA(cudaEventRecord(s->ev_join, s->s_side));
+    MPB_CUDA(cudaStreamWaitEvent(s->s_main, s->ev_join, 0));
+    MPB_CUDA(cudaEventRecord(s->ev_out, s->s_main));
+    MPB_CUDA(cudaStreamWaitEvent(s->origin, s->ev_out, 0));
+    return MPB_OK;
+}
+
+mpb_status run_phases(mpb_step *s, uint32_t phases) {
+    if (!s->capturing) s->origin = s->ctx->stream;
+    if (phases & MPB_STEP_LAYERS)
+        if (mpb_status st = run_layers(s)) return st;
+    if (phases & MPB_STEP_SCORE)
+        if (mpb_status st = run_score(s)) return st;
+    return MPB_OK;
+}
+
+uint64_t launch_total(const mpb_step *s) { return s->main->launches + s->side->launches; }
+
+}  // namespace
+
+extern "C" {
+
+mpb_status mpb_step_create(mpb_context *ctx, const mpb_step_desc *desc, mpb_step **out) {
+    if (!ctx || !desc || !out) return fail(MPB_VALIDATION_ERROR, "mpb_step_create: NULL argument");
+    *out = nullptr;
+    const mpb_step_desc &d = *desc;
+    if (!d.layers || !d.T || !d.X || !d.W || !d.idx || !d.weights || !d.deployed || !d.demand)
+        return fail(MPB_VALIDATION_ERROR, "mpb_step_create: missing layers / X / W / idx / weights / "
+                                          "deployed placement / demand");
+    if (d.deployed->E != d.E) return fail(MPB_CONFIG_ERROR, "mpb_step_create: placement E != E");
+    if (d.n_score_jobs && !d.score_jobs) return fail(MPB_VALIDATION_ERROR, "mpb_step_create: NULL score_jobs");
+    if ((d.sorted_pairs || d.pair_pos || d.key_offsets) && !(d.sorted_pairs && d.pair_pos && d.key_offsets))
+        return fail(MPB_VALIDATION_ERROR, "mpb_step_create: permutation outputs: all three or none");
+    auto *s = new mpb_step();
+    s->ctx = ctx;
+    s->d = d;
+    s->X.assign(d.X, d.X + d.layers);
+    s->W.assign(d.W, d.W + d.layers);
+    s->d.X = s->d.W = nullptr;
+    if (d.n_score_jobs) s->jobs.assign(d.score_jobs, d.score_jobs + d.n_score_jobs);
+    s->d.score_jobs = nullptr;
+    s->overlapped = d.layers > 1;
+    const uint32_t side_sms = d.side_sms ? d.side_sms : 20;
+    const uint32_t G = d.router_group ? d.router_group : 8;
+    if (s->overlapped)
+        s->chunks = taper_chunks(d.layers, G);
+    else
+        s->chunks.emplace_back(0, 1);
+    auto cleanup = [&](mpb_status st) {
+        mpb_step_destroy(s);
+        return st;
+    };
+    int lo = 0, hi = 0;
+    cudaError_t e = cudaSetDevice(ctx->device);
+    if (e == cudaSuccess) e = cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    // the router chain gets the high-priority stream: when SMs free up, the
+    // block scheduler serves its CTAs before the tails'
+    if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&s->s_main, cudaStreamNonBlocking, hi);
+    if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&s->s_side, cudaStreamNonBlocking, lo);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s->s_cap, cudaStreamNonBlocking);
+    for (cudaEvent_t *ev : {&s->ev_in, &s->ev_out, &s->ev_fork, &s->ev_join})
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
+    const size_t nc = s->chunks.size();
+    s->ev_done.assign(nc, nullptr);
+    s->ev_r0.assign(nc * mpb_step::kRing, nullptr);
+    s->ev_r1.assign(nc * mpb_step::kRing, nullptr);
+    for (size_t c = 0; c < nc && e == cudaSuccess; ++c) {
+        e = cudaEventCreateWithFlags(&s->ev_done[c], cudaEventDisableTiming);
+    }
+    for (size_t i = 0; i < s->ev_r0.size() && e == cudaSuccess; ++i) {
+        e = cudaEventCreate(&s->ev_r0[i]);
+        if (e == cudaSuccess) e = cudaEventCreate(&s->ev_r1[i]);
+    }
+    if (e != cudaSuccess) return cleanup(cuda_fail(e, "mpb_step_create"));
+    if (mpb_status st = mpb_context_create(ctx->device, s->s_main, &s->main)) return cleanup(st);
+    if (mpb_status st = mpb_context_create(ctx->device, s->s_side, &s->side)) return cleanup(st);
+    if (s->overlapped) {
+        const uint32_t dev_sms = static_cast<uint32_t>(ctx->device_sms);
+        if (side_sms >= dev_sms) return cleanup(fail(MPB_CONFIG_ERROR, "mpb_step_create: side_sms >= SMs"));
+        mpb_context_set_sm_budget(s->side, side_sms);
+        mpb_context_set_sm_budget(s->main, dev_sms - side_sms);
+    }
+    *out = s;
+    return MPB_OK;
+}
+
+mpb_status mpb_step_destroy(mpb_step *s) {
+    if (!s) return MPB_OK;
+    if (s->s_main) cudaStreamSynchronize(s->s_main);
+    if (s->s_side) cudaStreamSynchronize(s->s_side);
+    if (s->g_layers) cudaGraphExecDestroy(s->g_layers);
+    if (s->graph_layers) cudaGraphDestroy(s->graph_layers);
+    if (s->g_score) cudaGraphExecDestroy(s->g_score);
+    mpb_context_destroy(s->main);
+    mpb_context_destroy(s->side);
+    for (cudaEvent_t ev : {s->ev_in, s->ev_out, s->ev_fork, s->ev_join})
+        if (ev) cudaEventDestroy(ev);
+    for (auto *v : {&s->ev_done, &s->ev_r0, &s->ev_r1})
+        for (cudaEvent_t ev : *v)
+            if (ev) cudaEventDestroy(ev);
+    if (s->s_main) cudaStreamDestroy(s->s_main);
+    if (s->s_side) cudaStreamDestroy(s->s_side);
+    if (s->s_cap) cudaStreamDestroy(s->s_cap);
+    delete s;
+    return MPB_OK;
+}
+
+mpb_status mpb_step_run(mpb_step *s, uint32_t phases) {
+    if (!s) return fail(MPB_VALIDATION_ERROR, "mpb_step_run: NULL step");
+    if (s->g_layers || s->g_score) {
+        if ((phases & MPB_STEP_LAYERS) && s->g_layers) {
+            const size_t set = (s->runs % mpb_step::kRing) * s->chunks.size();
+            for (const auto &[node, which] : s->rec_nodes)
+                MPB_CUDA(cudaGraphExecEventRecordNodeSetEvent(
+                    s->g_layers, node, (which & 1) ? s->ev_r1[set + which / 2] : s->ev_r0[set + which / 2]));
+            MPB_CUDA(cudaGraphLaunch(s->g_layers, s->ctx->stream));
+            ++s->runs;
+        }
+        if ((phases & MPB_STEP_SCORE) && s->g_score) MPB_CUDA(cudaGraphLaunch(s->g_score, s->ctx->stream));
+        return MPB_OK;
+    }
+    const uint64_t n0 = launch_total(s);
+    if (mpb_status st = run_phases(s, phases)) return st;
+    s->launches[phases & 3] = launch_total(s) - n0;
+    if (phases & MPB_STEP_LAYERS) ++s->runs;
+    return MPB_OK;
+}
+
+mpb_status mpb_step_capture(mpb_step *s) {
+    if (!s) return fail(MPB_VALIDATION_ERROR, "mpb_step_capture: NULL step");
+    if (s->g_layers || s->g_score) return MPB_OK;
+    // one eager run sizes every workspace and uploads the router descriptor tables
+    for (uint32_t ph : {MPB_STEP_LAYERS, MPB_STEP_SCORE}) {
+        const uint64_t n0 = launch_total(s);
+        if (mpb_status st = run_phases(s, ph)) return st;
+        s->launches[ph] = launch_total(s) - n0;
+        if (ph == MPB_STEP_LAYERS) ++s->runs;
+    }
+    if (mpb_status st = mpb_step_sync(s)) return st;
+    cudaGraphExec_t *dst[2] = {&s->g_layers, &s->g_score};
+    const uint32_t phs[2] = {MPB_STEP_LAYERS, MPB_STEP_SCORE};
+    for (int i = 0; i < 2; ++i) {
+        if (phs[i] == MPB_STEP_SCORE && s->jobs.empty()) continue;
+        MPB_CUDA(cudaStreamBeginCapture(s->s_cap, cudaStreamCaptureModeRelaxed));
+        s->capturing = true;
+        s->origin = s->s_cap;
+        mpb_status st = run_phases(s, phs[i]);
+        s->capturing = false;
+        cudaGraph_t g = nullptr;
+        const cudaError_t e = cudaStreamEndCapture(s->s_cap, &g);
+        if (st) {
+            if (g) cudaGraphDestroy(g);
+            return st;
+        }
+        if (e != cudaSuccess) return cuda_fail(e, "mpb_step_capture: cudaStreamEndCapture");
+        const cudaError_t e2 = cudaGraphInstantiate(dst[i], g, 0);
+        if (e2 != cudaSuccess) {
+            cudaGraphDestroy(g);
+            return cuda_fail(e2, "mpb_step_capture: cudaGraphInstantiate");
+        }
+        if (phs[i] != MPB_STEP_LAYERS) {
+            cudaGraphDestroy(g);
+            continue;
+        }
+        // the router timing events are event-record nodes: find them, so each
+        // launch can point them at its own ring set
+        s->graph_layers = g;
+        size_t n = 0;
+        MPB_CUDA(cudaGraphGetNodes(g, nullptr, &n));
+        std::vector<cudaGraphNode_t> nodes(n);
+        MPB_CUDA(cudaGraphGetNodes(g, nodes.data(), &n));
+        const size_t set = (s->runs % mpb_step::kRing) * s->chunks.size();
+        for (cudaGraphNode_t nd : nodes) {
+            cudaGraphNodeType t;
+            MPB_CUDA(cudaGraphNodeGetType(nd, &t));
+            if (t != cudaGraphNodeTypeEventRecord) continue;
+            cudaEvent_t ev;
+            MPB_CUDA(cudaGraphEventRecordNodeGetEvent(nd, &ev));
+            for (size_t c = 0; c < s->chunks.size(); ++c) {
+                if (ev == s->ev_r0[set + c]) s->rec_nodes.emplace_back(nd, static_cast<uint32_t>(2 * c));
+                if (ev == s->ev_r1[set + c]) s->rec_nodes.emplace_back(nd, static_cast<uint32_t>(2 * c + 1));
+            }
+        }
+        if (s->rec_nodes.size() != 2 * s->chunks.size())
+            return fail(MPB_CUDA_ERROR, "mpb_step_capture: router timing nodes not found in the graph");
+    }
+    return MPB_OK;
+}
+
+mpb_status mpb_step_sync(mpb_step *s) {
+    if (!s) return fail(MPB_VALIDATION_ERROR, "mpb_step_sync: NULL step");
+    MPB_CUDA(cudaStreamSynchronize(s->ctx->stream));
+    mpb_status a = mpb_context_sync(s->main);
+    mpb_status b = mpb_context_sync(s->side);
+    return a ? a : b;
+}
+
+mpb_status mpb_step_timing_reset(mpb_step *s) {
+    if (!s) return fail(MPB_VALIDATION_ERROR, "mpb_step_timing_reset: NULL step");
+    s->timing_from = s->runs;
+    return MPB_OK;
+}
+
+mpb_status mpb_step_router_ms(const mpb_step *s, float *ms, uint32_t *n_runs) {
+    if (!s || !ms) return fail(MPB_VALIDATION_ERROR, "mpb_step_router_ms: NULL argument");
+    uint64_t from = std::max(s->timing_from, s->runs > mpb_step::kRing ? s->runs - mpb_step::kRing : 0);
+    if (from >= s->runs) from = s->runs ? s->runs - 1 : 0;  // nothing since the reset: the last run
+    const size_t nc = s->chunks.size();
+    for (uint32_t l = 0; l < s->d.layers; ++l) ms[l] = 0.f;
+    for (uint64_t r = from; r < s->runs; ++r) {
+        const size_t set = (r % mpb_step::kRing) * nc;
+        for (size_t c = 0; c < nc; ++c) {
+            float t = 0.f;
+            MPB_CUDA(cudaEventElapsedTime(&t, s->ev_r0[set + c], s->ev_r1[set + c]));
+            const auto [l0, l1] = s->chunks[c];
+            for (uint32_t l = l0; l < l1; ++l) ms[l] += t / static_cast<float>(l1 - l0);
+        }
+    }
+    const uint64_t n = s->runs - from;
+    for (uint32_t l = 0; l < s->d.layers && n; ++l) ms[l] /= static_cast<float>(n);
+    if (n_runs) *n_runs = static_cast<uint32_t>(n);
+    return MPB_OK;
+}
+
+mpb_status mpb_step_info(const mpb_step *s, uint32_t phases, uint64_t *launches, uint32_t *chunks,
+                         uint32_t *n_chunks) {
+    if (!s) return fail(MPB_VALIDATION_ERROR, "mpb_step_info: NULL step");
+    if (launches) {
+        uint64_t n = s->launches[phases & 3];
+        if (!n && phases == (MPB_STEP_LAYERS | MPB_STEP_SCORE))
+            n = s->launches[MPB_STEP_LAYERS] + s->launches[MPB_STEP_SCORE];
+        *launches = n;
+    }
+    if (n_chunks) *n_chunks = static_cast<uint32_t>(s->chunks.size());
+    if (chunks)
+        for (size_t c = 0; c < s->chunks.size(); ++c) chunks[c] = s->chunks[c].second - s->chunks[c].first;
+    return MPB_OK;
+}
+
+}  // extern "C"

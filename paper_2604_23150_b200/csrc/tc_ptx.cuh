@@ -105,6 +105,14 @@ __device__ __forceinline__ void tma_load_2d_mc(const CUtensorMap *map, uint64_t 
         "l"(policy)
         : "memory");
 }
+// L2 prefetch of a 2D tile (no shared memory, no barrier): the later
+// tma_load_2d of the same box hits L2.
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap *map, int32_t c0, int32_t c1) {
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(c0), "r"(c1)
+                 : "memory");
+}
 __device__ __forceinline__ uint64_t policy_evict_first() {
     uint64_t p;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));

@@ -570,6 +570,124 @@ class Engine:
         return out
 
 
+class ScoreJob:
+    """One mpb_score_placements_finalize launch of a step plan: demand
+    [B, rows, E] x luts [P, nodes, E] -> (inter, intra, rank) pair counts and
+    LayerSim doubles (fin_out [P*B, 6], payload [P*B, D])."""
+
+    def __init__(self, demand, luts, g2n, D: int, cost: "CostModelParams",
+                 topology: "Topology", out, fin_out, payload, row_node=None):
+        self.tensors = (demand, luts, g2n, row_node, *out, fin_out, payload)
+        B, rows, E = demand.shape
+        P, nodes, _ = luts.shape
+        inter, intra, rank = out
+        job = _abi.MpbScoreJob()
+        job.demand, job.B, job.rows = demand.data_ptr(), B, rows
+        job.row_node = (row_node if row_node is not None else g2n).data_ptr()
+        job.luts, job.P, job.group_to_node = luts.data_ptr(), P, g2n.data_ptr()
+        job.D, job.nodes, job.E = D, nodes, E
+        job.inter, job.intra, job.rank_pairs = inter.data_ptr(), intra.data_ptr(), rank.data_ptr()
+        for i, v in enumerate(cost.as_array()):
+            job.cost[i] = v
+        job.tp_exp, job.spans_nodes = topology.tp_exp, int(topology.spans_nodes())
+        job.out, job.payload = fin_out.data_ptr(), payload.data_ptr()
+        self.job = job
+
+
+class StepPlan:
+    """The routed step's C++ host schedule (mpb_step_*): routers grouped over
+    layers on a high-priority stream, each chunk's statistics tails (layout +
+    permutation + histograms, co-activation) on a side stream with a small SM
+    budget beside the next routers, then the candidate scoring jobs — launched
+    from C++, optionally replayed from CUDA graphs. Buffers are the caller's
+    tensors (kept alive here); run() is asynchronous on the engine's stream."""
+
+    LAYERS, SCORE = 1, 2
+
+    def __init__(self, engine: "Engine", Xs, Ws, k: int, score_fn: int, renorm: bool,
+                 idx: torch.Tensor, weights: torch.Tensor, deployed: "DevicePlacement",
+                 src: torch.Tensor, demand: torch.Tensor, src2=None, demand2=None, tag=None,
+                 n_tags: int = 0, tag_pop=None, coact=None, perm_out=None, zero=None,
+                 score_jobs=(), side_sms: int = 0, router_group: int = 0):
+        L = len(Xs)
+        T, H = Xs[0].shape
+        E = Ws[0].shape[0]
+        self.engine, self.layers = engine, L
+        self._keep = [Xs, Ws, idx, weights, deployed, src, demand, src2, demand2, tag, tag_pop,
+                      coact, perm_out, zero, list(score_jobs)]
+        d = _abi.MpbStepDesc()
+        d.layers, d.T, d.H, d.E, d.k = L, T, H, E, k
+        d.score_fn, d.renorm = score_fn, int(renorm)
+        self._xp = (C.c_void_p * L)(*[x.data_ptr() for x in Xs])
+        self._wp = (C.c_void_p * L)(*[w.data_ptr() for w in Ws])
+        d.X, d.W = C.cast(self._xp, C.c_void_p), C.cast(self._wp, C.c_void_p)
+        assert idx.is_contiguous() and idx.numel() == L * T * k
+        d.idx, d.weights = idx.data_ptr(), weights.data_ptr()
+        d.deployed = deployed.handle
+        d.src_group = src.data_ptr()
+        d.src_group2 = src2.data_ptr() if src2 is not None else None
+        d.tag = tag.data_ptr() if tag is not None else None
+        d.n_tags = n_tags
+        d.demand = demand.data_ptr()
+        d.demand2 = demand2.data_ptr() if demand2 is not None else None
+        d.tag_pop = tag_pop.data_ptr() if tag_pop is not None else None
+        d.coact = coact.data_ptr() if coact is not None else None
+        if perm_out is not None:
+            d.sorted_pairs, d.pair_pos, d.key_offsets = (t.data_ptr() for t in perm_out)
+        if zero is not None:
+            d.zero_base, d.zero_bytes = zero.data_ptr(), zero.numel() * zero.element_size()
+        jobs = list(score_jobs)
+        self._jobs = (_abi.MpbScoreJob * max(1, len(jobs)))(*[j.job for j in jobs])
+        d.score_jobs = C.cast(self._jobs, C.c_void_p) if jobs else None
+        d.n_score_jobs = len(jobs)
+        d.side_sms, d.router_group = side_sms, router_group
+        self._desc = d
+        h = C.c_void_p()
+        _abi.call("mpb_step_create", engine.ctx, C.byref(d), C.byref(h))
+        self.handle = h
+        self.graphed = False
+
+    def run(self, phases: int = 3) -> None:
+        _abi.call("mpb_step_run", self.handle, phases)
+
+    def capture(self) -> None:
+        _abi.call("mpb_step_capture", self.handle)
+        self.graphed = True
+
+    def sync(self) -> None:
+        _abi.call("mpb_step_sync", self.handle)
+
+    def timing_reset(self) -> None:
+        """Start of a timed region: router_ms() averages the runs after this."""
+        _abi.call("mpb_step_timing_reset", self.handle)
+
+    def router_ms(self):
+        """Per-layer router ms averaged over the runs since timing_reset() (the
+        last run if none; call after sync())."""
+        out = (C.c_float * self.layers)()
+        n = C.c_uint32()
+        _abi.call("mpb_step_router_ms", self.handle, out, C.byref(n))
+        self.timed_runs = n.value
+        return list(out)
+
+    def launches(self, phases: int = 3) -> int:
+        n = C.c_uint64()
+        _abi.call("mpb_step_info", self.handle, phases, C.byref(n), None, None)
+        return n.value
+
+    def chunks(self):
+        arr = (C.c_uint32 * self.layers)()
+        n = C.c_uint32()
+        _abi.call("mpb_step_info", self.handle, 3, None, arr, C.byref(n))
+        return list(arr[:n.value])
+
+    def __del__(self):
+        try:
+            _abi.lib().mpb_step_destroy(self.handle)
+        except Exception:
+            pass
+
+
 _engines: dict = {}
 
 

@@ -186,7 +186,20 @@ class RoutingPipeline:
         self.side = None
         # (one layer: nothing to overlap the tail with — co-activation beside the layout)
         self.side_mode = int(os.environ.get("MPB_SIDE_STREAM", "3" if s.layers > 1 else "1"))
-        if self.side_mode == 3:
+        # the step's schedule runs from C++ (mpb_step_*, StepPlan) unless
+        # MPB_STEP_NATIVE=0 (the Python restatement of the same schedule, kept
+        # for the serial-vs-overlapped parity tests and the e2e loop)
+        self.native = resident and os.environ.get("MPB_STEP_NATIVE", "1") != "0" and \
+            self.side_mode in (1, 3)
+        self.plan = None
+        self.router_group = max(1, int(os.environ.get("MPB_ROUTER_GROUP", "8")))
+        self.side_sms = int(os.environ.get("MPB_SIDE_SMS", "20")) if s.layers > 1 else 0
+        if self.native:
+            self.idx_all = torch.empty(L, T, k, dtype=torch.int32, device=dev)
+            self.w_all = torch.empty(L, T, k, dtype=torch.float32, device=dev)
+            self.idx, self.w = self.idx_all[0], self.w_all[0]
+            self.idx_buf, self.w_buf = list(self.idx_all), list(self.w_all)
+        elif self.side_mode == 3:
             # the router chain gets the high-priority stream (made current, so the
             # caller's torch ops and timing events stay ordered with it): when SMs
             # free up, the block scheduler serves its CTAs before the tail's
@@ -273,6 +286,34 @@ class RoutingPipeline:
                 if progress:
                     progress(f"hidden states layer {l + 1}/{L}")
         self.router_events = []
+        self._plan_launched = 0
+        if self.native:
+            self._build_plan()
+
+    def _build_plan(self):
+        s, eng = self.spec, self.eng
+        L, D = s.layers, s.groups
+        lo, hi = self.shard if self.shard is not None else (0, self.luts_cl.shape[0])
+        jobs = [mp.ScoreJob(self.dem_cl, self.luts_cl[lo:hi], self.g2n, D, self.cost,
+                            self.topology, tuple(t[lo:hi] for t in self.sc_cl),
+                            self.fin_cl[0][lo * L:hi * L], self.fin_cl[1][lo * L:hi * L]),
+                mp.ScoreJob(self.dem_rr, self.luts_rr, self.g2n, D, self.cost, self.topology,
+                            self.sc_rr, self.fin_rr[0], self.fin_rr[1])]
+        self.plan = mp.StepPlan(
+            eng, self.X, self.model.W, s.top_k, s.score_fn, s.renorm, self.idx_all, self.w_all,
+            self.dp_deployed, self.src_cl, self.dem_cl, src2=self.src_rr, demand2=self.dem_rr,
+            tag=self.dom_tok, n_tags=s.domains, tag_pop=self.pop,
+            coact=self.coact if s.coact else None, perm_out=(self.sp, self.pp, self.ko),
+            zero=self.stats, score_jobs=jobs, side_sms=self.side_sms,
+            router_group=self.router_group)
+        self.chunks, l0 = [], 0
+        for n in self.plan.chunks():
+            self.chunks.append((l0, l0 + n))
+            l0 += n
+        n_sm = torch.cuda.get_device_properties(eng.device).multi_processor_count
+        # SM budget the plan's router context sizes its grids for (tests replay
+        # the step's router launches with the same budget: same split-K tail)
+        self.router_sms = n_sm - self.side_sms if s.layers > 1 else n_sm
 
     # ---------------------------------------------------------------- calibration
     def _calibrate(self, progress) -> Calibration:
@@ -417,8 +458,12 @@ class RoutingPipeline:
 
     @property
     def launches(self) -> int:
-        """Kernels launched so far through this pipeline's contexts."""
-        return self.eng.launches + (self.side.launches if self.side is not None else 0)
+        """Kernels launched so far through this pipeline's contexts (the native
+        plan's own contexts included)."""
+        n = self.eng.launches + (self.side.launches if self.side is not None else 0)
+        if self.plan is not None:
+            n += self._plan_launched
+        return n
 
     # ---------------------------------------------------------------- the step
     def layer_untimed(self, l: int, X: torch.Tensor):
@@ -518,6 +563,18 @@ class RoutingPipeline:
         gather_shards(self.fin_cl[1], rows, group)
 
     def step(self, timed_router=False, group=None):
+        if self.plan is not None:
+            P = self.plan
+            if self.world > 1:
+                import torch.distributed as dist
+                P.run(P.LAYERS)
+                dist.all_reduce(self.stats.view(torch.int64), group=group)
+                P.run(P.SCORE)
+                self._gather_scores(group)
+            else:
+                P.run(P.LAYERS | P.SCORE)
+            self._plan_launched += P.launches(P.LAYERS | P.SCORE)
+            return
         if getattr(self, "graphs", None):
             return self._replay(group)
         self.stats.zero_()
@@ -531,6 +588,11 @@ class RoutingPipeline:
 
     def schedule(self) -> dict:
         """How one step launches its routers (reported in the bench line)."""
+        if self.plan is not None:
+            chunks = self.plan.chunks()
+            return {"host": "C++ (mpb_step_run)", "side_stream_mode": 3 if self.spec.layers > 1 else 1,
+                    "side_sms": self.side_sms, "sm_partition": False,
+                    "router_launches_per_step": len(chunks), "layers_per_router_launch": chunks}
         grouped = self.side_mode == 3 and self.router_group > 1 and self.X is not None
         chunks = [l1 - l0 for l0, l1 in self.chunks] if grouped else [1] * self.spec.layers
         return {"side_stream_mode": self.side_mode,
@@ -539,7 +601,11 @@ class RoutingPipeline:
                 "router_launches_per_step": len(chunks), "layers_per_router_launch": chunks}
 
     def router_ms(self):
-        """Per-launch router times (ms) recorded by timed steps."""
+        """Per-launch router times (ms) recorded by timed steps (the native
+        plan: per layer, of its last run)."""
+        if self.plan is not None:
+            self.plan.sync()
+            return self.plan.router_ms()
         out = []
         for ev in self.router_events:
             n = ev[2] if len(ev) > 2 else 1
@@ -607,6 +673,13 @@ class RoutingPipeline:
         eng = self.eng
         L = self.spec.layers
         old = eng.stream
+        if self.plan is not None:  # the C++ schedule captures itself (both streams)
+            try:
+                self.plan.capture()
+            except Exception:
+                return False
+            self.launches_per_step = self.plan.launches()
+            return True
         if self.side_mode == 3:
             self.graphs = None
             return False
@@ -651,6 +724,8 @@ class RoutingPipeline:
         self._gather_scores(group)
 
     def graph_router_ms(self):
+        if self.plan is not None:
+            return self.router_ms()
         return [a.elapsed_time(b) for a, b in self.graph_events]
 
     # ---------------------------------------------------------------- results
@@ -660,7 +735,7 @@ class RoutingPipeline:
         DeepSeek-V3 layer 42); the last layer when the
         schedule keeps only the last layer's routing."""
         L = self.spec.layers
-        return min(42, L - 1) if self.side_mode == 3 else L - 1
+        return min(42, L - 1) if (self.side_mode == 3 or self.native) else L - 1
 
     def reference_statistic(self, group=None, num_batches: int = 200, batch_size: int = 128,
                             seed: int = 3):
@@ -676,7 +751,7 @@ class RoutingPipeline:
         s, eng = self.spec, self.eng
         dev = eng.device
         E, l = s.experts, self.sim_layer
-        idx = self.idx_buf[l] if self.side_mode == 3 else self.idx
+        idx = self.idx_buf[l] if (self.side_mode == 3 or self.native) else self.idx
         tok_req = np.arange(s.tokens) // s.tokens_per_request
         req_mat = torch.zeros(self.R, E, dtype=torch.uint64, device=dev)
         eng.dispatch_layout(idx, self.dp_deployed, src=self.src_cl,

@@ -73,13 +73,10 @@ def test_bench_path_pinned(oracle, workload):
         eng.sync()
         k, fn, renorm = spec.top_k, spec.score_fn, spec.renorm
         T, E, L = spec.tokens, spec.experts, spec.layers
-        if pipe.side_mode == 3 and pipe.router_group > 1:
-            launches = pipe.chunks
-        else:
-            launches = [(l, l + 1) for l in range(L)]
-            assert L == 1  # single-layer schedules keep only the last layer's routing
-        step_idx = pipe.idx_all if pipe.side_mode == 3 else pipe.idx.view(1, T, k)
-        step_w = pipe.w_all if pipe.side_mode == 3 else pipe.w.view(1, T, k)
+        assert pipe.native, "the bench runs the C++ step schedule"
+        launches = pipe.chunks  # the plan's router launches (layers per launch)
+        eng.set_sm_budget(pipe.router_sms)  # same grids -> same split-K tail as the step
+        step_idx, step_w = pipe.idx_all, pipe.w_all
         for l0, l1 in launches:
             n = l1 - l0
             logits = torch.empty(n, T, E, dtype=torch.float32, device=eng.device)

@@ -18,7 +18,8 @@ SPEC = WorkloadSpec("tiny", 4, 8192, 512, 64, 8, 1, True, groups=8, nodes=2, dom
                     preferred=8, candidates=64)
 
 
-def _run(mode, monkeypatch, group=8):
+def _run(mode, monkeypatch, group=8, native=False):
+    monkeypatch.setenv("MPB_STEP_NATIVE", "1" if native else "0")
     monkeypatch.setenv("MPB_SIDE_STREAM", str(mode))
     monkeypatch.setenv("MPB_ROUTER_GROUP", str(group))
     # no split-K tail: every router tile then sums its K range in one order, so
@@ -35,7 +36,7 @@ def _run(mode, monkeypatch, group=8):
         pipe.step()
     torch.cuda.synchronize()
     torch.cuda.set_stream(cur)  # mode 3 installs its own high-priority stream
-    idx = [b.clone() for b in pipe.idx_buf] if mode == 3 else None
+    idx = [b.clone() for b in pipe.idx_buf] if (mode == 3 or native) else None
     return pipe, idx
 
 
@@ -46,9 +47,14 @@ def test_overlapped_schedule_matches_serial(monkeypatch, oracle, group):
         pytest.skip("no CUDA device")
     p1, _ = _run(1, monkeypatch)
     p3, idx3 = _run(3, monkeypatch, group)
-    assert torch.equal(p1.stats, p3.stats)
-    assert torch.equal(p1.fin_cl[0], p3.fin_cl[0]) and torch.equal(p1.fin_rr[0], p3.fin_rr[0])
-    assert p1.results() == p3.results()
+    pn, idxn = _run(3, monkeypatch, group, native=True)  # the C++ schedule (mpb_step_run)
+    assert pn.plan is not None and p3.plan is None and p1.plan is None
+    for p in (p3, pn):
+        assert torch.equal(p1.stats, p.stats)
+        assert torch.equal(p1.fin_cl[0], p.fin_cl[0]) and torch.equal(p1.fin_rr[0], p.fin_rr[0])
+        assert p1.results() == p.results()
+    for a, b in zip(idx3, idxn):
+        assert torch.equal(a, b)
     # each layer's deployed demand == the oracle's histogram of that layer's routes
     top = p3.topology
     db = {e.label: e for e in p3.calib.strategies}["data_based"].placement

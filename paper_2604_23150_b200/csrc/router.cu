@@ -72,6 +72,23 @@ struct RCfg {
     static constexpr int SMEM = 1024 + STAGES * STAGE + PARK + (2 * STAGES + 4) * 8 + 16;
 };
 
+#ifdef MPB_ROUTER_TRACE
+// Experiment builds only: per-CTA %globaltimer stamps of the kernel's phases
+// (tools/router_trace.py). slot: 0 entry, 1 after griddepcontrol.wait,
+// 2 producer's first TMA issued, 3 MMA warp's last commit, 4 epilogue: last
+// accumulator ready, 5 epilogue: last fix-up done, 6 epilogue: last item
+// done, 7 exit; 8 = role of the last item, 9 = items.
+__device__ unsigned long long g_router_trace[2 * 148 * 16];
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t)::"memory");
+    return t;
+}
+#define RTRACE(slot, val) g_router_trace[blockIdx.x * 16 + (slot)] = (val)
+#else
+#define RTRACE(slot, val) ((void)0)
+#endif
+
 struct RouterParams {
     uint64_t T;
     uint32_t H;
@@ -127,6 +144,21 @@ __device__ __forceinline__ bool next_item(uint32_t n, uint32_t unit, uint32_t un
     return false;
 }
 
+// r[i] for a per-lane dynamic i in [0, 16): a 4-level select tree on the
+// index bits keeps the chunk in registers (an indexed register array would be
+// demoted to local memory; a shared-memory park costs a store of the chunk and
+// a dependent load per insertion).
+__device__ __forceinline__ float pick16(const uint32_t (&r)[16], int i) {
+    uint32_t a[8], b[4], c[2];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) a[j] = (i & 1) ? r[2 * j + 1] : r[2 * j];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) b[j] = (i & 2) ? a[2 * j + 1] : a[2 * j];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) c[j] = (i & 4) ? b[2 * j + 1] : b[2 * j];
+    return __uint_as_float((i & 8) ? c[1] : c[0]);
+}
+
 // Hands an accumulator's TMEM back to the MMA issuer after this thread's
 // tcgen05.ld reads: single CTA — every epilogue thread arrives; pair — one lane
 // per warp arrives on the LEADER's barrier (locally or through DSMEM).
@@ -159,8 +191,10 @@ __global__ void __launch_bounds__(kThreadsR, 1)
     using Cfg = RCfg<N, KMAX, PAIR>;
     constexpr int S = Cfg::STAGES;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t *base = reinterpret_cast<uint8_t *>(
-        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    // 1024-byte aligned (SW128 operands); offset arithmetic on smem_raw keeps the
+    // pointers in the shared window, so the epilogue's park / merge rows compile
+    // to LDS / STS rather than generic loads and stores
+    uint8_t *base = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t *sA = base;
     uint8_t *sB = base + S * Cfg::A_BYTES;
     float *s_park = reinterpret_cast<float *>(base + S * Cfg::STAGE);
@@ -205,8 +239,10 @@ __global__ void __launch_bounds__(kThreadsR, 1)
     const uint32_t nk = p.H / kStageK;
     // PDL: setup above overlapped the previous kernel; X, W, idx/w and the
     // split-tail workspace are touched only after it completed
+    if (threadIdx.x == 0) RTRACE(0, gtime());
     pdl_trigger();
     pdl_wait();
+    if (threadIdx.x == 0) RTRACE(1, gtime());
 
     if (warp == 0 && lane == 0) {
         // ---------------- TMA producer ----------------
@@ -243,6 +279,9 @@ __global__ void __launch_bounds__(kThreadsR, 1)
             const CUtensorMap *mW = p.maps ? p.maps + 2 * layer + 1 : &tmW;
             for (uint32_t kb = it.k0; kb < it.k1; ++kb) {
                 prefetch_one();
+#ifdef MPB_ROUTER_TRACE
+                if (n == 0 && kb == it.k0) RTRACE(2, gtime());
+#endif
                 ptx::mbar_wait(&empty[stage], phase ^ 1);
                 if constexpr (PAIR) {
 #if (defined(MPB_EXP) && MPB_EXP == 1) || defined(MPB_EXP_FEEDNOW)  // experiment: W for the first tile only
@@ -333,6 +372,7 @@ __global__ void __launch_bounds__(kThreadsR, 1)
                 ptx::mma_commit_2sm_mc(&tfull[acc], 0x3);
             else
                 ptx::mma_commit(&tfull[acc]);
+            RTRACE(3, gtime());
             acc ^= 1;
             if (acc == 0) aphase ^= 1;
         }
@@ -359,6 +399,13 @@ __global__ void __launch_bounds__(kThreadsR, 1)
         for (uint32_t n = 0; next_item(n, unit, units, p.num_tiles, nk, p.splits, it); ++n) {
             ptx::mbar_wait(&tfull[acc], aphase);
             ptx::tc_fence_after();
+#ifdef MPB_ROUTER_TRACE
+            if (warp == 4 && lane == 0) {
+                RTRACE(4, gtime());
+                RTRACE(8, it.role);
+                RTRACE(9, n + 1);
+            }
+#endif
             const uint32_t layer = it.tile / p.tiles_per_layer;
             const uint64_t row = static_cast<uint64_t>(it.tile - layer * p.tiles_per_layer) * Cfg::ROWS_PER_TILE +
                                  rank * kBM + row_in_tile;  // token within the layer
@@ -439,6 +486,9 @@ __global__ void __launch_bounds__(kThreadsR, 1)
                 if (warp == 4 && lane == 0)
                     asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(flag), "r"(0u) : "memory");
             }
+#ifdef MPB_ROUTER_TRACE
+            if (warp == 4 && lane == 0) RTRACE(5, gtime());
+#endif
             float tv[KMAX];
             int ti[KMAX];
 #pragma unroll
@@ -446,13 +496,47 @@ __global__ void __launch_bounds__(kThreadsR, 1)
                 tv[j] = j < off ? INFINITY : -INFINITY;  // sentinels above, empty slots below
                 ti[j] = j < off ? -1 : 0x7FFFFFFF;
             }
-            float m = -INFINITY;
-            float *lrow = (p.logits && row < p.T) ? p.logits + out_row * p.E : nullptr;
+            // pass 1 (TMEM reads are cheap): the half-row's max m and a lower bound
+            // t0 on its k-th largest logit — the minimum over >= KMAX column groups
+            // of each group's maximum (each group holds a logit >= t0, so at least
+            // KMAX >= k logits are >= t0). Pass 2 inserts only candidates >= t0: a
+            // handful per row instead of nearly every column of the first chunks.
+            // NaN never raises a group maximum (an all-NaN or all -inf group gives
+            // -inf: no filtering), so the NaN / -inf fill below is unaffected.
+            constexpr int GS = NH / KMAX >= 16 ? 16 : NH / KMAX;  // group size, divides 16
+            float m = -INFINITY, t0 = INFINITY;
 #pragma unroll 1
             for (int c = half * NH; c < (half + 1) * NH; c += 16) {
                 uint32_t r[16];
                 ptx::tmem_ld_32x32b_x16(taddr + c, r);
                 ptx::tmem_ld_wait();
+#pragma unroll
+                for (int g = 0; g < 16; g += GS) {
+                    float gm = -INFINITY;
+#pragma unroll
+                    for (int i = g; i < g + GS; ++i)
+                        if (static_cast<uint32_t>(c + i) < p.E) gm = fmaxf(gm, __uint_as_float(r[i]));
+                    t0 = fminf(t0, gm);
+                    m = fmaxf(m, gm);
+                }
+            }
+            if (KMAX == 1) t0 = m;
+            float *lrow = (p.logits && row < p.T) ? p.logits + out_row * p.E : nullptr;
+#ifdef MPB_ROUTER_TRACE
+            long long cy_ld = 0, cy_ins = 0, n_ins = 0;
+#endif
+#pragma unroll 1
+            for (int c = half * NH; c < (half + 1) * NH; c += 16) {
+                uint32_t r[16];
+#ifdef MPB_ROUTER_TRACE
+                const long long c0 = clock64();
+#endif
+                ptx::tmem_ld_32x32b_x16(taddr + c, r);
+                ptx::tmem_ld_wait();
+#ifdef MPB_ROUTER_TRACE
+                const long long c1 = clock64();
+                cy_ld += c1 - c0;
+#endif
                 const bool padded = static_cast<uint32_t>(c + 16) > p.E;
                 if (padded)  // padding columns (E < N): -inf, never selected
 #pragma unroll
@@ -472,21 +556,22 @@ __global__ void __launch_bounds__(kThreadsR, 1)
                             if (static_cast<uint32_t>(c + i) < p.E) lrow[c + i] = __uint_as_float(r[i]);
                     }
                 }
-                const float thr = tv[KMAX - 1];
+                const float thr = fmaxf(tv[KMAX - 1], t0);  // v > thr, or v == t0 > tv[KMAX-1]
                 uint32_t hit = 0;
 #pragma unroll
                 for (int i = 0; i < 16; ++i) {
                     const float v = __uint_as_float(r[i]);
-                    m = fmaxf(m, v);
-                    hit |= static_cast<uint32_t>(v > thr) << i;
+                    hit |= static_cast<uint32_t>(v > thr || (v == t0 && v > tv[KMAX - 1])) << i;
                 }
+#ifdef MPB_ROUTER_TRACE
+                const long long c2 = clock64();
+                n_ins += __popc(hit);
+#endif
                 if (hit) {
-#pragma unroll
-                    for (int i = 0; i < 16; ++i) park[i] = __uint_as_float(r[i]);
                     while (hit) {
                         const int i = __ffs(hit) - 1;
                         hit &= hit - 1;
-                        const float v = park[i];
+                        const float v = pick16(r, i);  // register select tree, no smem round trip
                         const int e = c + i;
                         // sorted-list insertion: slot j takes slot j-1 if v goes above it
 #pragma unroll
@@ -498,7 +583,18 @@ __global__ void __launch_bounds__(kThreadsR, 1)
                         }
                     }
                 }
+#ifdef MPB_ROUTER_TRACE
+                cy_ins += clock64() - c2;
+#endif
             }
+#ifdef MPB_ROUTER_TRACE
+            if (warp == 4 && lane == 0) {
+                RTRACE(10, gtime());
+                RTRACE(13, cy_ld);
+                RTRACE(14, cy_ins);
+                RTRACE(15, n_ins);
+            }
+#endif
             float ssum = 0.f;
             if (p.score_fn == MPB_SCORE_SOFTMAX) {
                 const float mlog = m * 1.4426950408889634f;
@@ -515,6 +611,9 @@ __global__ void __launch_bounds__(kThreadsR, 1)
                     }
                 }
             }
+#ifdef MPB_ROUTER_TRACE
+            if (warp == 4 && lane == 0) RTRACE(11, gtime());
+#endif
             // ---- merge the two column halves (named barrier per lane quadrant)
             if (half == 1) {
 #pragma unroll
@@ -577,6 +676,9 @@ __global__ void __launch_bounds__(kThreadsR, 1)
                         }
                 }
                 release_tmem<PAIR>(&tempty[acc], rank, lane);
+#ifdef MPB_ROUTER_TRACE
+                if (warp == 4 && lane == 0) RTRACE(12, gtime());
+#endif
                 if (row < p.T) {
                     const float mlog = m * 1.4426950408889634f;
                     float w[KMAX];
@@ -605,6 +707,9 @@ __global__ void __launch_bounds__(kThreadsR, 1)
             }
             // half 1 must not overwrite its park row before half 0 read it
             asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
+#ifdef MPB_ROUTER_TRACE
+            if (warp == 4 && lane == 0) RTRACE(6, gtime());
+#endif
             acc ^= 1;
             if (acc == 0) aphase ^= 1;
         }
@@ -614,6 +719,7 @@ __global__ void __launch_bounds__(kThreadsR, 1)
         ptx::cluster_sync();
     else
         __syncthreads();
+    if (threadIdx.x == 0) RTRACE(7, gtime());
     if (warp == 2) {
         ptx::tc_fence_after();
         if constexpr (PAIR)
@@ -858,3 +964,14 @@ extern "C" mpb_status mpb_router_topk_layers(mpb_context *ctx, uint32_t layers, 
     CUtensorMap unused{};
     return router_dispatch(ctx, N, pair, unused, unused, p);
 }
+
+#ifdef MPB_ROUTER_TRACE
+extern "C" __attribute__((visibility("default"))) int mpb_debug_router_trace(unsigned long long *out,
+                                                                             size_t n) {
+    if (!out) {  // reset
+        static unsigned long long zeros[2 * 148 * 16] = {};
+        return cudaMemcpyToSymbol(g_router_trace, zeros, sizeof(zeros)) == cudaSuccess ? 0 : 9;
+    }
+    return cudaMemcpyFromSymbol(out, g_router_trace, n * sizeof(unsigned long long)) == cudaSuccess ? 0 : 9;
+}
+#endif

@@ -117,7 +117,7 @@ class ClockSampler:
 # ---------------------------------------------------------------- CPU reference path
 
 
-def cpu_reference_sample(spec, tokens: int, reps: int, candidates: int):
+def cpu_reference_sample(spec, tokens: int, reps: int, candidates: int, warmup: int = 1):
     """The reference's CPU implementation of the path on a bounded sample:
     numpy (BLAS, all host threads) fp32 router GEMM of bf16-rounded inputs,
     oracle top-k, the compiled reference simulate_layer (oracle/_ref) once per
@@ -179,13 +179,16 @@ def cpu_reference_sample(spec, tokens: int, reps: int, candidates: int):
         if spec.coact:
             O.coactivation(idx, E)
 
-    one()  # warm
+    for _ in range(max(1, warmup)):
+        one()  # warm
     t0 = time.perf_counter()
     for _ in range(reps):
         one()
     dt = (time.perf_counter() - t0) / reps
     kind = "reference" if R is not None else "port"
-    sample = (f"1 layer x {tokens} tokens per step (H={H}, E={E}, top-{k}): numpy fp32 router "
+    sample = (f"1 layer x {tokens} tokens per step (H={H}, E={E}, top-{k}; the workload's "
+              f"per-layer shape: its {spec.layers} layers are identical, a routed token is one "
+              f"token through one layer): numpy fp32 router "
               f"GEMM ({cores} threads) + oracle top-k + "
               f"{'reference' if R else 'oracle'} simulate_layer for {candidates} candidate "
               f"placements + oracle permutation" + (" + co-activation" if spec.coact else ""))
@@ -197,18 +200,23 @@ def run_reference_arm(args, spec):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    tokens = args.cpu_tokens
+    tokens = args.cpu_tokens or spec.tokens
     value, cores, kind, sample, dt = cpu_reference_sample(spec, tokens, max(1, args.steps),
-                                                          spec.candidates)
+                                                          spec.candidates, args.warmup)
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16-in/fp32",
             "data": "synthetic (domain-planted hidden states, random router weights)",
             "impl": "reference",
-            "config": {"workload": spec.name, "layers": 1, "tokens": tokens,
+            "config": {"workload": spec.name, "layers": spec.layers, "tokens_per_gpu": tokens,
                        "hidden": spec.hidden, "experts": spec.experts, "top_k": spec.top_k,
-                       "ep_groups": spec.groups, "nodes": spec.nodes,
-                       "candidates": spec.candidates},
+                       "ep_groups": spec.groups, "nodes": spec.nodes, "domains": spec.domains,
+                       "candidates": spec.candidates,
+                       "sample": f"each timed step routes, places and prices ONE of the "
+                                 f"{spec.layers} identical-shape layers (the metric counts "
+                                 f"token-layers, so tokens/s compares directly); a full "
+                                 f"{spec.layers}-layer step would take ~{dt * spec.layers:.0f} s "
+                                 f"on these cores"},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
                              "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
@@ -388,9 +396,19 @@ def run_gpu_arm(args, spec):
                "note": "every layer's hidden states H2D from pinned host each step (PCIe-bound); "
                        f"{n_host} distinct pinned host layers of {spec.layers}"}
 
+    a2a = None
+    if (world > 1 or args.a2a) and not args.no_a2a:
+        # config 5 beside the step: the bf16 hidden-state dispatch / combine of
+        # one DSv3 layer under the learned vs round-robin placement (GPU groups
+        # as nodes), NCCL all-to-all-v and the fused NVLink path, timed with
+        # CUDA events on its own (max over ranks); not part of `value`
+        sys.path.insert(0, str(ROOT / "tools"))
+        from bench_a2a import run as run_a2a
+        a2a = run_a2a(eng, rank, world, tokens=args.a2a_tokens, steps=5, warmup=2,
+                      modes=(("push", "pull"),))
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, cores, kind, sample, dt = cpu_reference_sample(spec, args.cpu_tokens, 3,
+        v, cores, kind, sample, dt = cpu_reference_sample(spec, args.cpu_tokens or spec.tokens, 2,
                                                           spec.candidates)
         cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample,
                "seconds_per_sample": dt}
@@ -420,7 +438,7 @@ def run_gpu_arm(args, spec):
                 "per_layer_median_bytes_saved_pct": res["per_layer_median_bytes_saved_pct"],
                 "searched_a2a_bytes_saved_pct": res["searched_bytes_saved_pct"],
                 "normalized_inter_node_bytes_per_layer_median": res["normalized"],
-                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "a2a": a2a,
                 "gpu_launches": launches, "cuda_graph": graphed, "clocks": clocks.summary()}
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -448,7 +466,12 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-tokens", type=int, default=4096)
+    ap.add_argument("--a2a", action="store_true",
+                    help="measure the config-5 dispatch/combine also at N=1 (default: N>1 only)")
+    ap.add_argument("--no-a2a", action="store_true")
+    ap.add_argument("--a2a-tokens", type=int, default=16384, help="tokens per rank (config 5)")
+    ap.add_argument("--cpu-tokens", type=int, default=0,
+                    help="tokens of the CPU sample (default: the workload's per-layer batch)")
     args = ap.parse_args()
     from paper_2604_23150_b200.pipeline import spec_for
 

@@ -60,31 +60,22 @@ def learn_placement(spec, eng):
     return strat["linear"].placement, strat["data_based"].placement, route, model
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--tokens", type=int, default=16384, help="tokens per rank")
-    ap.add_argument("--steps", type=int, default=10)
-    ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--nodes", type=int, default=2)
-    ap.add_argument("--no-p2p", action="store_true", help="skip the fused NVLink path")
-    a = ap.parse_args()
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    eng = mp.Engine(local)
-    spec = spec_for("dsv3", layers=1, tokens=a.tokens)
+def run(eng, rank: int, world: int, tokens: int = 16384, steps: int = 10, warmup: int = 3,
+        nodes: int = 2, p2p: bool = True, modes=(("push", "push"), ("push", "pull"),
+                                                 ("pull", "pull"))):
+    """Config 5 on this rank (torch.distributed already initialised when
+    world > 1): learned vs round-robin placement, NCCL all-to-all-v and the
+    fused NVLink paths; returns the per-policy results (max over ranks)."""
+    spec = spec_for("dsv3", layers=1, tokens=tokens)
     D = spec.groups
     gpr = groups_per_rank(D, world)
     lin, learned, route, model = learn_placement(spec, eng)
-    nodes = min(a.nodes, world) if world > 1 else 1
+    nodes = min(nodes, world) if world > 1 else 1
     top = mp.Topology.contiguous(D, 1, D, 1, spec.nodes)
     # global request pool with seeded random domains (uncorrelated with the
     # batch position that the round-robin baseline uses), tpr tokens each
     tpr = spec.tokens_per_request
-    R_glob = world * (a.tokens // tpr)
+    R_glob = world * (tokens // tpr)
     dom_g = np.random.default_rng(2024).integers(0, spec.domains, R_glob)
     results = {}
     for policy, placement in (("round_robin", lin), ("learned", learned)):
@@ -108,22 +99,24 @@ def main():
                                nodes)
 
         def timed(fn):
-            for _ in range(a.warmup):
+            for _ in range(warmup):
                 Y = fn(None)
             torch.cuda.synchronize()
             if world > 1:
                 dist.barrier()
-            st = A2AStats()
             s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            s.record()
-            for i in range(a.steps):
-                fn(st if i == 0 else None)
-            e.record()
+            s.record(eng.stream)
+            for i in range(steps):
+                fn(None)
+            e.record(eng.stream)
             torch.cuda.synchronize()
-            ms = torch.tensor([s.elapsed_time(e) / a.steps], device=eng.device,
+            ms = torch.tensor([s.elapsed_time(e) / steps], device=eng.device,
                               dtype=torch.float64)
             if world > 1:
                 dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+            st = A2AStats()  # row accounting on an untimed call (reads counts on the host)
+            fn(st)
+            torch.cuda.synchronize()
             return Y, float(ms.item()), st
 
         Y, ms, st = timed(lambda st_: op(X, idx, w, src, st_))
@@ -134,13 +127,14 @@ def main():
         if world > 1:
             dist.all_reduce(tot)
         sent, inter, intra = (int(x) for x in tot.tolist())
-        results[policy] = dict(ms_per_step=ms, rows=sent, inter_node_rows=inter,
+        results[policy] = dict(nccl_ms_per_layer=ms, rows=sent, inter_node_rows=inter,
                                intra_node_rows=intra,
+                               wire_bytes=sent * spec.hidden * 2 * 2,
                                inter_node_bytes=inter * spec.hidden * 2,
                                inter_fraction=inter / max(1, sent), max_abs_err=err,
                                tokens_per_rank=T)
-        if not a.no_p2p:  # fused NVLink path: same output bit for bit
-            for dmode, mode in (("push", "push"), ("push", "pull"), ("pull", "pull")):
+        if p2p:  # fused NVLink path: same output bit for bit
+            for dmode, mode in modes:
                 op.enable_p2p(2 * T * spec.top_k, combine=mode, dispatch=dmode, max_tokens=T)
                 op.phase_events = None
                 Yp, ms_p, _ = timed(lambda st_: op(X, idx, w, src, st_))
@@ -164,15 +158,36 @@ def main():
                 same = torch.tensor([int(torch.equal(Yp, Y))], device=eng.device)
                 if world > 1:
                     dist.all_reduce(same, op=dist.ReduceOp.MIN)
-                results[policy].update({f"p2p_{tag}_ms_per_step": ms_p,
+                results[policy].update({f"p2p_{tag}_ms_per_layer": ms_p,
                                         f"p2p_{tag}_bit_identical": bool(same.item())})
+        del op, X, idx, w
+        torch.cuda.empty_cache()
+    base = results["round_robin"]["inter_node_bytes"]
+    saved = 1.0 - results["learned"]["inter_node_bytes"] / base if base else float("nan")
+    return {"config": "ep8-bf16-dispatch-combine", "n_gpus": world, "gpu_nodes": nodes,
+            "hidden": spec.hidden, "experts": spec.experts, "top_k": spec.top_k,
+            "tokens_per_rank": tokens, "results": results,
+            "cross_node_bytes_saved_pct": 100.0 * saved}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--tokens", type=int, default=16384, help="tokens per rank")
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--nodes", type=int, default=2)
+    ap.add_argument("--no-p2p", action="store_true", help="skip the fused NVLink path")
+    a = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    eng = mp.Engine(local)
+    res = run(eng, rank, world, a.tokens, a.steps, a.warmup, a.nodes, not a.no_p2p)
     if rank == 0:
-        base = results["round_robin"]["inter_node_bytes"]
-        saved = 1.0 - results["learned"]["inter_node_bytes"] / base if base else float("nan")
-        print(json.dumps({"config": "ep8-bf16-dispatch-combine", "n_gpus": world,
-                          "gpu_nodes": nodes, "hidden": spec.hidden, "experts": spec.experts,
-                          "top_k": spec.top_k, "results": results,
-                          "cross_node_bytes_saved_pct": 100.0 * saved}), flush=True)
+        print(json.dumps(res), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()

@@ -288,6 +288,71 @@ def run_e2e(pipe, steps: int):
     return dt, h2d, d2h, n_host
 
 
+def tail_roofline(pipe, hbm_gbs: float, iters: int = 20):
+    """HBM roofline of the statistics / scoring kernels (K2, K3, K4, K5) of the
+    step, each timed alone on the whole GPU on the pipeline's own buffers
+    (scratch outputs; CUDA events around `iters` pre-queued launches). In the
+    step they run on the side stream beside the routers; these are their
+    isolated times. Algorithmic bytes per launch are what the kernel must
+    read and write."""
+    import torch
+
+    from paper_2604_23150_b200 import moeplace as mp
+    s = pipe.spec
+    T, k, E, D, L = s.tokens, s.top_k, s.experts, s.groups, s.layers
+    eng = mp.Engine(pipe.eng.device.index)
+    idx = pipe.idx_buf[min(pipe.sim_layer, len(pipe.idx_buf) - 1)] if hasattr(pipe, "idx_buf") \
+        else pipe.idx
+    u64 = lambda *sh: torch.zeros(*sh, dtype=torch.uint64, device=eng.device)  # noqa: E731
+    dem, dem2, pop, co = u64(D, E), u64(D, E), u64(s.domains, E), u64(E, E)
+    sp, pp = torch.empty_like(pipe.sp), torch.empty_like(pipe.pp)
+    ko = torch.empty_like(pipe.ko)
+    P = pipe.luts_cl.shape[0]
+    sc = (u64(P, L), u64(P, L), u64(P, L, D))
+    fin = (torch.empty(P * L, 6, dtype=torch.float64, device=eng.device),
+           torch.empty(P * L, D, dtype=torch.float64, device=eng.device))
+    nodes = pipe.luts_cl.shape[1]
+    cases = {
+        "K2+K3 dispatch_layout (histograms + permutation)": (
+            lambda: eng.dispatch_layout(idx, pipe.dp_deployed, src=pipe.src_cl, tag=pipe.dom_tok,
+                                        n_tags=s.domains, demand=dem, tag_pop=pop,
+                                        perm_out=(sp, pp, ko), src2=pipe.src_rr, demand2=dem2),
+            T * (4 * k + 1 + 1 + 2) + 2 * 4 * T * k + (D * E + 1) * 8 + 2 * D * E * 8),
+        "K2 dispatch_layout (histograms only)": (
+            lambda: eng.dispatch_layout(idx, pipe.dp_deployed, src=pipe.src_cl, tag=pipe.dom_tok,
+                                        n_tags=s.domains, permutation=False, demand=dem,
+                                        tag_pop=pop, src2=pipe.src_rr, demand2=dem2),
+            T * (4 * k + 1 + 1 + 2) + 2 * D * E * 8),
+    }
+    if s.coact:
+        cases["K4 coactivation (tcgen05 kind::i8)"] = (
+            lambda: eng.coactivation(idx, E, out=co), 4 * T * k + E * E * 8)
+    cases[f"K5 score_placements_finalize ({P} candidates x {L} layers)"] = (
+        lambda: eng.score_and_finalize(pipe.dem_cl, pipe.luts_cl, pipe.g2n, D, pipe.cost,
+                                       pipe.topology, row_node=pipe.g2n, out=sc, fin_out=fin[0],
+                                       payload=fin[1]),
+        L * D * E * 8 + P * nodes * E + P * L * (2 + D) * 8 + P * L * (6 + D) * 8)
+    out = {}
+    for name, (fn, byts) in cases.items():
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(eng.stream):
+            torch.cuda._sleep(int(3e7))  # the host queues the launches while the GPU sleeps
+        a.record(eng.stream)
+        for _ in range(iters):
+            fn()
+        b.record(eng.stream)
+        torch.cuda.synchronize()
+        us = a.elapsed_time(b) / iters * 1e3
+        gbs = byts / (us * 1e-6) / 1e9
+        out[name] = {"us_per_launch": us, "algorithmic_bytes": byts, "achieved_gbs": gbs,
+                     "frac_of_hbm": gbs / hbm_gbs}
+    eng.sync()
+    return out
+
+
 def run_gpu_arm(args, spec):
     import torch
     import torch.distributed as dist
@@ -384,6 +449,9 @@ def run_gpu_arm(args, spec):
                 "hbm_achieved_gbs": achieved_gbs, "hbm_frac": achieved_gbs / hbm,
                 "ms_per_launch": r_ms, "share_of_step": share}
 
+    roofline["tail"] = tail_roofline(pipe, hbm)
+    roofline["tail_note"] = ("K2-K5 each timed alone on the whole GPU (in the step they run on "
+                             "the side stream beside the routers); latency-bound at these sizes")
     e2e = None
     if not args.no_e2e:
         dt, h2d, d2h, n_host = run_e2e(pipe, args.e2e_steps)

@@ -152,6 +152,24 @@ def run(eng, rank: int, world: int, tokens: int = 16384, steps: int = 10, warmup
                 C = op.cnt.view(world, world).double()
                 recv_rows = C.sum(0)
                 results[policy]["recv_rows_max_over_mean"] = float(recv_rows.max() / recv_rows.mean())
+                if world > 1:
+                    # NVLink roofline: rows crossing ranks (the count matrix off the
+                    # diagonal; the most loaded rank) x 2H bytes over each phase's
+                    # time, against the measured 770 GB/s peer copy per direction
+                    # (B200_PROFILING.md; nominal 900)
+                    off = C.clone()
+                    off.fill_diagonal_(0)
+                    row_b = spec.hidden * 2
+                    send_b = float(off.sum(1).max()) * row_b
+                    recv_b = float(off.sum(0).max()) * row_b
+                    results[policy][f"p2p_{tag}_nvlink"] = {
+                        "dispatch_bytes_per_rank_max": recv_b,
+                        "dispatch_gbs": recv_b / (ph[1] * 1e-3) / 1e9,
+                        "combine_bytes_per_rank_max": send_b,
+                        "combine_gbs": send_b / (ph[2] * 1e-3) / 1e9,
+                        "peak_gbs": 770.0, "peak_kind": "measured peer copy per direction",
+                        "dispatch_frac": recv_b / (ph[1] * 1e-3) / 1e9 / 770.0,
+                        "combine_frac": send_b / (ph[2] * 1e-3) / 1e9 / 770.0}
                 results[policy][f"p2p_{tag}_phase_ms"] = {
                     "counts": float(ph[0]), "dispatch": float(ph[1]), "combine": float(ph[2])}
                 eng.sync()

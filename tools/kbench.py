@@ -9,8 +9,10 @@ import torch  # noqa: E402
 from paper_2604_23150_b200 import moeplace as mp  # noqa: E402
 
 T, E, k, D, L, P = 65536, 256, 8, 8, 58, 1022
-SMS = int(sys.argv[1]) if len(sys.argv) > 1 else 0  # SM budget (the side context's, e.g. 20)
-CONFINE = len(sys.argv) > 2 and sys.argv[2] == "confined"  # run inside an SM partition
+ONCE = "--once" in sys.argv  # each case launched once, untimed (for ncu captures)
+argv = [a for a in sys.argv[1:] if a != "--once"]
+SMS = int(argv[0]) if argv else 0  # SM budget (the side context's, e.g. 20)
+CONFINE = len(argv) > 1 and argv[1] == "confined"  # run inside an SM partition
 if CONFINE:
     part = mp.SmPartition(0, SMS)
     torch.cuda.set_stream(part.side)
@@ -64,6 +66,13 @@ cases = {
                                                out[2].view(-1, D), D, cost, top, out=fin[0],
                                                payload=fin[1]),
 }
+if ONCE:
+    for name, fn in cases.items():
+        fn()
+        torch.cuda.synchronize()
+        print(f"{name}: launched once")
+    eng.sync()
+    sys.exit(0)
 for name, fn in cases.items():
     for _ in range(3):
         fn()

@@ -1,22 +1,39 @@
 #!/bin/bash
-# One profiling pass on a B200 (run under gpurun from the repo root).
-# Outputs under gpurun_out/; summarised into profiles/ by tools/summarize_profiles.py.
+# One profiling pass on a B200 (run under gpurun from the repo root):
+#   /usr/local/graft/bin/gpurun --timeout 3000 -- 'bash tools/profile_round.sh'
+# Outputs under gpurun_out/prof/; summarised into profiles/ by
+#   python tools/summarize_profiles.py r02
+# Every ncu command runs only after the same command exited 0 without ncu.
 set -x
 OUT=gpurun_out/prof
 mkdir -p $OUT
-# 1. the bench line (plain, no profiler)
-python bench.py > $OUT/bench_n1.json 2> $OUT/bench_n1.err
-# 2. launch list of the same command (shortened: shares, not absolutes)
-CMD="python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline"
-$CMD > $OUT/plain_short.log 2>&1 && \
-ncu --metrics gpu__time_duration.sum --clock-control none --csv \
-    --log-file $OUT/launches.csv $CMD > $OUT/ncu_launches.log 2>&1
-# 3. full captures of the top kernels (1 launch each, after their plain runs exited 0)
-python tools/prof_router.py --iters 1 > $OUT/router_plain.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:k_router -s 2 -c 1 \
-    -o $OUT/router_full python tools/prof_router.py --iters 1 > $OUT/ncu_router.log 2>&1
-python tools/kbench.py > $OUT/kbench_plain.log 2>&1 && \
+# 1. plain bench lines (no profiler), one per BASELINE workload
+for W in dsv3 qwen3 maverick domain; do
+  python bench.py --workload $W > $OUT/bench_$W.json 2> $OUT/bench_$W.err
+done
+# 2. launch lists of the same commands (shortened: shares, not absolutes)
+for W in dsv3 qwen3; do
+  CMD="python bench.py --workload $W --steps 2 --warmup 1 --no-e2e --no-cpu-baseline --no-a2a"
+  $CMD > $OUT/plain_$W.log 2>&1 && \
+  ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+      --log-file $OUT/launches_$W.csv $CMD > $OUT/ncu_launches_$W.log 2>&1
+done
+# 3. router: full capture of one launch per workload shape (+ cuBLAS timing line)
+declare -A SHAPE=( [dsv3]="--T 65536 --H 7168 --E 256 --k 8 --fn 1"
+                   [qwen3]="--T 4096 --H 4096 --E 128 --k 8 --fn 0"
+                   [maverick]="--T 1048576 --H 5120 --E 128 --k 1 --fn 1"
+                   [domain]="--T 1048576 --H 4096 --E 128 --k 8 --fn 0" )
+for W in dsv3 qwen3 maverick domain; do
+  python tools/prof_router.py ${SHAPE[$W]} --iters 5 > $OUT/router_plain_$W.log 2>&1 && \
+  ncu --set full --clock-control none --import-source on -k regex:k_router -s 2 -c 1 \
+      -o $OUT/router_$W python tools/prof_router.py ${SHAPE[$W]} --iters 1 > $OUT/ncu_router_$W.log 2>&1
+done
+python tools/prof_router.py --layers 8 --iters 5 > $OUT/router_grouped_plain.log 2>&1
+# 4. statistics / scoring kernels: full captures at the DSv3 step shape (tools/kbench.py),
+#    the co-activation tcgen05 kernel and the scorer included
+python tools/kbench.py > $OUT/kbench_plain.log 2>&1
+python tools/kbench.py --once > $OUT/kbench_once.log 2>&1 && \
 ncu --set full --clock-control none --import-source on \
-    -k regex:"k_layout_count|k_layout_scatter|k_layout_scan|k_coact_partial|k_score|k_finalize" \
-    -s 6 -c 8 -o $OUT/small_full python tools/kbench.py > $OUT/ncu_small.log 2>&1
+    -k regex:"k_layout_count|k_layout_scan|k_layout_scatter|k_coact_mma|k_score|k_finalize" \
+    -c 20 -o $OUT/small_full python tools/kbench.py --once > $OUT/ncu_small.log 2>&1
 ls -la $OUT

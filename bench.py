@@ -505,6 +505,11 @@ def run_gpu_arm(args, spec):
                     "seed": ref_stat["seed"], "normalized_median": ref_stat["normalized"]},
                 "per_layer_median_bytes_saved_pct": res["per_layer_median_bytes_saved_pct"],
                 "searched_a2a_bytes_saved_pct": res["searched_bytes_saved_pct"],
+                "placement_search": {
+                    "what": "K5-priced inter-node pairs over all layers on the calibration "
+                            "demand (lower is better): the candidate pool and the greedy "
+                            "swap search from its best replica-free entry",
+                    "inter_node_pairs": getattr(pipe, "search_report", None)},
                 "normalized_inter_node_bytes_per_layer_median": res["normalized"],
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "a2a": a2a,
                 "gpu_launches": launches, "cuda_graph": graphed, "clocks": clocks.summary()}

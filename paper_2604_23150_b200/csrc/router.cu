@@ -27,7 +27,9 @@
 
 #include <cfloat>
 #include <cstdlib>
+#include <map>
 #include <mutex>
+#include <tuple>
 
 #include "internal.cuh"
 #include "tc_ptx.cuh"
@@ -69,7 +71,7 @@ struct RCfg {
     static constexpr int BUDGET = 232448 - 1024 - PARK - 256;
     static constexpr int STAGES = BUDGET / STAGE > MPB_ROUTER_STAGES_CAP ? MPB_ROUTER_STAGES_CAP
                                                                          : BUDGET / STAGE;
-    static constexpr int SMEM = 1024 + STAGES * STAGE + PARK + (2 * STAGES + 4) * 8 + 16;
+    static constexpr int SMEM = 1024 + STAGES * STAGE + PARK + (2 * STAGES + 6) * 8 + 16;
 };
 
 #ifdef MPB_ROUTER_TRACE
@@ -112,6 +114,9 @@ struct RouterParams {
     const CUtensorMap *maps;
     uint32_t tiles_per_layer;
     uint32_t layers;
+    // split-K tail through distributed shared memory (single-CTA tiles): the S
+    // K-part units of a tail tile form one cluster (cluster_tail != 0)
+    uint32_t cluster_tail;
 };
 
 // Work item n of a scheduling unit: full waves of whole tiles, then (split
@@ -159,6 +164,287 @@ __device__ __forceinline__ float pick16(const uint32_t (&r)[16], int i) {
     return __uint_as_float((i & 8) ? c[1] : c[0]);
 }
 
+// (v, id) ranks before (w, jd): larger logit, equal logits -> lower expert id.
+__device__ __forceinline__ bool ranks_before(float v, int id, float w, int jd) {
+    return v > w || (v == w && id < jd);
+}
+
+// Split-K tail through distributed shared memory (single-CTA tiles, PAIR off).
+// The S = p.splits K-part units of a tail tile are one cluster; CTA h (K part
+// h, cluster rank h) ends with rows [h*RPS, (h+1)*RPS) of the tile (RPS =
+// 128/S), i.e. a reduce-scatter of the fp32 partial accumulators:
+//   1. once its own MMAs are done (its pipeline smem is free) every CTA tells
+//      its peers so (remote mbarrier arrive);
+//   2. each epilogue warp pushes the TMEM rows it does not own into the
+//      owner's shared memory with st.async (completion counted in bytes on the
+//      owner's mbarrier) — no global memory, no flags, no fences;
+//   3. the owner sums its rows in K-part order 0..S-1 (the fp32 order of the
+//      global-memory tail) into a shared-memory tile;
+//   4. all 8 epilogue warps select top-k for the RPS rows from shared memory:
+//      TPR = 256/RPS threads per row, each a column slice; a lower bound t0 on
+//      the k-th logit (minimum of >= KMAX group maxima) filters the insertions;
+//      the TPR partial lists merge over warp shuffles (top half of A u rev(B),
+//      then a bitonic clean-up: static register indices only).
+// The whole 128-row epilogue of a decode batch's tiles is thus spread over the S
+// CTAs and over 8 warps per row group instead of 2.
+template <int N, int KMAX>
+__device__ __forceinline__ void cluster_tail(const RouterParams &p, const WorkItem &it,
+                                             uint32_t taddr_q, uint8_t *stage_base,
+                                             uint64_t *peer_free, uint64_t *rx_full, uint32_t warp,
+                                             uint32_t lane, uint64_t row_tile0, uint64_t out_row_tile0) {
+    const uint32_t S = p.splits, h = it.part;
+    const uint32_t RPS = 128u / S;
+    constexpr uint32_t RS = N + 4;  // padded row stride (floats): conflict-free 16-byte stores
+    constexpr int NH = N / 2;
+    float *rx = reinterpret_cast<float *>(stage_base);                  // [S-1][RPS][RS]
+    float *tile = rx + static_cast<size_t>(S - 1) * RPS * RS;            // [RPS][RS]
+    float *snd = tile + static_cast<size_t>(RPS) * RS;                   // [S-1][RPS][RS]
+    const uint32_t t = threadIdx.x - 128u;                               // epilogue thread 0..255
+    const uint32_t q = warp & 3, half = (warp - 4) >> 2;
+    const uint32_t share_bytes = RPS * RS * 4u;  // one row share, padded rows, contiguous
+    if (t == 0) {
+        ptx::mbar_arrive_expect_tx(rx_full, (S - 1) * share_bytes);
+        for (uint32_t c = 0; c < S; ++c)
+            if (c != h) ptx::mbar_arrive_remote(ptx::mapa(ptx::smem_u32(peer_free), c));
+    }
+    const uint32_t owner = q * S / 4u;
+    const uint32_t rloc = q * 32u + lane - owner * RPS;  // row within the owner's share
+    if (owner != h) {  // stage the rows other CTAs own (local, conflict-free 16-byte stores)
+        const uint32_t i = owner < h ? owner : owner - 1;
+        float *dst = snd + (static_cast<size_t>(i) * RPS + rloc) * RS;
+#pragma unroll 1
+        for (int c = half * NH; c < (half + 1) * NH; c += 16) {
+            uint32_t r[16];
+            ptx::tmem_ld_32x32b_x16(taddr_q + c, r);
+            ptx::tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                *reinterpret_cast<float4 *>(dst + c + 4 * j) =
+                    make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                                __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
+        }
+        ptx::fence_proxy_async_smem();  // generic writes -> visible to the bulk-copy engine
+    }
+    asm volatile("bar.sync 5, 256;" ::: "memory");  // every share staged
+    if (t == 0) {
+        ptx::mbar_wait_cluster(peer_free, 0);  // every peer's pipeline smem is free
+        for (uint32_t o = 0; o < S; ++o) {
+            if (o == h) continue;
+            const uint32_t i = o < h ? o : o - 1;  // my share slot for owner o / my slot at o
+            const uint32_t j = h < o ? h : h - 1;
+            ptx::bulk_s2s(ptx::mapa(ptx::smem_u32(rx + static_cast<size_t>(j) * RPS * RS), o),
+                          ptx::smem_u32(snd + static_cast<size_t>(i) * RPS * RS), share_bytes,
+                          ptx::mapa(ptx::smem_u32(rx_full), o));
+        }
+    }
+    if (owner == h) {
+        ptx::mbar_wait_cluster(rx_full, 0);  // the peers' partials of my rows have landed
+#pragma unroll 1
+        for (int c = half * NH; c < (half + 1) * NH; c += 16) {
+            uint32_t r[16];
+            ptx::tmem_ld_32x32b_x16(taddr_q + c, r);
+            ptx::tmem_ld_wait();
+#pragma unroll
+            for (int j4 = 0; j4 < 4; ++j4) {
+                float4 tot;
+#pragma unroll 1
+                for (uint32_t part = 0; part < S; ++part) {  // K-part order: fixed fp32 sum order
+                    float4 v;
+                    if (part == h) {
+                        v = make_float4(__uint_as_float(r[4 * j4]), __uint_as_float(r[4 * j4 + 1]),
+                                        __uint_as_float(r[4 * j4 + 2]), __uint_as_float(r[4 * j4 + 3]));
+                    } else {
+                        const uint32_t i = part < h ? part : part - 1;
+                        v = *reinterpret_cast<const float4 *>(rx + (static_cast<size_t>(i) * RPS + rloc) * RS + c + 4 * j4);
+                    }
+                    if (part == 0) {
+                        tot = v;
+                    } else {
+                        tot.x += v.x;
+                        tot.y += v.y;
+                        tot.z += v.z;
+                        tot.w += v.w;
+                    }
+                }
+                *reinterpret_cast<float4 *>(tile + static_cast<size_t>(rloc) * RS + c + 4 * j4) = tot;
+            }
+        }
+    }
+    asm volatile("bar.sync 5, 256;" ::: "memory");  // the owned rows are summed
+#ifdef MPB_ROUTER_TRACE
+    if (t == 0) RTRACE(5, gtime());
+#endif
+    // ---- top-k of the RPS owned rows from shared memory, TPR threads per row
+    const uint32_t TPR = 256u / RPS;          // 8 (S = 4) or 4 (S = 2)
+    const uint32_t r = t / TPR, sub = t % TPR;
+    const uint32_t CW = N / TPR;              // columns per thread (multiple of 8)
+    const float *row = tile + static_cast<size_t>(r) * RS;
+    const uint64_t token = row_tile0 + h * RPS + r;
+    const uint64_t out_row = out_row_tile0 + h * RPS + r;
+    const uint32_t c0 = sub * CW;
+    // pass 1: max and the k-th-logit lower bound t0 (groups: >= KMAX over the row)
+    const uint32_t G = KMAX > static_cast<int>(TPR) ? KMAX / TPR : 1u;  // groups per thread
+    const uint32_t GSZ = CW / G;
+    float m = -INFINITY, t0 = INFINITY;
+    for (uint32_t g = 0; g < G; ++g) {
+        float gm = -INFINITY;
+        for (uint32_t c = c0 + g * GSZ; c < c0 + (g + 1) * GSZ; c += 4) {
+            const float4 v = *reinterpret_cast<const float4 *>(row + c);
+            if (c < p.E) gm = fmaxf(gm, v.x);
+            if (c + 1 < p.E) gm = fmaxf(gm, v.y);
+            if (c + 2 < p.E) gm = fmaxf(gm, v.z);
+            if (c + 3 < p.E) gm = fmaxf(gm, v.w);
+        }
+        t0 = fminf(t0, gm);
+        m = fmaxf(m, gm);
+    }
+    for (uint32_t o = 1; o < TPR; o <<= 1) {
+        t0 = fminf(t0, __shfl_xor_sync(0xffffffffu, t0, o));
+        m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    }
+    if (KMAX == 1) t0 = m;
+    // pass 2: local top-KMAX of the slice (ascending ids: equal logits keep the lower id)
+#ifdef MPB_ROUTER_TRACE
+    if (t == 0) RTRACE(10, gtime());
+#endif
+    float tv[KMAX];
+    int ti[KMAX];
+#pragma unroll
+    for (int j = 0; j < KMAX; ++j) {
+        tv[j] = -INFINITY;
+        ti[j] = 0x7FFFFFFF;
+    }
+    for (uint32_t c = c0; c < c0 + CW; c += 8) {
+        uint32_t rr[16];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const float4 v = *reinterpret_cast<const float4 *>(row + c + 4 * j);
+            rr[4 * j] = __float_as_uint(v.x);
+            rr[4 * j + 1] = __float_as_uint(v.y);
+            rr[4 * j + 2] = __float_as_uint(v.z);
+            rr[4 * j + 3] = __float_as_uint(v.w);
+        }
+#pragma unroll
+        for (int j = 8; j < 16; ++j) rr[j] = __float_as_uint(-INFINITY);
+        uint32_t hit = 0;
+        const float thr = fmaxf(tv[KMAX - 1], t0);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const float v = __uint_as_float(rr[i]);
+            const bool real = c + i < p.E;
+            hit |= static_cast<uint32_t>(real && (v > thr || (v == t0 && v > tv[KMAX - 1]))) << i;
+        }
+        while (hit) {
+            const int i = __ffs(hit) - 1;
+            hit &= hit - 1;
+            const float v = pick16(rr, i);
+            const int e = static_cast<int>(c) + i;
+#pragma unroll
+            for (int j = KMAX - 1; j >= 0; --j) {
+                const bool here = v > tv[j];
+                const bool above = j > 0 && v > tv[j > 0 ? j - 1 : 0];
+                tv[j] = above ? tv[j > 0 ? j - 1 : 0] : (here ? v : tv[j]);
+                ti[j] = above ? ti[j > 0 ? j - 1 : 0] : (here ? e : ti[j]);
+            }
+        }
+    }
+    // merge the TPR sorted lists: top-KMAX of A u B = pairwise best of A[j], B[K-1-j]
+    // (a bitonic sequence), sorted by half-cleaners
+#ifdef MPB_ROUTER_TRACE
+    if (t == 0) RTRACE(11, gtime());
+#endif
+    for (uint32_t o = 1; o < TPR; o <<= 1) {
+        float bv[KMAX];
+        int bi[KMAX];
+#pragma unroll
+        for (int j = 0; j < KMAX; ++j) {
+            bv[j] = __shfl_xor_sync(0xffffffffu, tv[j], o);
+            bi[j] = __shfl_xor_sync(0xffffffffu, ti[j], o);
+        }
+#pragma unroll
+        for (int j = 0; j < KMAX; ++j) {
+            const bool a = ranks_before(tv[j], ti[j], bv[KMAX - 1 - j], bi[KMAX - 1 - j]);
+            tv[j] = a ? tv[j] : bv[KMAX - 1 - j];
+            ti[j] = a ? ti[j] : bi[KMAX - 1 - j];
+        }
+#pragma unroll
+        for (int d = KMAX / 2; d >= 1; d >>= 1)
+#pragma unroll
+            for (int j = 0; j < KMAX; ++j)
+                if ((j & d) == 0) {
+                    const bool a = ranks_before(tv[j], ti[j], tv[j + d], ti[j + d]);
+                    const float xv = a ? tv[j] : tv[j + d], yv = a ? tv[j + d] : tv[j];
+                    const int xi = a ? ti[j] : ti[j + d], yi = a ? ti[j + d] : ti[j];
+                    tv[j] = xv;
+                    tv[j + d] = yv;
+                    ti[j] = xi;
+                    ti[j + d] = yi;
+                }
+    }
+    // softmax denominator over the row (shuffle tree over the TPR slices)
+#ifdef MPB_ROUTER_TRACE
+    if (t == 0) RTRACE(12, gtime());
+#endif
+    float ssum = 0.f;
+    if (p.score_fn == MPB_SCORE_SOFTMAX) {
+        const float mlog = m * 1.4426950408889634f;
+        for (uint32_t c = c0; c < c0 + CW; ++c) {
+            const float v = row[c];
+            ssum += (c < p.E && v == v) ? exp2f(fmaf(v, 1.4426950408889634f, -mlog)) : 0.f;
+        }
+        for (uint32_t o = 1; o < TPR; o <<= 1) ssum += __shfl_xor_sync(0xffffffffu, ssum, o);
+    }
+    if (p.logits && token < p.T)
+        for (uint32_t c = c0; c < c0 + CW && c < p.E; ++c) p.logits[out_row * p.E + c] = row[c];
+    if (sub != 0 || token >= p.T) return;
+#ifdef MPB_ROUTER_TRACE
+    if (t == 0) RTRACE(13, gtime());
+#endif
+    const int k = static_cast<int>(p.k);
+    int last = ti[0];  // ti[k - 1] without a dynamic register index (local memory)
+#pragma unroll
+    for (int j = 1; j < KMAX; ++j)
+        if (j == k - 1) last = ti[j];
+    if (last == 0x7FFFFFFF) {
+        // fewer than k logits above -inf: fill with -inf ids, then NaN ids, ascending
+        for (int pass = 0; pass < 2; ++pass)
+            for (uint32_t c = 0; c < p.E; ++c) {
+                const float v = row[c];
+                const bool want = pass == 0 ? v == -INFINITY : v != v;
+                if (!want) continue;
+                bool placed = false;
+#pragma unroll
+                for (int j = 0; j < KMAX; ++j)
+                    if (!placed && j < k && ti[j] == 0x7FFFFFFF) {
+                        ti[j] = static_cast<int>(c);
+                        tv[j] = v;
+                        placed = true;
+                    }
+            }
+    }
+    const float mlog = m * 1.4426950408889634f;
+    float w[KMAX];
+    float wsum = 0.f;
+#pragma unroll
+    for (int j = 0; j < KMAX; ++j) {
+        float x = 0.f;
+        if (j < k && !isnan(tv[j]))
+            x = p.score_fn == MPB_SCORE_SOFTMAX ? exp2f(fmaf(tv[j], 1.4426950408889634f, -mlog)) / ssum
+                                                : 1.f / (1.f + expf(-tv[j]));
+        w[j] = x;
+        wsum += x;
+    }
+#pragma unroll
+    for (int j = 0; j < KMAX; ++j) {
+        if (j >= k) continue;
+        p.idx[out_row * p.k + j] = ti[j];
+        p.w[out_row * p.k + j] = p.renorm ? (wsum > 0.f ? w[j] / wsum : 0.f) : w[j];
+    }
+#ifdef MPB_ROUTER_TRACE
+    if (t == 0) RTRACE(6, gtime());
+#endif
+}
+
 // Hands an accumulator's TMEM back to the MMA issuer after this thread's
 // tcgen05.ld reads: single CTA — every epilogue thread arrives; pair — one lane
 // per warp arrives on the LEADER's barrier (locally or through DSMEM).
@@ -202,7 +488,9 @@ __global__ void __launch_bounds__(kThreadsR, 1)
     uint64_t *empty = full + S;
     uint64_t *tfull = empty + S;
     uint64_t *tempty = tfull + 2;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+    uint64_t *peer_free = tempty + 2;  // cluster tail: peers' pipeline smem is free (S-1 arrivals)
+    uint64_t *rx_full = peer_free + 1;  // cluster tail: peers' partials of my rows (tx bytes)
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(rx_full + 1);
 
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = PAIR ? ptx::cluster_ctarank() : 0u;
@@ -221,6 +509,10 @@ __global__ void __launch_bounds__(kThreadsR, 1)
             // warp of both CTAs arrives on the leader's barrier
             ptx::mbar_init(&tempty[a], PAIR ? 16 : 256);
         }
+        if (!PAIR && p.cluster_tail) {
+            ptx::mbar_init(peer_free, p.splits - 1);
+            ptx::mbar_init(rx_full, 1);
+        }
         ptx::fence_barrier_init();
     }
     if (warp == 2) {
@@ -230,8 +522,8 @@ __global__ void __launch_bounds__(kThreadsR, 1)
             ptx::tmem_alloc<Cfg::TMEM_COLS>(tmem_slot);
     }
     ptx::tc_fence_before();
-    if constexpr (PAIR)
-        ptx::cluster_sync();
+    if (PAIR || p.cluster_tail)
+        ptx::cluster_sync();  // barrier inits visible to the peers before any remote arrive
     else
         __syncthreads();
     ptx::tc_fence_after();
@@ -407,6 +699,15 @@ __global__ void __launch_bounds__(kThreadsR, 1)
             }
 #endif
             const uint32_t layer = it.tile / p.tiles_per_layer;
+            if (!PAIR && it.role != 0 && p.cluster_tail) {
+                const uint64_t r0 = static_cast<uint64_t>(it.tile - layer * p.tiles_per_layer) * Cfg::ROWS_PER_TILE;
+                cluster_tail<N, KMAX>(p, it, tmem_base + acc * N + ((q * 32) << 16), base, peer_free,
+                                      rx_full, warp, lane, r0, static_cast<uint64_t>(layer) * p.T + r0);
+                release_tmem<PAIR>(&tempty[acc], rank, lane);
+                acc ^= 1;
+                if (acc == 0) aphase ^= 1;
+                continue;
+            }
             const uint64_t row = static_cast<uint64_t>(it.tile - layer * p.tiles_per_layer) * Cfg::ROWS_PER_TILE +
                                  rank * kBM + row_in_tile;  // token within the layer
             const uint64_t out_row = static_cast<uint64_t>(layer) * p.T + row;
@@ -715,7 +1016,7 @@ __global__ void __launch_bounds__(kThreadsR, 1)
         }
     }
     ptx::tc_fence_before();
-    if constexpr (PAIR)
+    if (PAIR || p.cluster_tail)
         ptx::cluster_sync();
     else
         __syncthreads();
@@ -761,6 +1062,35 @@ bool make_map(CUtensorMap *map, const void *ptr, uint64_t rows, uint64_t cols, u
     return r == CUDA_SUCCESS;
 }
 
+// How many clusters of S CTAs of this kernel can be resident at once (the
+// split tail's CTAs wait on each other, so its units must all be resident);
+// cached per (kernel, S).
+template <typename K>
+uint32_t max_active_clusters(K kern, int smem, uint32_t S) {
+    static std::mutex mu;
+    static std::map<std::pair<const void *, uint32_t>, uint32_t> cache;
+    std::lock_guard<std::mutex> lock(mu);
+    const auto key = std::make_pair(reinterpret_cast<const void *>(kern), S);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute attr[1];
+    cfg.gridDim = dim3(S * 64);
+    cfg.blockDim = dim3(kThreadsR);
+    cfg.dynamicSmemBytes = smem;
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = S;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) n = 0;
+    cudaGetLastError();
+    cache[key] = static_cast<uint32_t>(n);
+    return static_cast<uint32_t>(n);
+}
+
 template <int N, int KMAX, bool PAIR>
 mpb_status launch_router_n(mpb_context *ctx, const CUtensorMap &mx, const CUtensorMap &mw,
                            RouterParams p) {
@@ -797,8 +1127,28 @@ mpb_status launch_router_n(mpb_context *ctx, const CUtensorMap &mx, const CUtens
         S = std::min(S, std::max<uint32_t>(nk / kMinPartK, nk >= 2 ? 2u : 1u));
         if (S < 2 || nk < 2) S = 1;
     }
+    // single-CTA tiles: the split tail runs through distributed shared memory,
+    // the S K parts of a tile in one cluster (S a power of two dividing the units)
+    // When some SMs cannot host a whole cluster (GPC granularity) the split runs
+    // on the resident clusters if every tile is in the tail (decode batches);
+    // otherwise (whole waves before the tail) only if all units fit.
+    bool ct = false;
+    if (!PAIR && N <= 128 && S > 1 && !std::getenv("MPB_ROUTER_GLOBAL_TAIL")) {
+        if (S == 3) S = 2;
+        const uint32_t cap = std::min(full_units, max_active_clusters(kern, smem, S) * S) / S * S;
+        if (waves == 0 && S * rem <= cap) {
+            ct = true;
+            units = cap;
+        } else if (cap == full_units && full_units % S == 0) {
+            ct = true;
+            units = full_units;
+        }
+    }
     p.splits = S;
-    if (S > 1) {
+    p.cluster_tail = ct ? 1u : 0u;
+    if (S > 1 && ct) {
+        // units set above
+    } else if (S > 1) {
         units = full_units;
         const size_t ranks = PAIR ? 2 : 1;
         const size_t flag_bytes = 4096;
@@ -812,6 +1162,14 @@ mpb_status launch_router_n(mpb_context *ctx, const CUtensorMap &mx, const CUtens
         cfg.gridDim = dim3(2 * units);
         attr[0].id = cudaLaunchAttributeClusterDimension;
         attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+    } else if (ct) {
+        cfg.gridDim = dim3(units);
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = S;
         attr[0].val.clusterDim.y = 1;
         attr[0].val.clusterDim.z = 1;
         cfg.attrs = attr;
@@ -868,10 +1226,8 @@ mpb_status router_check(const char *fn, uint64_t T, uint32_t H, uint32_t E, uint
 // the next of 64 / 128 / 256: W rows past E come in as TMA out-of-bounds zeros
 // and their columns are masked in the epilogue.
 uint32_t router_tile_n(uint32_t E, bool *pair) {
-    static const bool single = [] {
-        const char *v = std::getenv("MPB_ROUTER_SINGLE");
-        return v && v[0] == '1';
-    }();
+    const char *v = std::getenv("MPB_ROUTER_SINGLE");
+    const bool single = v && v[0] == '1';
     const uint32_t N = E <= 64 ? 64 : E <= 128 ? 128 : 256;
     *pair = N == 256 && !single;
     return N;

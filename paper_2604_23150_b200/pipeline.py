@@ -392,17 +392,35 @@ class RoutingPipeline:
         from .distributed import shard_bounds
         self.shard = shard_bounds(P, self.world, self.rank)
 
+    def _candidate_pool(self):
+        """Placements the search starts from: data_based
+        (placement.cpp:283-294) over several balance seeds without redundancy
+        and with R_redundancy = D (phase 2 replicas, :163-189), EPLB (:315-350)
+        and linear, all under the calibrated cluster routing."""
+        s, stage = self.spec, self.calib.stage
+        D = s.groups
+        usage = pol.aggregate_usage(stage.group_map, stage.matrix, stage.model, D)
+        pool = [(f"data_based_R0_seed{sd}", pol.data_based_placement(usage, 0, sd))
+                for sd in (2, 3, 5, 7, 11)]
+        pool += [(f"data_based_R{D}_seed{sd}", pol.data_based_placement(usage, D, sd))
+                 for sd in (2, 3)]
+        strat = {e.label: e for e in self.calib.strategies}
+        pool += [("eplb", strat["eplb"].placement), ("linear", strat["linear"].placement)]
+        return pool
+
     def _search_placements(self, db, n: int):
-        """Placement search at scale: greedy local search
-        from the data-based placement over expert swaps between groups, every
-        neighbourhood of 1,024 candidates priced at once on the device (K5) on
-        the calibration demand of all layers (objective: total inter-node
-        pairs; moves: 1-4 swaps between groups on different nodes, since
-        same-node swaps cannot change inter-node bytes). Returns the searched
-        placement followed by its last neighbourhood (n placements), scored
-        each step on the measurement tokens — out of sample. On the DSv3 shape
-        (2 nodes) the data-based placement is already swap-locally optimal,
-        which for a two-way split with fixed capacities is the optimum."""
+        """Placement search at scale. Every candidate is priced
+        at once on the device (K5) on the calibration demand of all layers
+        (objective: total inter-node pairs). 1. the candidate pool
+        (_candidate_pool: data_based over seeds and R_redundancy in {0, D},
+        EPLB, linear) is scored; 2. greedy local search from the best
+        replica-free pool entry over expert swaps between groups on different
+        nodes (same-node swaps cannot change inter-node bytes), each
+        neighbourhood of up to 1,024 swaps priced in one launch. Returns the
+        searched placement, the pool, then the last neighbourhood (n in all),
+        scored each step on the measurement tokens — out of sample. The scores
+        land in self.search_report (checked against the oracle by
+        tests/test_gpu_pipeline.py)."""
         s, eng = self.spec, self.eng
         rng = np.random.default_rng(12345 + s.seed)
         D, E = s.groups, s.experts
@@ -423,11 +441,11 @@ class RoutingPipeline:
             return g
 
         def luts(cands):
-            if db.R_redundancy:  # replicated experts: the library's holder rule
-                return np.stack([mp.host_dest_lut(mp.Placement(c, E, db.R_redundancy, db.M), g2n)
-                                 for c in cands])
             out = np.full((len(cands), nodes, E), 255, np.uint8)
             for p, c in enumerate(cands):
+                if isinstance(c, mp.Placement):  # replicas: the library's holder rule
+                    out[p] = mp.host_dest_lut(c, g2n)
+                    continue
                 for d, g in enumerate(c):
                     out[p, :, g] = d
             return out
@@ -440,8 +458,13 @@ class RoutingPipeline:
                                                g2n_t, D, row_node=g2n_t)
             return inter.sum(dim=1).cpu().numpy()  # [P] pairs over all layers
 
-        cur = [list(g) for g in db.groups]
-        cur_val = score([cur])[0]
+        pool = self._candidate_pool() if n else []
+        pool_vals = score([p for _, p in pool]) if pool else []
+        report = {lab: int(v) for (lab, _), v in zip(pool, pool_vals)}
+        flat = [(lab, p, v) for (lab, p), v in zip(pool, pool_vals) if p.R_redundancy == 0]
+        start_lab, start, cur_val = min(flat, key=lambda x: x[2]) if flat else \
+            ("data_based", db, score([db])[0])
+        cur = [list(g) for g in start.groups]
         hood = []
         iters = int(os.environ.get("MPB_SEARCH_ITERS", "24")) if n else 0
         for _ in range(iters):
@@ -450,11 +473,16 @@ class RoutingPipeline:
             b = int(np.argmin(vals))
             if vals[b] < cur_val:
                 cur, cur_val = hood[b], vals[b]
-        while len(hood) < n:
+        report["start"] = start_lab
+        report["searched"] = int(cur_val)
+        self.search_report = report
+        self.search_gain = float(cur_val) / float(score([db])[0])
+        out = [mp.Placement(cur, E, 0, len(cur[0]))] + [p for _, p in pool]
+        rest = max(0, n - len(out))
+        while len(hood) < rest:
             hood.append(swap(cur))
-        self.search_gain = float(cur_val) / float(score([[list(g) for g in db.groups]])[0])
-        out = [cur] + hood[: max(0, n - 1)]
-        return [mp.Placement(g, E, db.R_redundancy, db.M) for g in out]
+        out += [mp.Placement(g, E, 0, len(g[0])) for g in hood[:rest]]
+        return out[:max(n, 0)] if n else []
 
     @property
     def launches(self) -> int:

@@ -105,3 +105,36 @@ def test_sm_partition_confines_kernels(monkeypatch):
     assert p_part.partition is not None
     assert torch.equal(p_budget.stats, p_part.stats)
     assert p_budget.results() == p_part.results()
+
+
+def test_placement_search_scores_match_oracle(monkeypatch, oracle):
+    """Placement search: the candidate pool (data_based over
+    balance seeds with R_redundancy 0 and D, EPLB, linear) and the searched
+    placement are priced by K5 on the calibration demand; every reported score
+    equals the oracle's inter-node pair count (holder resolution of
+    simulator.cpp:52-55, 74-80 on the oracle's destination table), the search
+    never ends worse than its start."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    monkeypatch.setenv("MPB_ROUTER_NO_SPLIT", "1")
+    eng = mp.Engine(0)
+    pipe = RoutingPipeline(SPEC, eng, 0, 1, resident=True)
+    rep = pipe.search_report
+    dem = pipe.calib.demand.cpu().numpy().astype(np.int64)  # [L, D, E]
+    g2n = np.array(pipe.topology.group_to_node[:SPEC.groups])
+
+    def oracle_inter(groups):
+        lut = oracle.dest_lut(groups, list(g2n), SPEC.experts)  # [nodes, E]
+        dest = lut[g2n]  # [D(source), E]
+        cross = g2n[dest] != g2n[:, None]
+        return int((dem * cross[None]).sum())
+
+    pool = pipe._candidate_pool()
+    assert [lab for lab, _ in pool] == [k for k in rep if k not in ("start", "searched")]
+    for lab, p in pool:
+        assert rep[lab] == oracle_inter(p.groups), lab
+    searched = pipe.placements_cl[1]
+    searched.verify()
+    assert rep["searched"] == oracle_inter(searched.groups)
+    assert rep["searched"] <= rep[rep["start"]]
+    assert any(p.R_redundancy == SPEC.groups for _, p in pool)

@@ -152,6 +152,39 @@ def test_router_split_k_parts(eng, oracle, shape, monkeypatch):
         np.testing.assert_allclose(w.cpu().numpy(), rw, rtol=2e-6, atol=1e-7)
 
 
+@pytest.mark.parametrize("shape", [(4096, 4096, 128, 8, 0, True), (4096, 4096, 128, 1, 1, False),
+                                   (2048, 1024, 64, 4, 0, False), (1000, 2048, 96, 6, 1, True),
+                                   (3000, 512, 128, 16, 0, True), (4096, 2048, 256, 8, 1, True)])
+def test_router_cluster_tail_equals_global_tail(eng, oracle, shape, monkeypatch):
+    """Single-CTA tiles run the split-K tail through distributed shared memory
+    (the K parts of a tile in one cluster, reduce-scatter of the partials with
+    st.async, top-k of each CTA's row share by all 8 epilogue warps). The
+    partials are summed in the same K-part order as the global-memory tail
+    (MPB_ROUTER_GLOBAL_TAIL=1), so the logits are bit-identical, the indices
+    are the oracle's top-k of those logits and the weights agree with it; the
+    256-expert case runs single-CTA tiles (MPB_ROUTER_SINGLE=1)."""
+    T, H, E, k, fn, renorm = shape
+    if E > 128:
+        monkeypatch.setenv("MPB_ROUTER_SINGLE", "1")
+    g = torch.Generator(device="cuda").manual_seed(T * 3 + E)
+    X = torch.randn(T, H, device="cuda", generator=g).to(torch.bfloat16)
+    W = (torch.randn(E, H, device="cuda", generator=g) / H ** 0.5).to(torch.bfloat16)
+    out = {}
+    for tail in ("global", "cluster", "cluster"):
+        if tail == "global":
+            monkeypatch.setenv("MPB_ROUTER_GLOBAL_TAIL", "1")
+        else:
+            monkeypatch.delenv("MPB_ROUTER_GLOBAL_TAIL", raising=False)
+        out[tail] = eng.router_topk(X, W, k, fn, renorm, want_logits=True)
+        torch.cuda.synchronize()
+    (gi, gw, gl), (ci, cw, cl) = out["global"], out["cluster"]
+    assert torch.equal(gl, cl)
+    ri, rw = oracle.topk_logits(cl.cpu().numpy(), k, fn, renorm)
+    np.testing.assert_array_equal(ci.cpu().numpy(), ri)
+    np.testing.assert_array_equal(gi.cpu().numpy(), ri)
+    np.testing.assert_allclose(cw.cpu().numpy(), rw, rtol=2e-6, atol=1e-7)
+
+
 @pytest.mark.parametrize("shape", [(3, 5000, 1024, 256, 8, 1, True), (4, 4096, 4096, 128, 8, 0, False),
                                    (2, 300, 512, 64, 4, 0, True), (5, 65536, 7168, 256, 8, 1, True)])
 def test_router_topk_layers_matches_per_layer(eng, shape, monkeypatch):

@@ -44,7 +44,7 @@ used = t[:, 0] > 0
 t = t[used].astype(np.int64)
 t0 = t[:, 0].min()
 names = ["entry", "pdl_wait", "first_tma", "last_commit", "acc_ready", "fixup_done", "epi_done",
-         "exit", None, None, "scan_done", "softmax_done", "merged"]
+         "exit", None, None, "s10", "s11", "s12", "s13"]
 roles = t[:, 8]
 print(f"T={a.T} H={a.H} E={a.E} k={a.k} layers={a.layers}: {used.sum()} CTAs; "
       f"items/CTA {np.bincount(t[:, 9]).nonzero()[0].tolist()}")
@@ -59,4 +59,4 @@ print(f"scan (warp 4 lane 0, medians over CTAs): tmem-load cycles {np.median(ep[
       f"insertion cycles {np.median(ep[:, 14]):.0f}, hits {np.median(ep[:, 15]):.0f}")
 for r in sorted(set(roles.tolist())):
     row = t[roles == r][0]
-    print(f"  e.g. role {r}:", [round((v - t0) / 1e3, 2) if v > 0 else None for v in row[:13]])
+    print(f"  e.g. role {r}:", [round((v - t0) / 1e3, 2) if v > 0 else None for v in row[:14]])

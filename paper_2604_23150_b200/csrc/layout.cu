@@ -139,8 +139,7 @@ __device__ __forceinline__ void cursor_next(const LayoutParams &p, TokenCursor &
 }
 
 template <bool kPerm>
-__global__ void __launch_bounds__(kThreads) k_layout_count(LayoutParams p) {
-    extern __shared__ uint32_t sm[];
+__device__ __forceinline__ void count_body(const LayoutParams &p, uint32_t *sm) {
     const uint32_t DE = p.D * p.E;
     uint32_t *s_demand = sm;
     uint32_t *s_demand2 = s_demand + (p.demand_smem ? DE : 0);
@@ -272,6 +271,12 @@ __global__ void __launch_bounds__(kThreads) k_layout_count(LayoutParams p) {
     }
 }
 
+template <bool kPerm>
+__global__ void __launch_bounds__(kThreads) k_layout_count(LayoutParams p) {
+    extern __shared__ uint32_t sm[];
+    count_body<kPerm>(p, sm);
+}
+
 // Block-wide exclusive scan of one value per thread (kThreads threads).
 __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t *s_warp, uint32_t &total) {
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -302,13 +307,11 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t *s_warp
 // One CTA per 32 slots: exclusive scan down the block axis of bhist[.][slot]
 // in place + slot totals. Lane = slot (coalesced 128-byte rows); warp w owns a
 // contiguous range of blocks: per-warp sums, prefix over warps, then rewrite.
-__global__ void __launch_bounds__(kThreads) k_layout_scan(uint32_t *bhist, uint32_t nb,
-                                                          uint32_t NS, uint32_t *totals) {
+__device__ __forceinline__ void scan_columns(uint32_t *bhist, uint32_t nb, uint32_t NS,
+                                             uint32_t *totals, uint32_t group) {
     __shared__ uint32_t s_part[kWarps][32];
-    pdl_trigger();
-    pdl_wait();
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint32_t slot = blockIdx.x * 32 + lane;
+    const uint32_t slot = group * 32 + lane;
     const bool ok = slot < NS;
     const uint32_t per = (nb + kWarps - 1) / kWarps;
     const uint32_t b0 = min(nb, warp * per), b1 = min(nb, b0 + per);
@@ -348,22 +351,29 @@ __global__ void __launch_bounds__(kThreads) k_layout_scan(uint32_t *bhist, uint3
             run += v;
         }
     }
+    __syncthreads();  // s_part is reused by the next column group
 }
 
-__global__ void __launch_bounds__(kThreads) k_layout_scatter(LayoutParams p, int32_t *sorted_pairs,
-                                                             int32_t *pair_pos,
-                                                             const uint16_t *key_lb,
-                                                             uint32_t nkeys,
-                                                             int64_t *key_offsets) {
-    extern __shared__ uint32_t s_w[];  // [kWarps][NS] per-warp counts / positions, [NS+1] bases
+__global__ void __launch_bounds__(kThreads) k_layout_scan(uint32_t *bhist, uint32_t nb,
+                                                          uint32_t NS, uint32_t *totals) {
+    pdl_trigger();
+    pdl_wait();
+    scan_columns(bhist, nb, NS, totals, blockIdx.x);
+}
+
+template <bool kFused>
+__device__ __forceinline__ void scatter_body(const LayoutParams &p, int32_t *sorted_pairs,
+                                             int32_t *pair_pos, const uint16_t *key_lb,
+                                             uint32_t nkeys, int64_t *key_offsets,
+                                             uint32_t *s_w) {  // [kWarps][NS] counts / positions, [NS+1] bases
     __shared__ uint32_t s_warp[32];
     uint32_t *s_base = s_w + kWarps * p.NS;
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     // slot bases: exclusive scan of the slot totals (coalesced loads into smem,
     // then a blocked scan; every block, NS is small)
-    pdl_trigger();
+    if (!kFused) pdl_trigger();
     for (uint32_t i = threadIdx.x; i < kWarps * p.NS; i += kThreads) s_w[i] = 0;
-    pdl_wait();
+    if (!kFused) pdl_wait();
     for (uint32_t i = threadIdx.x; i < p.NS; i += kThreads) s_base[i] = __ldcg(p.totals + i);
     __syncthreads();
     {
@@ -481,6 +491,56 @@ __global__ void __launch_bounds__(kThreads) k_layout_scatter(LayoutParams p, int
     }
 }
 
+__global__ void __launch_bounds__(kThreads) k_layout_scatter(LayoutParams p, int32_t *sorted_pairs,
+                                                             int32_t *pair_pos,
+                                                             const uint16_t *key_lb,
+                                                             uint32_t nkeys,
+                                                             int64_t *key_offsets) {
+    extern __shared__ uint32_t s_w[];
+    scatter_body<false>(p, sorted_pairs, pair_pos, key_lb, nkeys, key_offsets, s_w);
+}
+
+// Grid-wide barrier of a launch whose blocks are all resident (nb <= SMs):
+// arrival counter + generation word, self-resetting (graph-replay safe).
+__device__ __forceinline__ void grid_barrier(uint32_t *bar, uint32_t nblocks) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile uint32_t *vgen = bar + 1;
+        const uint32_t gen = *vgen;
+        __threadfence();
+        if (atomicAdd(bar, 1u) == nblocks - 1) {
+            atomicExch(bar, 0u);
+            __threadfence();
+            atomicAdd(bar + 1, 1u);
+        } else {
+            uint32_t g;
+            do {
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(bar + 1) : "memory");
+            } while (g == gen);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+// Small batches (decode: T*k <= 1024 * SMs): count, scan and scatter in ONE
+// launch of nb <= SMs resident blocks separated by two grid barriers — the
+// same three phases (same per-block histograms, same stable order) without
+// two kernel boundaries.
+__global__ void __launch_bounds__(kThreads) k_layout_fused(LayoutParams p, int32_t *sorted_pairs,
+                                                           int32_t *pair_pos, const uint16_t *key_lb,
+                                                           uint32_t nkeys, int64_t *key_offsets,
+                                                           uint32_t *gbar) {
+    extern __shared__ uint32_t sm[];
+    count_body<true>(p, sm);
+    grid_barrier(gbar, gridDim.x);
+    for (uint32_t g = blockIdx.x; g < (p.NS + 31) / 32; g += gridDim.x)
+        scan_columns(p.bhist, p.nb, p.NS, p.totals, g);
+    grid_barrier(gbar, gridDim.x);
+    __syncthreads();
+    scatter_body<true>(p, sorted_pairs, pair_pos, key_lb, nkeys, key_offsets, sm);
+}
+
 __global__ void __launch_bounds__(256) k_layout_derive(const uint64_t *demand, const uint8_t *g2n,
                                                        const uint8_t *dest_lut, uint32_t D,
                                                        uint32_t E, uint32_t nodes,
@@ -494,25 +554,37 @@ __global__ void __launch_bounds__(256) k_layout_derive(const uint64_t *demand, c
     unsigned long long inter = 0, intra = 0;
     for (uint32_t e = threadIdx.x; e < E; e += blockDim.x) {
         unsigned long long col = 0;
-        if (node_demand)
-            for (uint32_t n = 0; n < nodes; ++n) node_demand[static_cast<size_t>(n) * E + e] = 0;
-        for (uint32_t s = 0; s < D; ++s) {
-            const unsigned long long a = demand[static_cast<size_t>(s) * E + e];
-            if (!a) continue;
-            const uint32_t n = g2n[s];
-            const uint32_t d = dest_lut[static_cast<size_t>(n) * E + e];
-            if (d >= D) {
-                atomicOr(err, kErrUncovered);
-                continue;
+        // the column's demands in flight together (8 source groups per batch),
+        // node sums kept in registers: one store per (node, expert), no global
+        // read-modify-write chain
+        for (uint32_t s0 = 0; s0 < D; s0 += 8) {
+            unsigned long long a[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) a[j] = s0 + j < D ? demand[static_cast<size_t>(s0 + j) * E + e] : 0ull;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                if (!a[j]) continue;
+                const uint32_t s = s0 + j, n = g2n[s];
+                const uint32_t d = dest_lut[static_cast<size_t>(n) * E + e];
+                if (d >= D) {
+                    atomicOr(err, kErrUncovered);
+                    continue;
+                }
+                col += a[j];
+                atomicAdd(&s_g[d], a[j]);
+                if (g2n[d] == n)
+                    intra += a[j];
+                else
+                    inter += a[j];
             }
-            col += a;
-            if (node_demand) node_demand[static_cast<size_t>(n) * E + e] += a;
-            atomicAdd(&s_g[d], a);
-            if (g2n[d] == n)
-                intra += a;
-            else
-                inter += a;
         }
+        if (node_demand)
+            for (uint32_t n = 0; n < nodes; ++n) {
+                unsigned long long t = 0;
+                for (uint32_t s = 0; s < D; ++s)
+                    if (g2n[s] == n) t += demand[static_cast<size_t>(s) * E + e];
+                node_demand[static_cast<size_t>(n) * E + e] = t;
+            }
         if (expert_count) expert_count[e] = col;
     }
     atomicAdd(&s_g[D], inter);
@@ -596,11 +668,20 @@ mpb_status launch_layout(mpb_context *ctx, const mpb_tokens *tk, const mpb_place
     // latency)
     static const char *cenv = std::getenv("MPB_LAYOUT_BLOCKS_PER_SM");
     static const char *menv = std::getenv("MPB_LAYOUT_MIN_BLOCKS");
+    static const bool fuse_on = std::getenv("MPB_LAYOUT_FUSE") != nullptr;
     const uint64_t kMinBlocks = menv ? std::max(1, std::atoi(menv)) : 160;
     const uint64_t want_blocks = std::max<uint64_t>(
         kMinBlocks, uint64_t(ctx->num_sms) * (cenv ? std::max(1, std::atoi(cenv)) : 2));
     uint64_t chunk = (P + want_blocks - 1) / want_blocks;
+    // at most 8 quanta per block: large batches (1M tokens x 8) get more, thinner
+    // blocks — the scatter's per-warp ranking is latency-bound, and 28K-pair
+    // blocks at 2 per SM left it at 25% occupancy (K2+K3 200 -> 106 us measured)
+    chunk = std::min<uint64_t>(chunk, 8 * kChunkQuantum);
     chunk = std::max<uint64_t>(kChunkQuantum, (chunk + kChunkQuantum - 1) / kChunkQuantum * kChunkQuantum);
+    // opt-in (MPB_LAYOUT_FUSE=1): small batches in one launch with grid barriers —
+    // measured slower than the three PDL-chained kernels at the decode shape
+    const bool fused = perm && fuse_on && (P + kChunkQuantum - 1) / kChunkQuantum <= uint64_t(ctx->num_sms);
+    if (fused) chunk = kChunkQuantum;
     const uint32_t nb = static_cast<uint32_t>((P + chunk - 1) / chunk);
     p.nb = nb;
     p.chunk = static_cast<uint32_t>(chunk);
@@ -610,6 +691,17 @@ mpb_status launch_layout(mpb_context *ctx, const mpb_tokens *tk, const mpb_place
         MPB_CUDA(ctx->ensure_scratch((size_t(nb) + 1) * pl->NS * 4 + 256));
         p.bhist = static_cast<uint32_t *>(ctx->scratch);
         p.totals = p.bhist + size_t(nb) * pl->NS;
+    }
+    if (fused) {
+        const size_t sc_smem = (size_t(kWarps) * pl->NS + pl->NS + 1) * 4;
+        const size_t f_smem = std::max(smem, sc_smem);
+        MPB_CUDA(cudaFuncSetAttribute(k_layout_fused, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(f_smem)));
+        MPB_CUDA(launch_pdl(k_layout_fused, dim3(nb), dim3(kThreads), f_smem, ctx->stream, p,
+                            sorted_pairs, pair_pos, pl->d_key_lb, pl->D * pl->E, key_offsets,
+                            ctx->d_gbar));
+        MPB_LAUNCHED(ctx);
+        return MPB_OK;
     }
     auto count = perm ? k_layout_count<true> : k_layout_count<false>;
     MPB_CUDA(cudaFuncSetAttribute(count, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));

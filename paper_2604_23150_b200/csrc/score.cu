@@ -154,22 +154,35 @@ __global__ void __launch_bounds__(kScoreWarps * 32) k_score(const uint64_t *dema
         __syncwarp();
         const uint8_t *lut = luts + static_cast<size_t>(p) * NE;
         unsigned long long inter = 0, intra = 0;
-        for (uint32_t i = lane; i < NE; i += 32) {
-            const unsigned long long v = s_nd[i];
-            const uint32_t d = __ldg(lut + i);
-            if (!v) continue;
-            if (d >= D) {  // 255 = uncovered; any other out-of-range group too
-                atomicOr(err, kErrUncovered);
-                continue;
+        // four LUT bytes per lane in flight before any is used (the L2 latency
+        // of the candidate's table is paid once per 128 cells, not per cell)
+        for (uint32_t i0 = lane; i0 < NE; i0 += 128) {
+            uint32_t dd[4];
+            unsigned long long vv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t i = i0 + 32u * u;
+                dd[u] = i < NE ? __ldg(lut + i) : 255u;
+                vv[u] = i < NE ? s_nd[i] : 0ull;
             }
-            if (kPrivate)
-                acc[d * 32 + lane] += v;
-            else
-                atomicAdd(acc + d, v);
-            if (s_g2n[d] == i / E)
-                intra += v;
-            else
-                inter += v;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t i = i0 + 32u * u, d = dd[u];
+                const unsigned long long v = vv[u];
+                if (!v) continue;
+                if (d >= D) {  // 255 = uncovered; any other out-of-range group too
+                    atomicOr(err, kErrUncovered);
+                    continue;
+                }
+                if (kPrivate)
+                    acc[d * 32 + lane] += v;
+                else
+                    atomicAdd(acc + d, v);
+                if (s_g2n[d] == i / E)
+                    intra += v;
+                else
+                    inter += v;
+            }
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {

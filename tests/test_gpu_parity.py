@@ -445,3 +445,46 @@ def test_score_and_finalize_fused_equals_two_launches(oracle, spans):
     for a, b in zip(sc, sc1):
         assert torch.equal(a, b)
     assert torch.equal(f1, f2) and torch.equal(p1, p2)
+
+
+def test_fused_small_batch_layout_matches_oracle(tmp_path):
+    """MPB_LAYOUT_FUSE=1 (read once per process, so in a child): small batches
+    run count, scan and scatter as ONE launch with two grid barriers; the
+    histograms and the stable permutation equal the oracle's, twice in a row
+    (the barrier words reset themselves)."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    root = Path(__file__).resolve().parents[1]
+    code = r'''
+import sys; sys.path.insert(0, %r)
+import numpy as np, torch
+from oracle.pyoracle import Oracle
+from paper_2604_23150_b200 import moeplace as mp
+O = Oracle(); eng = mp.Engine(0)
+for T, E, k, D, red in ((4096, 128, 8, 8, 0), (1000, 256, 8, 8, 3), (37, 64, 4, 4, 0)):
+    rng = np.random.default_rng(T)
+    idx = np.argsort(rng.random((T, E)), axis=1)[:, :k].astype(np.int32)
+    groups = [list(range(d * E // D, (d + 1) * E // D)) for d in range(D)]
+    for g in groups:
+        g += [e for e in rng.permutation(E).tolist() if e not in g][:red]
+    pl = mp.Placement(groups, E, red * D, len(groups[0]))
+    top = mp.Topology.contiguous(D, 1, D, 1, 2)
+    src = rng.integers(0, D, T).astype(np.uint8)
+    dp = eng.placement(pl, top)
+    lut = O.dest_lut(pl.groups, top.group_to_node, E)
+    ref = O.dispatch_layout(idx, src.astype(np.uint32), lut, D, E, top.group_to_node)
+    for _ in range(2):
+        lay = eng.dispatch_layout(torch.from_numpy(idx).cuda(), dp, src=torch.from_numpy(src).cuda())
+        eng.sync()
+        assert np.array_equal(lay["sorted_pairs"].cpu().numpy(), ref["sorted_pairs"])
+        assert np.array_equal(lay["demand"].cpu().numpy().reshape(-1), ref["demand"].reshape(-1))
+print("fused ok")
+''' % str(root)
+    env = dict(os.environ, MPB_LAYOUT_FUSE="1")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
+                       timeout=300)
+    assert r.returncode == 0 and "fused ok" in r.stdout, r.stdout + r.stderr

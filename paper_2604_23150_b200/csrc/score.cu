@@ -16,6 +16,8 @@
 //                    intrinsics so the result is bit-identical to the host.
 // Algorithmic bytes per (candidate, batch): nodes*E*8 (demand) + nodes*E
 // (LUT, reused across batches from smem) + (2 + D)*8 out.
+#include <cstdlib>
+
 #include "internal.cuh"
 
 namespace mpb {
@@ -210,6 +212,99 @@ __global__ void __launch_bounds__(kScoreWarps * 32) k_score(const uint64_t *dema
     }
 }
 
+constexpr uint32_t kFastMaxD = 16;  // static smem: lane-private rank columns for D <= 16
+
+// Fast path of the scorer for nodes*E <= 512 with E % 16 == 0 (every BASELINE
+// shape): lane l owns the 16 consecutive (node, expert) cells 16l..16l+15 of
+// the batch's folded demand in REGISTERS, and reads a candidate's destination
+// table as one 16-byte load — one L2 round trip per candidate, prefetched one
+// candidate ahead. Rank totals pass to the finalizing lane through shared
+// memory (no global read-back). Same integer sums and the same finalize_cell:
+// bit-identical to k_score.
+__global__ void __launch_bounds__(kScoreWarps * 32) k_score16(const uint64_t *demand, uint32_t B,
+                                                              uint32_t rows,
+                                                              const uint8_t *row_node_g,
+                                                              const uint8_t *luts, uint32_t P,
+                                                              const uint8_t *g2n_g, uint32_t D,
+                                                              uint32_t nodes, uint32_t E,
+                                                              uint64_t *inter_out,
+                                                              uint64_t *intra_out,
+                                                              uint64_t *rank_out, uint32_t *err,
+                                                              FinalizeArgs fin) {
+    __shared__ unsigned long long s_nd[512];
+    __shared__ unsigned long long s_acc[kScoreWarps][kFastMaxD][32];
+    __shared__ unsigned long long s_rank[kScoreWarps][kFastMaxD];
+    __shared__ uint8_t s_g2n[256];
+    const uint32_t NE = nodes * E;
+    const uint32_t b = blockIdx.x;
+    for (uint32_t i = threadIdx.x; i < D; i += blockDim.x) s_g2n[i] = g2n_g[i];
+    for (uint32_t i = threadIdx.x; i < NE; i += blockDim.x) s_nd[i] = 0;
+    __syncthreads();
+    const uint64_t *a = demand + static_cast<size_t>(b) * rows * E;
+    for (uint32_t i = threadIdx.x; i < rows * E; i += blockDim.x) {
+        const unsigned long long v = a[i];
+        if (v) atomicAdd(&s_nd[static_cast<uint32_t>(row_node_g[i / E]) * E + i % E], v);
+    }
+    __syncthreads();
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const bool active = lane * 16 < NE;
+    unsigned long long v[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = active ? s_nd[lane * 16 + j] : 0ull;
+    const uint32_t my_node = active ? lane * 16 / E : 0u;  // 16 cells never straddle a node
+    unsigned long long(*acc)[32] = s_acc[warp];
+    const uint32_t stride = gridDim.y * kScoreWarps;
+    uint32_t p = blockIdx.y * kScoreWarps + warp;
+    uint4 nxt = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+    if (p < P && active) nxt = __ldg(reinterpret_cast<const uint4 *>(luts + static_cast<size_t>(p) * NE) + lane);
+    for (; p < P; p += stride) {
+        const uint4 cur = nxt;
+        if (p + stride < P && active)  // next candidate's table in flight during this one
+            nxt = __ldg(reinterpret_cast<const uint4 *>(luts + static_cast<size_t>(p + stride) * NE) + lane);
+        for (uint32_t d = 0; d < D; ++d) acc[d][lane] = 0;
+        __syncwarp();
+        unsigned long long inter = 0, intra = 0;
+        const uint32_t w4[4] = {cur.x, cur.y, cur.z, cur.w};
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const uint32_t d = (w4[j >> 2] >> (8 * (j & 3))) & 0xFFu;
+            if (!v[j]) continue;
+            if (d >= D) {
+                atomicOr(err, kErrUncovered);
+                continue;
+            }
+            acc[d][lane] += v[j];
+            if (s_g2n[d] == my_node)
+                intra += v[j];
+            else
+                inter += v[j];
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            inter += __shfl_xor_sync(0xffffffffu, inter, o);
+            intra += __shfl_xor_sync(0xffffffffu, intra, o);
+        }
+        __syncwarp();
+        const size_t cell = static_cast<size_t>(p) * B + b;
+        if (lane == 0) {
+            inter_out[cell] = inter;
+            intra_out[cell] = intra;
+        }
+        for (uint32_t d = lane; d < D; d += 32) {
+            unsigned long long t = 0;
+            for (uint32_t l = 0; l < 32; ++l) t += acc[d][(l + lane) & 31];
+            rank_out[cell * D + d] = t;
+            s_rank[warp][d] = t;
+        }
+        __syncwarp();  // the warp's rank totals are visible to lane 0
+        if (fin.out && lane == 0)
+            finalize_cell(cell, inter, intra, reinterpret_cast<const uint64_t *>(s_rank[warp]), D, fin.c,
+                          fin.tp_exp, fin.spans, fin.out,
+                          fin.payload);
+        __syncwarp();
+    }
+}
+
 __global__ void k_finalize(const uint64_t *inter, const uint64_t *intra, const uint64_t *rank,
                            uint64_t N, uint32_t D, CostParams c, uint32_t tp_exp, int spans,
                            double *out, double *payload) {
@@ -277,15 +372,19 @@ mpb_status launch_score(mpb_context *ctx, const char *fn, const uint64_t *demand
     const size_t smem =
         size_t(nodes) * E * 8 + size_t(kScoreWarps) * D * (priv ? 32 : 1) * 8 + D + 8;
     if (smem > 200 * 1024) return fail(MPB_CONFIG_ERROR, std::string(fn) + ": nodes*E too large");
-    auto kern = priv ? k_score<true> : k_score<false>;
-    MPB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    // register-resident fast path: 16 cells per lane, one 16-byte LUT load per candidate
+    const bool fast = size_t(nodes) * E <= 512 && E % 16 == 0 && D <= kFastMaxD &&
+                      (reinterpret_cast<uintptr_t>(luts) & 15) == 0 && !std::getenv("MPB_SCORE_SLOW");
+    auto kern = fast ? k_score16 : priv ? k_score<true> : k_score<false>;
+    if (!fast)
+        MPB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     // one CTA per batch; split candidates over grid.y until the machine is full
     const uint32_t want = 4u * static_cast<uint32_t>(ctx->num_sms);
     uint32_t gy = std::max(1u, want / std::max(1u, B));
     gy = std::min(gy, (P + kScoreWarps - 1) / kScoreWarps);
     gy = std::min(gy, 65535u);
     dim3 grid(B, gy);
-    kern<<<grid, kScoreWarps * 32, smem, ctx->stream>>>(demand, B, rows, row_node, luts, P,
+    kern<<<grid, kScoreWarps * 32, fast ? 0 : smem, ctx->stream>>>(demand, B, rows, row_node, luts, P,
                                                            group_to_node, D, nodes, E, inter,
                                                            intra, rank_pairs, ctx->d_error, fin);
     MPB_LAUNCHED(ctx);

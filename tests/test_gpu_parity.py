@@ -488,3 +488,38 @@ print("fused ok")
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
                        timeout=300)
     assert r.returncode == 0 and "fused ok" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("P,B,nodes,D,E", [(1022, 58, 2, 8, 256), (254, 1, 2, 8, 128),
+                                           (37, 5, 4, 8, 64), (9, 3, 2, 16, 32)])
+def test_register_scorer_equals_general_scorer(eng, monkeypatch, P, B, nodes, D, E):
+    """k_score16 (demand cells in registers, one 16-byte LUT load per candidate)
+    and the general k_score (MPB_SCORE_SLOW=1) give identical pair counts and
+    bit-identical LayerSim doubles; uncovered cells still raise."""
+    rng = np.random.default_rng(P + B)
+    g2n = torch.tensor([d * nodes // D for d in range(D)], dtype=torch.uint8, device="cuda")
+    demand = dev(rng.integers(0, 5000, (B, D, E)).astype(np.uint64))
+    luts = dev(rng.integers(0, D, (P, nodes, E)).astype(np.uint8))
+    cost = mp.CostModelParams(7168, 2)
+    top = mp.Topology.contiguous(D, 1, D, 1, nodes)
+    outs = []
+    for slow in ("", "1"):
+        if slow:
+            monkeypatch.setenv("MPB_SCORE_SLOW", slow)
+        else:
+            monkeypatch.delenv("MPB_SCORE_SLOW", raising=False)
+        (i, n, r), fin, pay = eng.score_and_finalize(demand, luts, g2n, D, cost, top, row_node=g2n,
+                                                     payload=torch.empty(P * B, D,
+                                                                         dtype=torch.float64,
+                                                                         device="cuda"))
+        eng.sync()
+        outs.append([t.clone() for t in (i, n, r, fin, pay)])
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
+    monkeypatch.delenv("MPB_SCORE_SLOW", raising=False)
+    bad = luts.clone()
+    bad[0, 0, 0] = 200  # out-of-range group
+    demand[:, :, 0] = 1
+    eng.score_and_finalize(demand, bad, g2n, D, cost, top, row_node=g2n)
+    with pytest.raises(ValidationError):
+        eng.sync()

@@ -382,6 +382,13 @@ typedef struct {
     uint32_t n_score_jobs;
     uint32_t side_sms;         /* 0: 20 when layers > 1 */
     uint32_t router_group;     /* 0: 8 */
+    /* 1 (single GPU: the demand is final once a layer's tail is in): every
+     * score job with B == layers is priced chunk by chunk right after the
+     * chunk's statistics tails, beside the next routers, and the last chunk's
+     * tails run on the main stream's grids after the last router; the SCORE
+     * phase is then empty. 0: all scoring in the SCORE phase (multi-GPU: after
+     * the caller's all-reduce). */
+    uint32_t score_per_chunk;
 } mpb_step_desc;
 
 #define MPB_STEP_LAYERS 1u

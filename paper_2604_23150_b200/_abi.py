@@ -45,7 +45,8 @@ class MpbStepDesc(C.Structure):
                 ("demand2", _p), ("tag_pop", _p), ("coact", _p), ("sorted_pairs", _p),
                 ("pair_pos", _p), ("key_offsets", _p), ("zero_base", _p),
                 ("zero_bytes", C.c_uint64), ("score_jobs", _p), ("n_score_jobs", C.c_uint32),
-                ("side_sms", C.c_uint32), ("router_group", C.c_uint32)]
+                ("side_sms", C.c_uint32), ("router_group", C.c_uint32),
+                ("score_per_chunk", C.c_uint32)]
 
 
 _SIGS = {

@@ -129,14 +129,14 @@ __global__ void __launch_bounds__(kScoreWarps * 32) k_score(const uint64_t *dema
                                                             uint64_t *inter_out,
                                                             uint64_t *intra_out,
                                                             uint64_t *rank_out, uint32_t *err,
-                                                            FinalizeArgs fin) {
+                                                            FinalizeArgs fin, uint32_t b0) {
     extern __shared__ unsigned long long s_raw[];
     const uint32_t NE = nodes * E;
     unsigned long long *s_nd = s_raw;                        // [nodes*E]
     unsigned long long *s_acc = s_nd + NE;  // [warps][D][32] lane-private, or [warps][D]
     const uint32_t cols = kPrivate ? 32u : 1u;
     uint8_t *s_g2n = reinterpret_cast<uint8_t *>(s_acc + kScoreWarps * D * cols);
-    const uint32_t b = blockIdx.x;
+    const uint32_t b = b0 + blockIdx.x;  // batches [b0, b0 + gridDim.x) of B
     for (uint32_t i = threadIdx.x; i < D; i += blockDim.x) s_g2n[i] = g2n_g[i];
     for (uint32_t i = threadIdx.x; i < NE; i += blockDim.x) s_nd[i] = 0;
     __syncthreads();
@@ -230,13 +230,13 @@ __global__ void __launch_bounds__(kScoreWarps * 32) k_score16(const uint64_t *de
                                                               uint64_t *inter_out,
                                                               uint64_t *intra_out,
                                                               uint64_t *rank_out, uint32_t *err,
-                                                              FinalizeArgs fin) {
+                                                              FinalizeArgs fin, uint32_t b0) {
     __shared__ unsigned long long s_nd[512];
     __shared__ unsigned long long s_acc[kScoreWarps][kFastMaxD][32];
     __shared__ unsigned long long s_rank[kScoreWarps][kFastMaxD];
     __shared__ uint8_t s_g2n[256];
     const uint32_t NE = nodes * E;
-    const uint32_t b = blockIdx.x;
+    const uint32_t b = b0 + blockIdx.x;  // batches [b0, b0 + gridDim.x) of B
     for (uint32_t i = threadIdx.x; i < D; i += blockDim.x) s_g2n[i] = g2n_g[i];
     for (uint32_t i = threadIdx.x; i < NE; i += blockDim.x) s_nd[i] = 0;
     __syncthreads();
@@ -361,7 +361,8 @@ mpb_status check_cost(const double *cost, uint32_t tp_exp) {
 mpb_status launch_score(mpb_context *ctx, const char *fn, const uint64_t *demand, uint32_t B,
                         uint32_t rows, const uint8_t *row_node, const uint8_t *luts, uint32_t P,
                         const uint8_t *group_to_node, uint32_t D, uint32_t nodes, uint32_t E,
-                        uint64_t *inter, uint64_t *intra, uint64_t *rank_pairs, FinalizeArgs fin) {
+                        uint64_t *inter, uint64_t *intra, uint64_t *rank_pairs, FinalizeArgs fin,
+                        uint32_t b0, uint32_t nb) {
     if (!ctx || !demand || !row_node || !luts || !group_to_node || !inter || !intra || !rank_pairs)
         return fail(MPB_VALIDATION_ERROR, std::string(fn) + ": NULL argument");
     if (rows == 0 || rows > 255) return fail(MPB_CONFIG_ERROR, std::string(fn) + ": need 1 <= rows <= 255");
@@ -380,13 +381,15 @@ mpb_status launch_score(mpb_context *ctx, const char *fn, const uint64_t *demand
         MPB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     // one CTA per batch; split candidates over grid.y until the machine is full
     const uint32_t want = 4u * static_cast<uint32_t>(ctx->num_sms);
-    uint32_t gy = std::max(1u, want / std::max(1u, B));
+    if (b0 + nb > B) return fail(MPB_CONFIG_ERROR, std::string(fn) + ": batch range past B");
+    if (nb == 0) return MPB_OK;
+    uint32_t gy = std::max(1u, want / std::max(1u, nb));
     gy = std::min(gy, (P + kScoreWarps - 1) / kScoreWarps);
     gy = std::min(gy, 65535u);
-    dim3 grid(B, gy);
+    dim3 grid(nb, gy);
     kern<<<grid, kScoreWarps * 32, fast ? 0 : smem, ctx->stream>>>(demand, B, rows, row_node, luts, P,
                                                            group_to_node, D, nodes, E, inter,
-                                                           intra, rank_pairs, ctx->d_error, fin);
+                                                           intra, rank_pairs, ctx->d_error, fin, b0);
     MPB_LAUNCHED(ctx);
     return MPB_OK;
 }
@@ -401,7 +404,7 @@ mpb_status mpb_score_placements(mpb_context *ctx, const uint64_t *demand, uint32
                                 uint64_t *rank_pairs) {
     return launch_score(ctx, "mpb_score_placements", demand, B, rows, row_node, luts, P,
                         group_to_node, D, nodes, E, inter, intra, rank_pairs,
-                        FinalizeArgs{CostParams{}, 1, 0, nullptr, nullptr});
+                        FinalizeArgs{CostParams{}, 1, 0, nullptr, nullptr}, 0, B);
 }
 
 mpb_status mpb_score_placements_finalize(mpb_context *ctx, const uint64_t *demand, uint32_t B,
@@ -416,7 +419,8 @@ mpb_status mpb_score_placements_finalize(mpb_context *ctx, const uint64_t *deman
     return launch_score(ctx, "mpb_score_placements_finalize", demand, B, rows, row_node, luts, P,
                         group_to_node, D, nodes, E, inter, intra, rank_pairs,
                         FinalizeArgs{CostParams{cost[0], cost[1], cost[2], cost[3], cost[4], cost[5]},
-                                     tp_exp, spans_nodes, out, payload});
+                                     tp_exp, spans_nodes, out, payload},
+                        0, B);
 }
 
 mpb_status mpb_finalize_layer_sims(mpb_context *ctx, const uint64_t *inter, const uint64_t *intra,
@@ -436,3 +440,18 @@ mpb_status mpb_finalize_layer_sims(mpb_context *ctx, const uint64_t *inter, cons
 }
 
 }  // extern "C"
+
+namespace mpb {
+// Batches [b0, b0 + nb) of an mpb_score_placements_finalize job (the step plan
+// prices each chunk of layers as soon as its statistics are in).
+mpb_status score_finalize_range(mpb_context *ctx, const mpb_score_job &j, uint32_t b0, uint32_t nb) {
+    if (!ctx || !j.out) return fail(MPB_VALIDATION_ERROR, "score_finalize_range: NULL argument");
+    if (mpb_status st = check_cost(j.cost, j.tp_exp)) return st;
+    return launch_score(ctx, "mpb_step score", j.demand, j.B, j.rows, j.row_node, j.luts, j.P,
+                        j.group_to_node, j.D, j.nodes, j.E, j.inter, j.intra, j.rank_pairs,
+                        FinalizeArgs{CostParams{j.cost[0], j.cost[1], j.cost[2], j.cost[3], j.cost[4],
+                                                j.cost[5]},
+                                     j.tp_exp, j.spans_nodes, j.out, j.payload},
+                        b0, nb);
+}
+}  // namespace mpb

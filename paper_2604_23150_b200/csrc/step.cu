@@ -131,14 +131,28 @@ mpb_status run_layers(mpb_step *s) {
         // router c+1 is enqueued before the tails of chunk c, so the main stream
         // never idles while the host enqueues the side stream's launches
         if ((st = launch_router(s, 0))) return st;
-        for (size_t c = 0; c < s->chunks.size(); ++c) {
-            if (c + 1 < s->chunks.size() && (st = launch_router(s, c + 1))) return st;
-            MPB_CUDA(cudaStreamWaitEvent(s->s_side, s->ev_done[c], 0));
-            for (uint32_t l = s->chunks[c].first; l < s->chunks[c].second; ++l) {
-                if ((st = tail(s, s->side, l))) return st;
-                if (d.coact && (st = mpb_coactivation(s->side, d.idx + l * pairs, d.T, d.k, d.E, d.coact)))
+        const size_t nc = s->chunks.size();
+        for (size_t c = 0; c < nc; ++c) {
+            if (c + 1 < nc && (st = launch_router(s, c + 1))) return st;
+            mpb_context *tc = s->side;
+            if (d.score_per_chunk && c + 1 == nc) {
+                // nothing runs beside the last chunk's tails: they take the main
+                // stream's grids, after the side stream's earlier tails
+                MPB_CUDA(cudaEventRecord(s->ev_join, s->s_side));
+                MPB_CUDA(cudaStreamWaitEvent(s->s_main, s->ev_join, 0));
+                tc = s->main;
+            } else {
+                MPB_CUDA(cudaStreamWaitEvent(s->s_side, s->ev_done[c], 0));
+            }
+            const auto [l0, l1] = s->chunks[c];
+            for (uint32_t l = l0; l < l1; ++l) {
+                if ((st = tail(s, tc, l))) return st;
+                if (d.coact && (st = mpb_coactivation(tc, d.idx + l * pairs, d.T, d.k, d.E, d.coact)))
                     return st;
             }
+            if (d.score_per_chunk)
+                for (const mpb_score_job &j : s->jobs)
+                    if (j.B == d.layers && (st = score_finalize_range(tc, j, l0, l1 - l0))) return st;
         }
     } else {
         for (size_t c = 0; c < s->chunks.size(); ++c) {
@@ -164,13 +178,20 @@ mpb_status run_layers(mpb_step *s) {
     return MPB_OK;
 }
 
+bool score_in_layers(const mpb_step *s, const mpb_score_job &j) {
+    return s->overlapped && s->d.score_per_chunk && j.B == s->d.layers;
+}
+
 mpb_status run_score(mpb_step *s) {
-    if (s->jobs.empty()) return MPB_OK;
+    bool any = false;
+    for (const mpb_score_job &j : s->jobs) any = any || !score_in_layers(s, j);
+    if (!any) return MPB_OK;
     MPB_CUDA(cudaEventRecord(s->ev_in, s->origin));
     MPB_CUDA(cudaStreamWaitEvent(s->s_main, s->ev_in, 0));
     MPB_CUDA(cudaStreamWaitEvent(s->s_side, s->ev_in, 0));
     for (size_t j = 0; j < s->jobs.size(); ++j) {
         const mpb_score_job &b = s->jobs[j];
+        if (score_in_layers(s, b)) continue;
         mpb_context *c = j == 0 ? s->main : s->side;
         if (mpb_status st = mpb_score_placements_finalize(
                 c, b.demand, b.B, b.rows, b.row_node, b.luts, b.P, b.group_to_node, b.D, b.nodes, b.E,
@@ -319,7 +340,11 @@ mpb_status mpb_step_capture(mpb_step *s) {
     cudaGraphExec_t *dst[2] = {&s->g_layers, &s->g_score};
     const uint32_t phs[2] = {MPB_STEP_LAYERS, MPB_STEP_SCORE};
     for (int i = 0; i < 2; ++i) {
-        if (phs[i] == MPB_STEP_SCORE && s->jobs.empty()) continue;
+        if (phs[i] == MPB_STEP_SCORE) {
+            bool any = false;
+            for (const mpb_score_job &j : s->jobs) any = any || !score_in_layers(s, j);
+            if (!any) continue;
+        }
         MPB_CUDA(cudaStreamBeginCapture(s->s_cap, cudaStreamCaptureModeRelaxed));
         s->capturing = true;
         s->origin = s->s_cap;

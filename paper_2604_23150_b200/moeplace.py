@@ -608,7 +608,8 @@ class StepPlan:
                  idx: torch.Tensor, weights: torch.Tensor, deployed: "DevicePlacement",
                  src: torch.Tensor, demand: torch.Tensor, src2=None, demand2=None, tag=None,
                  n_tags: int = 0, tag_pop=None, coact=None, perm_out=None, zero=None,
-                 score_jobs=(), side_sms: int = 0, router_group: int = 0):
+                 score_jobs=(), side_sms: int = 0, router_group: int = 0,
+                 score_per_chunk: bool = False):
         L = len(Xs)
         T, H = Xs[0].shape
         E = Ws[0].shape[0]
@@ -641,6 +642,7 @@ class StepPlan:
         d.score_jobs = C.cast(self._jobs, C.c_void_p) if jobs else None
         d.n_score_jobs = len(jobs)
         d.side_sms, d.router_group = side_sms, router_group
+        d.score_per_chunk = int(score_per_chunk)
         self._desc = d
         h = C.c_void_p()
         _abi.call("mpb_step_create", engine.ctx, C.byref(d), C.byref(h))

@@ -305,7 +305,10 @@ class RoutingPipeline:
             tag=self.dom_tok, n_tags=s.domains, tag_pop=self.pop,
             coact=self.coact if s.coact else None, perm_out=(self.sp, self.pp, self.ko),
             zero=self.stats, score_jobs=jobs, side_sms=self.side_sms,
-            router_group=self.router_group)
+            router_group=self.router_group,
+            # one GPU: each chunk of layers is priced as soon as its statistics
+            # are in (multi-GPU scoring waits for the all-reduced demand)
+            score_per_chunk=self.world == 1 and os.environ.get("MPB_SCORE_PER_CHUNK", "1") != "0")
         self.chunks, l0 = [], 0
         for n in self.plan.chunks():
             self.chunks.append((l0, l0 + n))

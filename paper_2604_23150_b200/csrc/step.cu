@@ -36,7 +36,8 @@ struct mpb_step {
     std::vector<mpb_score_job> jobs;
     std::vector<std::pair<uint32_t, uint32_t>> chunks;
     bool overlapped = false;
-    cudaEvent_t ev_in = nullptr, ev_out = nullptr, ev_fork = nullptr, ev_join = nullptr;
+    cudaEvent_t ev_in = nullptr, ev_out = nullptr, ev_fork = nullptr, ev_join = nullptr,
+                ev_zero = nullptr;
     std::vector<cudaEvent_t> ev_done;
     // router timing: kRing sets of (start, end) events per chunk; run r of the
     // LAYERS phase records into set r % kRing, so the per-layer router time can
@@ -125,7 +126,21 @@ mpb_status run_layers(mpb_step *s) {
     MPB_CUDA(cudaEventRecord(s->ev_in, s->origin));
     MPB_CUDA(cudaStreamWaitEvent(s->s_main, s->ev_in, 0));
     MPB_CUDA(cudaStreamWaitEvent(s->s_side, s->ev_in, 0));
-    if (d.zero_base && d.zero_bytes) MPB_CUDA(cudaMemsetAsync(d.zero_base, 0, d.zero_bytes, s->s_main));
+    // the statistics buffer is zeroed on the side stream, beside the first
+    // router (nothing reads or writes it before that router's tails); the main
+    // stream's own tails (single layer / last chunk) wait for it
+    if (d.zero_base && d.zero_bytes) {
+        MPB_CUDA(cudaMemsetAsync(d.zero_base, 0, d.zero_bytes, s->s_side));
+        MPB_CUDA(cudaEventRecord(s->ev_zero, s->s_side));
+    }
+    bool main_zeroed = !(d.zero_base && d.zero_bytes);
+    auto main_waits_zero = [&]() -> mpb_status {
+        if (!main_zeroed) {
+            MPB_CUDA(cudaStreamWaitEvent(s->s_main, s->ev_zero, 0));
+            main_zeroed = true;
+        }
+        return MPB_OK;
+    };
     mpb_status st;
     if (s->overlapped) {
         // router c+1 is enqueued before the tails of chunk c, so the main stream
@@ -140,6 +155,7 @@ mpb_status run_layers(mpb_step *s) {
                 // stream's grids, after the side stream's earlier tails
                 MPB_CUDA(cudaEventRecord(s->ev_join, s->s_side));
                 MPB_CUDA(cudaStreamWaitEvent(s->s_main, s->ev_join, 0));
+                main_zeroed = true;
                 tc = s->main;
             } else {
                 MPB_CUDA(cudaStreamWaitEvent(s->s_side, s->ev_done[c], 0));
@@ -157,6 +173,7 @@ mpb_status run_layers(mpb_step *s) {
     } else {
         for (size_t c = 0; c < s->chunks.size(); ++c) {
             if ((st = launch_router(s, c))) return st;
+            if ((st = main_waits_zero())) return st;
             for (uint32_t l = s->chunks[c].first; l < s->chunks[c].second; ++l) {
                 if (d.coact) {  // co-activation beside the layout (both only read idx)
                     MPB_CUDA(cudaEventRecord(s->ev_fork, s->s_main));
@@ -258,7 +275,7 @@ mpb_status mpb_step_create(mpb_context *ctx, const mpb_step_desc *desc, mpb_step
     if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&s->s_main, cudaStreamNonBlocking, hi);
     if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&s->s_side, cudaStreamNonBlocking, lo);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s->s_cap, cudaStreamNonBlocking);
-    for (cudaEvent_t *ev : {&s->ev_in, &s->ev_out, &s->ev_fork, &s->ev_join})
+    for (cudaEvent_t *ev : {&s->ev_in, &s->ev_out, &s->ev_fork, &s->ev_join, &s->ev_zero})
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
     const size_t nc = s->chunks.size();
     s->ev_done.assign(nc, nullptr);
@@ -293,7 +310,7 @@ mpb_status mpb_step_destroy(mpb_step *s) {
     if (s->g_score) cudaGraphExecDestroy(s->g_score);
     mpb_context_destroy(s->main);
     mpb_context_destroy(s->side);
-    for (cudaEvent_t ev : {s->ev_in, s->ev_out, s->ev_fork, s->ev_join})
+    for (cudaEvent_t ev : {s->ev_in, s->ev_out, s->ev_fork, s->ev_join, s->ev_zero})
         if (ev) cudaEventDestroy(ev);
     for (auto *v : {&s->ev_done, &s->ev_r0, &s->ev_r1})
         for (cudaEvent_t ev : *v)

@@ -46,9 +46,12 @@ struct mpb_step {
     static constexpr uint32_t kRing = 64;
     std::vector<cudaEvent_t> ev_r0, ev_r1;  // [kRing][chunk]
     uint64_t runs = 0, timing_from = 0;
-    cudaGraph_t graph_layers = nullptr;
-    std::vector<std::pair<cudaGraphNode_t, uint32_t>> rec_nodes;  // (node, chunk*2 + end)
-    cudaGraphExec_t g_layers = nullptr, g_score = nullptr;
+    // graphs: the LAYERS phase, the SCORE phase (multi-GPU: the caller's
+    // all-reduce runs between them) and both in one graph (single GPU)
+    using RecNodes = std::vector<std::pair<cudaGraphNode_t, uint32_t>>;  // (node, chunk*2 + end)
+    cudaGraph_t graph_layers = nullptr, graph_all = nullptr;
+    RecNodes rec_layers, rec_all;
+    cudaGraphExec_t g_layers = nullptr, g_score = nullptr, g_all = nullptr;
     uint64_t launches[4] = {0, 0, 0, 0};  // per phase mask (1, 2, 3)
     bool capturing = false;
     // stream the phases order against: the caller's stream, or during capture
@@ -307,6 +310,8 @@ mpb_status mpb_step_destroy(mpb_step *s) {
     if (s->s_side) cudaStreamSynchronize(s->s_side);
     if (s->g_layers) cudaGraphExecDestroy(s->g_layers);
     if (s->graph_layers) cudaGraphDestroy(s->graph_layers);
+    if (s->g_all) cudaGraphExecDestroy(s->g_all);
+    if (s->graph_all) cudaGraphDestroy(s->graph_all);
     if (s->g_score) cudaGraphExecDestroy(s->g_score);
     mpb_context_destroy(s->main);
     mpb_context_destroy(s->side);
@@ -322,14 +327,81 @@ mpb_status mpb_step_destroy(mpb_step *s) {
     return MPB_OK;
 }
 
+}  // extern "C"
+
+namespace {
+
+// Points the graph's router timing nodes at ring set `runs % kRing`.
+mpb_status retarget_timing(mpb_step *s, cudaGraphExec_t g, const mpb_step::RecNodes &rec) {
+    const size_t set = (s->runs % mpb_step::kRing) * s->chunks.size();
+    for (const auto &[node, which] : rec)
+        MPB_CUDA(cudaGraphExecEventRecordNodeSetEvent(
+            g, node, (which & 1) ? s->ev_r1[set + which / 2] : s->ev_r0[set + which / 2]));
+    return MPB_OK;
+}
+
+// Captures `phases` into an executable graph (on the plan's origin stream); for
+// graphs with the LAYERS phase, finds the router timing nodes.
+mpb_status capture_graph(mpb_step *s, uint32_t phases, cudaGraphExec_t *exec, cudaGraph_t *keep,
+                         mpb_step::RecNodes *rec) {
+    MPB_CUDA(cudaStreamBeginCapture(s->s_cap, cudaStreamCaptureModeRelaxed));
+    s->capturing = true;
+    s->origin = s->s_cap;
+    mpb_status st = run_phases(s, phases);
+    s->capturing = false;
+    cudaGraph_t g = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(s->s_cap, &g);
+    if (st) {
+        if (g) cudaGraphDestroy(g);
+        return st;
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "mpb_step_capture: cudaStreamEndCapture");
+    const cudaError_t e2 = cudaGraphInstantiate(exec, g, 0);
+    if (e2 != cudaSuccess) {
+        cudaGraphDestroy(g);
+        return cuda_fail(e2, "mpb_step_capture: cudaGraphInstantiate");
+    }
+    if (!(phases & MPB_STEP_LAYERS)) {
+        cudaGraphDestroy(g);
+        return MPB_OK;
+    }
+    *keep = g;  // node handles stay valid while the graph lives
+    size_t n = 0;
+    MPB_CUDA(cudaGraphGetNodes(g, nullptr, &n));
+    std::vector<cudaGraphNode_t> nodes(n);
+    MPB_CUDA(cudaGraphGetNodes(g, nodes.data(), &n));
+    const size_t set = (s->runs % mpb_step::kRing) * s->chunks.size();
+    for (cudaGraphNode_t nd : nodes) {
+        cudaGraphNodeType t;
+        MPB_CUDA(cudaGraphNodeGetType(nd, &t));
+        if (t != cudaGraphNodeTypeEventRecord) continue;
+        cudaEvent_t ev;
+        MPB_CUDA(cudaGraphEventRecordNodeGetEvent(nd, &ev));
+        for (size_t c = 0; c < s->chunks.size(); ++c) {
+            if (ev == s->ev_r0[set + c]) rec->emplace_back(nd, static_cast<uint32_t>(2 * c));
+            if (ev == s->ev_r1[set + c]) rec->emplace_back(nd, static_cast<uint32_t>(2 * c + 1));
+        }
+    }
+    if (rec->size() != 2 * s->chunks.size())
+        return fail(MPB_CUDA_ERROR, "mpb_step_capture: router timing nodes not found in the graph");
+    return MPB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
 mpb_status mpb_step_run(mpb_step *s, uint32_t phases) {
     if (!s) return fail(MPB_VALIDATION_ERROR, "mpb_step_run: NULL step");
+    if (s->g_all && (phases & 3) == 3) {  // single GPU: the whole step, one graph
+        if (mpb_status st = retarget_timing(s, s->g_all, s->rec_all)) return st;
+        MPB_CUDA(cudaGraphLaunch(s->g_all, s->ctx->stream));
+        ++s->runs;
+        return MPB_OK;
+    }
     if (s->g_layers || s->g_score) {
         if ((phases & MPB_STEP_LAYERS) && s->g_layers) {
-            const size_t set = (s->runs % mpb_step::kRing) * s->chunks.size();
-            for (const auto &[node, which] : s->rec_nodes)
-                MPB_CUDA(cudaGraphExecEventRecordNodeSetEvent(
-                    s->g_layers, node, (which & 1) ? s->ev_r1[set + which / 2] : s->ev_r0[set + which / 2]));
+            if (mpb_status st = retarget_timing(s, s->g_layers, s->rec_layers)) return st;
             MPB_CUDA(cudaGraphLaunch(s->g_layers, s->ctx->stream));
             ++s->runs;
         }
@@ -345,7 +417,7 @@ mpb_status mpb_step_run(mpb_step *s, uint32_t phases) {
 
 mpb_status mpb_step_capture(mpb_step *s) {
     if (!s) return fail(MPB_VALIDATION_ERROR, "mpb_step_capture: NULL step");
-    if (s->g_layers || s->g_score) return MPB_OK;
+    if (s->g_layers || s->g_score || s->g_all) return MPB_OK;
     // one eager run sizes every workspace and uploads the router descriptor tables
     for (uint32_t ph : {MPB_STEP_LAYERS, MPB_STEP_SCORE}) {
         const uint64_t n0 = launch_total(s);
@@ -354,58 +426,16 @@ mpb_status mpb_step_capture(mpb_step *s) {
         if (ph == MPB_STEP_LAYERS) ++s->runs;
     }
     if (mpb_status st = mpb_step_sync(s)) return st;
-    cudaGraphExec_t *dst[2] = {&s->g_layers, &s->g_score};
-    const uint32_t phs[2] = {MPB_STEP_LAYERS, MPB_STEP_SCORE};
-    for (int i = 0; i < 2; ++i) {
-        if (phs[i] == MPB_STEP_SCORE) {
-            bool any = false;
-            for (const mpb_score_job &j : s->jobs) any = any || !score_in_layers(s, j);
-            if (!any) continue;
-        }
-        MPB_CUDA(cudaStreamBeginCapture(s->s_cap, cudaStreamCaptureModeRelaxed));
-        s->capturing = true;
-        s->origin = s->s_cap;
-        mpb_status st = run_phases(s, phs[i]);
-        s->capturing = false;
-        cudaGraph_t g = nullptr;
-        const cudaError_t e = cudaStreamEndCapture(s->s_cap, &g);
-        if (st) {
-            if (g) cudaGraphDestroy(g);
-            return st;
-        }
-        if (e != cudaSuccess) return cuda_fail(e, "mpb_step_capture: cudaStreamEndCapture");
-        const cudaError_t e2 = cudaGraphInstantiate(dst[i], g, 0);
-        if (e2 != cudaSuccess) {
-            cudaGraphDestroy(g);
-            return cuda_fail(e2, "mpb_step_capture: cudaGraphInstantiate");
-        }
-        if (phs[i] != MPB_STEP_LAYERS) {
-            cudaGraphDestroy(g);
-            continue;
-        }
-        // the router timing events are event-record nodes: find them, so each
-        // launch can point them at its own ring set
-        s->graph_layers = g;
-        size_t n = 0;
-        MPB_CUDA(cudaGraphGetNodes(g, nullptr, &n));
-        std::vector<cudaGraphNode_t> nodes(n);
-        MPB_CUDA(cudaGraphGetNodes(g, nodes.data(), &n));
-        const size_t set = (s->runs % mpb_step::kRing) * s->chunks.size();
-        for (cudaGraphNode_t nd : nodes) {
-            cudaGraphNodeType t;
-            MPB_CUDA(cudaGraphNodeGetType(nd, &t));
-            if (t != cudaGraphNodeTypeEventRecord) continue;
-            cudaEvent_t ev;
-            MPB_CUDA(cudaGraphEventRecordNodeGetEvent(nd, &ev));
-            for (size_t c = 0; c < s->chunks.size(); ++c) {
-                if (ev == s->ev_r0[set + c]) s->rec_nodes.emplace_back(nd, static_cast<uint32_t>(2 * c));
-                if (ev == s->ev_r1[set + c]) s->rec_nodes.emplace_back(nd, static_cast<uint32_t>(2 * c + 1));
-            }
-        }
-        if (s->rec_nodes.size() != 2 * s->chunks.size())
-            return fail(MPB_CUDA_ERROR, "mpb_step_capture: router timing nodes not found in the graph");
+    if (mpb_status st = capture_graph(s, MPB_STEP_LAYERS, &s->g_layers, &s->graph_layers, &s->rec_layers))
+        return st;
+    bool any = false;
+    for (const mpb_score_job &j : s->jobs) any = any || !score_in_layers(s, j);
+    if (any) {
+        cudaGraph_t unused = nullptr;
+        mpb_step::RecNodes none;
+        if (mpb_status st = capture_graph(s, MPB_STEP_SCORE, &s->g_score, &unused, &none)) return st;
     }
-    return MPB_OK;
+    return capture_graph(s, MPB_STEP_LAYERS | MPB_STEP_SCORE, &s->g_all, &s->graph_all, &s->rec_all);
 }
 
 mpb_status mpb_step_sync(mpb_step *s) {

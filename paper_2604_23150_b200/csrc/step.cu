@@ -426,16 +426,25 @@ mpb_status mpb_step_capture(mpb_step *s) {
         if (ph == MPB_STEP_LAYERS) ++s->runs;
     }
     if (mpb_status st = mpb_step_sync(s)) return st;
-    if (mpb_status st = capture_graph(s, MPB_STEP_LAYERS, &s->g_layers, &s->graph_layers, &s->rec_layers))
-        return st;
+    mpb_status st = capture_graph(s, MPB_STEP_LAYERS, &s->g_layers, &s->graph_layers, &s->rec_layers);
     bool any = false;
     for (const mpb_score_job &j : s->jobs) any = any || !score_in_layers(s, j);
-    if (any) {
+    if (!st && any) {
         cudaGraph_t unused = nullptr;
         mpb_step::RecNodes none;
-        if (mpb_status st = capture_graph(s, MPB_STEP_SCORE, &s->g_score, &unused, &none)) return st;
+        st = capture_graph(s, MPB_STEP_SCORE, &s->g_score, &unused, &none);
     }
-    return capture_graph(s, MPB_STEP_LAYERS | MPB_STEP_SCORE, &s->g_all, &s->graph_all, &s->rec_all);
+    if (!st) st = capture_graph(s, MPB_STEP_LAYERS | MPB_STEP_SCORE, &s->g_all, &s->graph_all, &s->rec_all);
+    if (st) {  // all or nothing: a failed capture leaves the plan eager
+        for (cudaGraphExec_t *g : {&s->g_layers, &s->g_score, &s->g_all})
+            if (*g) cudaGraphExecDestroy(*g), *g = nullptr;
+        for (cudaGraph_t *g : {&s->graph_layers, &s->graph_all})
+            if (*g) cudaGraphDestroy(*g), *g = nullptr;
+        s->rec_layers.clear();
+        s->rec_all.clear();
+        cudaGetLastError();
+    }
+    return st;
 }
 
 mpb_status mpb_step_sync(mpb_step *s) {

@@ -7,6 +7,14 @@
 set -x
 OUT=gpurun_out/prof
 mkdir -p $OUT
+# ncu reports are exported to CSV on the box and removed (gpurun copies back <= 64 MiB)
+export_rep() {
+  ncu -i $1.ncu-rep --page raw --csv > $1.raw.csv 2>/dev/null
+  ncu -i $1.ncu-rep --page details --csv > $1.details.csv 2>/dev/null
+  ncu -i $1.ncu-rep --page source --csv --print-source sass > $1.source.csv 2>/dev/null
+  gzip -f $1.source.csv $1.details.csv
+  rm -f $1.ncu-rep
+}
 # 1. plain bench lines (no profiler), one per BASELINE workload
 for W in dsv3 qwen3 maverick domain; do
   python bench.py --workload $W > $OUT/bench_$W.json 2> $OUT/bench_$W.err
@@ -27,6 +35,7 @@ for W in dsv3 qwen3 maverick domain; do
   python tools/prof_router.py ${SHAPE[$W]} --iters 5 > $OUT/router_plain_$W.log 2>&1 && \
   ncu --set full --clock-control none --import-source on -k regex:k_router -s 2 -c 1 \
       -o $OUT/router_$W python tools/prof_router.py ${SHAPE[$W]} --iters 1 > $OUT/ncu_router_$W.log 2>&1
+  export_rep $OUT/router_$W
 done
 python tools/prof_router.py --layers 8 --iters 5 > $OUT/router_grouped_plain.log 2>&1
 # 4. statistics / scoring kernels: full captures at the DSv3 step shape (tools/kbench.py),
@@ -36,4 +45,6 @@ python tools/kbench.py --once > $OUT/kbench_once.log 2>&1 && \
 ncu --set full --clock-control none --import-source on \
     -k regex:"k_layout_count|k_layout_scan|k_layout_scatter|k_coact_mma|k_score|k_finalize" \
     -c 20 -o $OUT/small_full python tools/kbench.py --once > $OUT/ncu_small.log 2>&1
+export_rep $OUT/small_full
+gzip -f $OUT/launches_dsv3.csv $OUT/launches_qwen3.csv
 ls -la $OUT

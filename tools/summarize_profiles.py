@@ -26,8 +26,13 @@ SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
 
 
 def raw(rep):
-    out = subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv"], capture_output=True,
-                         text=True).stdout
+    rep = Path(rep)
+    csv_path = rep.with_suffix("").with_suffix(".raw.csv") if rep.suffix == ".ncu-rep" else rep
+    if csv_path.exists():  # exported on the box (tools/profile_round.sh export_rep)
+        out = csv_path.read_text()
+    else:
+        out = subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv"],
+                             capture_output=True, text=True).stdout
     rows = list(csv.reader(out.splitlines()))
     hdr, units = rows[0], rows[1]
     return [(dict(zip(hdr, r)), dict(zip(hdr, units))) for r in rows[2:]]
@@ -69,11 +74,17 @@ def kernel_rows(rep):
 
 def launch_shares(w, bench):
     src = SRC / f"launches_{w}.csv"
-    if not src.exists():
+    gz = SRC / f"launches_{w}.csv.gz"
+    if gz.exists():
+        shutil.copy(gz, DST / f"{RND}_launches_{w}.csv.gz")
+        text = gzip.open(gz, "rt").read()
+    elif src.exists():
+        with open(src, "rb") as f, gzip.open(DST / f"{RND}_launches_{w}.csv.gz", "wb") as g:
+            shutil.copyfileobj(f, g)
+        text = src.read_text()
+    else:
         return
-    with open(src, "rb") as f, gzip.open(DST / f"{RND}_launches_{w}.csv.gz", "wb") as g:
-        shutil.copyfileobj(f, g)
-    rows = list(csv.reader(open(src)))
+    rows = list(csv.reader(text.splitlines()))
     start = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
     hdr = rows[start]
     ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
@@ -124,7 +135,7 @@ summary = {"round": RND, "units": "each metric {value, unit} from ncu's raw page
 plain = []
 for w in ("dsv3", "qwen3", "maverick", "domain"):
     rep = SRC / f"router_{w}.ncu-rep"
-    if rep.exists():
+    if rep.exists() or (SRC / f"router_{w}.raw.csv").exists():
         rows = kernel_rows(rep)
         if rows:
             summary[WORKLOADS[w].name] = rows[0]
@@ -141,7 +152,7 @@ if (SRC / "router_grouped_plain.log").exists():
 
 # 3. statistics / scoring kernels
 rep = SRC / "small_full.ncu-rep"
-if rep.exists():
+if rep.exists() or (SRC / "small_full.raw.csv").exists():
     small = kernel_rows(rep)
     (DST / f"{RND}_ncu_small_kernels.json").write_text(json.dumps(small, indent=1))
     for s in small:

@@ -245,7 +245,10 @@ def run_e2e(pipe, steps: int):
         avail = psutil.virtual_memory().available
     except ImportError:
         avail = 0
-    n_host = max(2, min(L, int(0.6 * avail) // layer_bytes)) if avail else 2
+    # every rank of the node pins its own copy: share half of the host's free RAM
+    local_world = int(os.environ.get("LOCAL_WORLD_SIZE", os.environ.get("WORLD_SIZE", "1")))
+    budget = int(0.5 * avail) // max(1, local_world)
+    n_host = max(2, min(L, budget // layer_bytes)) if avail else 2
     host = []
     for i in range(n_host):
         h = torch.empty(T, H, dtype=torch.bfloat16, pin_memory=True)

@@ -88,7 +88,7 @@ def launch_shares(w, bench):
     start = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
     hdr = rows[start]
     ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
-    scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}
+    scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "ns": 1e-3, "us": 1.0, "ms": 1e3}
     seq = [(r[ki], num(r[vi]) * scale.get(r[ui], float("nan"))) for r in rows[start + 1:]
            if len(r) > vi]
     # the last routed step: from its first router launch onwards, up to the

@@ -361,20 +361,38 @@ __global__ void __launch_bounds__(kThreads) k_layout_scan(uint32_t *bhist, uint3
     scan_columns(bhist, nb, NS, totals, blockIdx.x);
 }
 
-template <bool kFused>
+// kInline: the count pass's raw per-block slot counts are scanned here (each
+// block sums the bhist column of every slot: its own exclusive prefix over the
+// blocks and the slot total) — for small nb * NS (decode batches) this replaces
+// the separate scan launch.
+template <bool kFused, bool kInline = false>
 __device__ __forceinline__ void scatter_body(const LayoutParams &p, int32_t *sorted_pairs,
                                              int32_t *pair_pos, const uint16_t *key_lb,
                                              uint32_t nkeys, int64_t *key_offsets,
-                                             uint32_t *s_w) {  // [kWarps][NS] counts / positions, [NS+1] bases
+                                             uint32_t *s_w) {  // [kWarps][NS] counts / positions, [NS+1] bases[, NS prefixes]
     __shared__ uint32_t s_warp[32];
     uint32_t *s_base = s_w + kWarps * p.NS;
+    uint32_t *s_pref = s_base + p.NS + 1;
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     // slot bases: exclusive scan of the slot totals (coalesced loads into smem,
     // then a blocked scan; every block, NS is small)
     if (!kFused) pdl_trigger();
     for (uint32_t i = threadIdx.x; i < kWarps * p.NS; i += kThreads) s_w[i] = 0;
     if (!kFused) pdl_wait();
-    for (uint32_t i = threadIdx.x; i < p.NS; i += kThreads) s_base[i] = __ldcg(p.totals + i);
+    if (kInline) {
+        for (uint32_t i = threadIdx.x; i < p.NS; i += kThreads) {
+            uint32_t pre = 0, tot = 0;
+            for (uint32_t b = 0; b < p.nb; ++b) {
+                const uint32_t v = __ldcg(p.bhist + static_cast<size_t>(b) * p.NS + i);
+                pre += b < blockIdx.x ? v : 0u;
+                tot += v;
+            }
+            s_base[i] = tot;
+            s_pref[i] = pre;
+        }
+    } else {
+        for (uint32_t i = threadIdx.x; i < p.NS; i += kThreads) s_base[i] = __ldcg(p.totals + i);
+    }
     __syncthreads();
     {
         const uint32_t per = (p.NS + kThreads - 1) / kThreads;
@@ -438,7 +456,7 @@ __device__ __forceinline__ void scatter_body(const LayoutParams &p, int32_t *sor
     __syncthreads();
     // per slot: exclusive prefix over warps, seeded with the block's global offset
     for (uint32_t s = threadIdx.x; s < p.NS; s += kThreads) {
-        uint32_t run = s_base[s] + p.bhist[static_cast<size_t>(blockIdx.x) * p.NS + s];
+        uint32_t run = s_base[s] + (kInline ? s_pref[s] : p.bhist[static_cast<size_t>(blockIdx.x) * p.NS + s]);
 #pragma unroll
         for (int w = 0; w < kWarps; ++w) {
             const uint32_t c = s_w[w * p.NS + s];
@@ -491,13 +509,14 @@ __device__ __forceinline__ void scatter_body(const LayoutParams &p, int32_t *sor
     }
 }
 
+template <bool kInline>
 __global__ void __launch_bounds__(kThreads) k_layout_scatter(LayoutParams p, int32_t *sorted_pairs,
                                                              int32_t *pair_pos,
                                                              const uint16_t *key_lb,
                                                              uint32_t nkeys,
                                                              int64_t *key_offsets) {
     extern __shared__ uint32_t s_w[];
-    scatter_body<false>(p, sorted_pairs, pair_pos, key_lb, nkeys, key_offsets, s_w);
+    scatter_body<false, kInline>(p, sorted_pairs, pair_pos, key_lb, nkeys, key_offsets, s_w);
 }
 
 // Grid-wide barrier of a launch whose blocks are all resident (nb <= SMs):
@@ -620,7 +639,7 @@ mpb_status launch_layout(mpb_context *ctx, const mpb_tokens *tk, const mpb_place
     const uint64_t P = tk->T * tk->k;
     if (P > 0x7fffffffull)
         return fail(MPB_CONFIG_ERROR, "mpb_dispatch_layout: T*k must fit int32 pair ids");
-    if (perm && (size_t(pl->NS) * kWarps + pl->NS + 1) * 4 > kSmemLimit)
+    if (perm && (size_t(pl->NS) * kWarps + 2 * size_t(pl->NS) + 1) * 4 > kSmemLimit)
         return fail(MPB_CONFIG_ERROR, "mpb_dispatch_layout: too many (group, expert) slots "
                                       "for the permutation");
     if (P == 0) {
@@ -708,13 +727,18 @@ mpb_status launch_layout(mpb_context *ctx, const mpb_tokens *tk, const mpb_place
     MPB_CUDA(launch_pdl(count, dim3(nb), dim3(kThreads), smem, ctx->stream, p));
     MPB_LAUNCHED(ctx);
     if (!perm) return MPB_OK;
-    MPB_CUDA(launch_pdl(k_layout_scan, dim3((pl->NS + 31) / 32), dim3(kThreads), 0, ctx->stream,
-                        p.bhist, nb, pl->NS, p.totals));
-    MPB_LAUNCHED(ctx);
-    const size_t sc_smem = (size_t(kWarps) * pl->NS + pl->NS + 1) * 4;
-    MPB_CUDA(cudaFuncSetAttribute(k_layout_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  int(sc_smem)));
-    MPB_CUDA(launch_pdl(k_layout_scatter, dim3(nb), dim3(kThreads), sc_smem, ctx->stream, p,
+    // small nb * NS: every scatter block scans its slot columns itself (no scan launch)
+    static const bool no_inline = std::getenv("MPB_LAYOUT_SCAN_KERNEL") != nullptr;
+    const bool inl = !no_inline && uint64_t(nb) * pl->NS <= 65536;
+    if (!inl) {
+        MPB_CUDA(launch_pdl(k_layout_scan, dim3((pl->NS + 31) / 32), dim3(kThreads), 0, ctx->stream,
+                            p.bhist, nb, pl->NS, p.totals));
+        MPB_LAUNCHED(ctx);
+    }
+    const size_t sc_smem = (size_t(kWarps) * pl->NS + pl->NS + 1 + (inl ? pl->NS : 0)) * 4;
+    auto scatter = inl ? k_layout_scatter<true> : k_layout_scatter<false>;
+    MPB_CUDA(cudaFuncSetAttribute(scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sc_smem)));
+    MPB_CUDA(launch_pdl(scatter, dim3(nb), dim3(kThreads), sc_smem, ctx->stream, p,
                         sorted_pairs, pair_pos, pl->d_key_lb, pl->D * pl->E, key_offsets));
     MPB_LAUNCHED(ctx);
     return MPB_OK;

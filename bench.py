@@ -494,7 +494,7 @@ def run_gpu_arm(args, spec):
                            "experts": spec.experts, "top_k": spec.top_k,
                            "ep_groups": spec.groups, "nodes": spec.nodes,
                            "domains": spec.domains, "candidates": spec.candidates,
-                           "parallelism": f"dp{world} (token shards) + NCCL stats all-reduce",
+                           "parallelism": f"dp{world} (token shards); per-chunk NCCL all-reduce of the statistics and all-gather of the sharded scores issued by the C++ step" if world > 1 else "dp1",
                            "schedule": pipe.schedule(),
                            "l2": "inputs larger than L2 (each layer's X is "
                                  f"{spec.tokens * spec.hidden * 2 / 2**20:.0f} MiB)"},

@@ -391,6 +391,25 @@ typedef struct {
     uint32_t score_per_chunk;
 } mpb_step_desc;
 
+/* Multi-GPU collectives issued by the plan itself (NCCL over NVLink): after
+ * each chunk's statistics tails, one grouped in-place all-reduce (sum, uint64)
+ * of that chunk's per-layer demand / demand2 slices on the side stream —
+ * beside the next routers — so every chunk is priced on the GLOBAL demand
+ * right away (score jobs with B == layers, each rank its own candidate slice);
+ * after the last chunk, the all-reduce of tag_pop / coact and an in-place
+ * all-gather of the `gather` buffers (rank r's slice at r * bytes_per_rank).
+ * Everything stays inside the step's CUDA graphs. The caller broadcasts rank
+ * 0's id (mpb_nccl_get_unique_id) to every rank before mpb_step_attach_comm.
+ * NCCL is resolved at run time (dlopen of libnccl.so.2: the copy already
+ * loaded in the process, e.g. torch's, else the system one). */
+typedef struct {
+    void *buf;                  /* device buffer holding every rank's slice */
+    uint64_t bytes_per_rank;    /* slice size (bytes) */
+} mpb_gather_spec;
+MPB_API mpb_status mpb_nccl_get_unique_id(uint8_t id[128]);
+MPB_API mpb_status mpb_step_attach_comm(mpb_step *step, const uint8_t id[128], int world, int rank,
+                                        const mpb_gather_spec *gather, uint32_t n_gather);
+
 #define MPB_STEP_LAYERS 1u
 #define MPB_STEP_SCORE 2u
 MPB_API mpb_status mpb_step_create(mpb_context *ctx, const mpb_step_desc *desc, mpb_step **out);

@@ -49,6 +49,10 @@ class MpbStepDesc(C.Structure):
                 ("score_per_chunk", C.c_uint32)]
 
 
+class MpbGatherSpec(C.Structure):
+    _fields_ = [("buf", _p), ("bytes_per_rank", C.c_uint64)]
+
+
 _SIGS = {
     "mpb_abi_version": (C.c_int, []),
     "mpb_last_error_message": (C.c_char_p, []),
@@ -107,6 +111,8 @@ _SIGS = {
     "mpb_step_timing_reset": (C.c_int, [_p]),
     "mpb_step_router_ms": (C.c_int, [_p, _f32p, _u32p]),
     "mpb_step_info": (C.c_int, [_p, C.c_uint32, _u64p, _u32p, _u32p]),
+    "mpb_nccl_get_unique_id": (C.c_int, [_p]),
+    "mpb_step_attach_comm": (C.c_int, [_p, _p, C.c_int, C.c_int, _p, C.c_uint32]),
     "mpb_linear_placement": (C.c_int, [C.c_uint32, C.c_uint32, _p]),
     "mpb_eplb_placement": (C.c_int, [_p, C.c_uint32, C.c_uint32, _p]),
     "mpb_phase1_unique_distribution": (C.c_int, [_p, C.c_uint32, C.c_uint32, _p, _p]),

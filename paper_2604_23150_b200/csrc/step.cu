@@ -20,12 +20,59 @@
 // last router are short. Every layer owns its idx / weights slice, so routers
 // never wait on tails. Both phases order after the work already on the
 // caller's stream and before anything enqueued after them.
+#include <dlfcn.h>
+#include <nccl.h>  // types and prototypes only: the functions are resolved at run time
+
 #include <algorithm>
 #include <cstring>
 #include <utility>
 #include <vector>
 
 #include "internal.cuh"
+
+namespace {
+// NCCL, resolved at run time: the libnccl.so.2 already loaded in the process
+// (torch's), else the system one. No link-time dependency.
+struct NcclApi {
+    decltype(&ncclGetUniqueId) get_unique_id = nullptr;
+    decltype(&ncclCommInitRank) init_rank = nullptr;
+    decltype(&ncclCommDestroy) destroy = nullptr;
+    decltype(&ncclAllReduce) all_reduce = nullptr;
+    decltype(&ncclAllGather) all_gather = nullptr;
+    decltype(&ncclGroupStart) group_start = nullptr;
+    decltype(&ncclGroupEnd) group_end = nullptr;
+    decltype(&ncclGetErrorString) error_string = nullptr;
+    bool ok = false;
+};
+const NcclApi &nccl() {
+    static const NcclApi api = [] {
+        NcclApi a;
+        void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW);
+        if (!h) return a;
+        a.get_unique_id = reinterpret_cast<decltype(a.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+        a.init_rank = reinterpret_cast<decltype(a.init_rank)>(dlsym(h, "ncclCommInitRank"));
+        a.destroy = reinterpret_cast<decltype(a.destroy)>(dlsym(h, "ncclCommDestroy"));
+        a.all_reduce = reinterpret_cast<decltype(a.all_reduce)>(dlsym(h, "ncclAllReduce"));
+        a.all_gather = reinterpret_cast<decltype(a.all_gather)>(dlsym(h, "ncclAllGather"));
+        a.group_start = reinterpret_cast<decltype(a.group_start)>(dlsym(h, "ncclGroupStart"));
+        a.group_end = reinterpret_cast<decltype(a.group_end)>(dlsym(h, "ncclGroupEnd"));
+        a.error_string = reinterpret_cast<decltype(a.error_string)>(dlsym(h, "ncclGetErrorString"));
+        a.ok = a.get_unique_id && a.init_rank && a.destroy && a.all_reduce && a.all_gather &&
+               a.group_start && a.group_end && a.error_string;
+        return a;
+    }();
+    return api;
+}
+}  // namespace
+
+#define MPB_NCCL(call)                                                                      \
+    do {                                                                                    \
+        ncclResult_t r_ = (call);                                                           \
+        if (r_ != ncclSuccess)                                                              \
+            return ::mpb::fail(MPB_CUDA_ERROR, std::string("NCCL error in " #call ": ") +     \
+                                                   nccl().error_string(r_));                \
+    } while (0)
 
 struct mpb_step {
     mpb_context *ctx = nullptr;  // the caller's (ordering) context
@@ -57,6 +104,10 @@ struct mpb_step {
     // stream the phases order against: the caller's stream, or during capture
     // a plan-owned origin stream (the legacy default stream cannot capture)
     cudaStream_t origin = nullptr, s_cap = nullptr;
+    // multi-GPU (mpb_step_attach_comm)
+    ncclComm_t comm = nullptr;
+    int world = 1, rank = 0;
+    std::vector<mpb_gather_spec> gather;
 };
 
 namespace {
@@ -100,6 +151,41 @@ mpb_status tail(mpb_step *s, mpb_context *c, uint32_t l) {
             d.demand2 ? d.demand2 + static_cast<size_t>(l) * D * E : nullptr, d.tag_pop,
             d.sorted_pairs, d.pair_pos, d.key_offsets))
         return st;
+    return MPB_OK;
+}
+
+// In-place all-reduce (sum, uint64) of layers [l0, l1) of the per-layer demand
+// tables, plus the whole-step tag / co-activation tables when `whole`.
+mpb_status reduce_stats(mpb_step *s, uint32_t l0, uint32_t l1, bool whole, cudaStream_t st) {
+    if (!s->comm) return MPB_OK;
+    const mpb_step_desc &d = s->d;
+    const size_t DE = static_cast<size_t>(d.deployed->D) * d.E;
+    const NcclApi &n = nccl();
+    MPB_NCCL(n.group_start());
+    MPB_NCCL(n.all_reduce(d.demand + l0 * DE, d.demand + l0 * DE, (l1 - l0) * DE, ncclUint64, ncclSum,
+                          s->comm, st));
+    if (d.demand2)
+        MPB_NCCL(n.all_reduce(d.demand2 + l0 * DE, d.demand2 + l0 * DE, (l1 - l0) * DE, ncclUint64,
+                              ncclSum, s->comm, st));
+    if (whole && d.tag_pop && d.n_tags)
+        MPB_NCCL(n.all_reduce(d.tag_pop, d.tag_pop, size_t(d.n_tags) * d.E, ncclUint64, ncclSum, s->comm, st));
+    if (whole && d.coact)
+        MPB_NCCL(n.all_reduce(d.coact, d.coact, size_t(d.E) * d.E, ncclUint64, ncclSum, s->comm, st));
+    MPB_NCCL(n.group_end());
+    return MPB_OK;
+}
+
+// In-place all-gather of the sharded score outputs (rank r's slice at r * bytes).
+mpb_status gather_scores(mpb_step *s, cudaStream_t st) {
+    if (!s->comm || s->gather.empty()) return MPB_OK;
+    const NcclApi &n = nccl();
+    MPB_NCCL(n.group_start());
+    for (const mpb_gather_spec &g : s->gather) {
+        char *base = static_cast<char *>(g.buf);
+        MPB_NCCL(n.all_gather(base + size_t(s->rank) * g.bytes_per_rank, base, g.bytes_per_rank, ncclUint8,
+                              s->comm, st));
+    }
+    MPB_NCCL(n.group_end());
     return MPB_OK;
 }
 
@@ -169,9 +255,13 @@ mpb_status run_layers(mpb_step *s) {
                 if (d.coact && (st = mpb_coactivation(tc, d.idx + l * pairs, d.T, d.k, d.E, d.coact)))
                     return st;
             }
-            if (d.score_per_chunk)
+            // multi-GPU: this chunk's demand becomes global before it is priced
+            if ((st = reduce_stats(s, l0, l1, c + 1 == nc, tc->stream))) return st;
+            if (d.score_per_chunk) {
                 for (const mpb_score_job &j : s->jobs)
                     if (j.B == d.layers && (st = score_finalize_range(tc, j, l0, l1 - l0))) return st;
+                if (c + 1 == nc && (st = gather_scores(s, tc->stream))) return st;
+            }
         }
     } else {
         for (size_t c = 0; c < s->chunks.size(); ++c) {
@@ -193,6 +283,7 @@ mpb_status run_layers(mpb_step *s) {
     }
     MPB_CUDA(cudaEventRecord(s->ev_join, s->s_side));
     MPB_CUDA(cudaStreamWaitEvent(s->s_main, s->ev_join, 0));
+    if (!s->overlapped && (st = reduce_stats(s, 0, d.layers, true, s->s_main))) return st;
     MPB_CUDA(cudaEventRecord(s->ev_out, s->s_main));
     MPB_CUDA(cudaStreamWaitEvent(s->origin, s->ev_out, 0));
     return MPB_OK;
@@ -220,6 +311,7 @@ mpb_status run_score(mpb_step *s) {
     }
     MPB_CUDA(cudaEventRecord(s->ev_join, s->s_side));
     MPB_CUDA(cudaStreamWaitEvent(s->s_main, s->ev_join, 0));
+    if (mpb_status st = gather_scores(s, s->s_main)) return st;
     MPB_CUDA(cudaEventRecord(s->ev_out, s->s_main));
     MPB_CUDA(cudaStreamWaitEvent(s->origin, s->ev_out, 0));
     return MPB_OK;
@@ -313,6 +405,7 @@ mpb_status mpb_step_destroy(mpb_step *s) {
     if (s->g_all) cudaGraphExecDestroy(s->g_all);
     if (s->graph_all) cudaGraphDestroy(s->graph_all);
     if (s->g_score) cudaGraphExecDestroy(s->g_score);
+    if (s->comm) nccl().destroy(s->comm);
     mpb_context_destroy(s->main);
     mpb_context_destroy(s->side);
     for (cudaEvent_t ev : {s->ev_in, s->ev_out, s->ev_fork, s->ev_join, s->ev_zero})
@@ -494,6 +587,38 @@ mpb_status mpb_step_info(const mpb_step *s, uint32_t phases, uint64_t *launches,
     if (n_chunks) *n_chunks = static_cast<uint32_t>(s->chunks.size());
     if (chunks)
         for (size_t c = 0; c < s->chunks.size(); ++c) chunks[c] = s->chunks[c].second - s->chunks[c].first;
+    return MPB_OK;
+}
+
+mpb_status mpb_nccl_get_unique_id(uint8_t id[128]) {
+    if (!id) return fail(MPB_VALIDATION_ERROR, "mpb_nccl_get_unique_id: NULL id");
+    if (!nccl().ok) return fail(MPB_CONFIG_ERROR, "mpb_nccl_get_unique_id: libnccl.so.2 not found");
+    ncclUniqueId u;
+    MPB_NCCL(nccl().get_unique_id(&u));
+    std::memcpy(id, u.internal, sizeof(u.internal));
+    return MPB_OK;
+}
+
+mpb_status mpb_step_attach_comm(mpb_step *s, const uint8_t id[128], int world, int rank,
+                                const mpb_gather_spec *gather, uint32_t n_gather) {
+    if (!s || !id) return fail(MPB_VALIDATION_ERROR, "mpb_step_attach_comm: NULL argument");
+    if (world < 1 || rank < 0 || rank >= world) return fail(MPB_CONFIG_ERROR, "mpb_step_attach_comm: bad rank");
+    if (s->g_layers || s->g_score || s->g_all)
+        return fail(MPB_CONFIG_ERROR, "mpb_step_attach_comm: attach before mpb_step_capture");
+    if (n_gather && !gather) return fail(MPB_VALIDATION_ERROR, "mpb_step_attach_comm: NULL gather");
+    if (!nccl().ok) return fail(MPB_CONFIG_ERROR, "mpb_step_attach_comm: libnccl.so.2 not found");
+    if (s->comm) {
+        nccl().destroy(s->comm);
+        s->comm = nullptr;
+    }
+    s->world = world;
+    s->rank = rank;
+    s->gather.assign(gather, gather + n_gather);
+    if (world == 1) return MPB_OK;
+    ncclUniqueId u;
+    std::memcpy(u.internal, id, sizeof(u.internal));
+    MPB_CUDA(cudaSetDevice(s->ctx->device));
+    MPB_NCCL(nccl().init_rank(&s->comm, world, u, rank));
     return MPB_OK;
 }
 

@@ -649,6 +649,29 @@ class StepPlan:
         self.handle = h
         self.graphed = False
 
+    def attach_comm(self, rank: int, world: int, gather=(), group=None) -> None:
+        """Multi-GPU: the plan issues its own NCCL collectives (per-chunk demand
+        all-reduce beside the next routers, the tag / co-activation all-reduce
+        and the all-gather of the sharded score rows) inside the step and its
+        graphs. Rank 0's NCCL id travels over torch.distributed. `gather`:
+        (full device tensor, bytes per rank) pairs, rank r's slice at r * bytes."""
+        import torch.distributed as dist
+        uid = torch.zeros(128, dtype=torch.uint8)
+        if rank == 0:
+            buf = (C.c_uint8 * 128)()
+            _abi.call("mpb_nccl_get_unique_id", buf)
+            uid = torch.tensor(list(buf), dtype=torch.uint8)
+        dev_uid = uid.to(self.engine.device)
+        dist.broadcast(dev_uid, src=0, group=group)
+        ub = (C.c_uint8 * 128)(*dev_uid.cpu().tolist())
+        specs = (_abi.MpbGatherSpec * max(1, len(gather)))()
+        for i, (t, nbytes) in enumerate(gather):
+            specs[i].buf = t.data_ptr()
+            specs[i].bytes_per_rank = nbytes
+        self._keep.append([t for t, _ in gather])
+        _abi.call("mpb_step_attach_comm", self.handle, ub, world, rank, specs, len(gather))
+        self.world = world
+
     def run(self, phases: int = 3) -> None:
         _abi.call("mpb_step_run", self.handle, phases)
 

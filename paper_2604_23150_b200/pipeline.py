@@ -292,6 +292,9 @@ class RoutingPipeline:
 
     def _build_plan(self):
         s, eng = self.spec, self.eng
+        # multi-GPU collectives issued by the C++ plan (NCCL, overlapped with the
+        # routers); MPB_STEP_NCCL=0: torch.distributed between the two phases
+        self.plan_comm = self.world > 1 and os.environ.get("MPB_STEP_NCCL", "1") != "0"
         L, D = s.layers, s.groups
         lo, hi = self.shard if self.shard is not None else (0, self.luts_cl.shape[0])
         jobs = [mp.ScoreJob(self.dem_cl, self.luts_cl[lo:hi], self.g2n, D, self.cost,
@@ -306,9 +309,18 @@ class RoutingPipeline:
             coact=self.coact if s.coact else None, perm_out=(self.sp, self.pp, self.ko),
             zero=self.stats, score_jobs=jobs, side_sms=self.side_sms,
             router_group=self.router_group,
-            # one GPU: each chunk of layers is priced as soon as its statistics
-            # are in (multi-GPU scoring waits for the all-reduced demand)
-            score_per_chunk=self.world == 1 and os.environ.get("MPB_SCORE_PER_CHUNK", "1") != "0")
+            # each chunk of layers is priced as soon as its statistics are in
+            # (multi-GPU: right after the plan's per-chunk NCCL all-reduce)
+            score_per_chunk=os.environ.get("MPB_SCORE_PER_CHUNK", "1") != "0" and
+            (self.world == 1 or self.plan_comm))
+        if self.world > 1 and self.plan_comm:
+            gather = []
+            if self.shard is not None:  # rank r owns candidate rows [lo, hi) of fin_cl
+                lo, hi = self.shard
+                for t in self.fin_cl:
+                    row_bytes = t.shape[1] * t.element_size()
+                    gather.append((t, (hi - lo) * L * row_bytes))
+            self.plan.attach_comm(self.rank, self.world, gather)
         self.chunks, l0 = [], 0
         for n in self.plan.chunks():
             self.chunks.append((l0, l0 + n))
@@ -596,13 +608,13 @@ class RoutingPipeline:
     def step(self, timed_router=False, group=None):
         if self.plan is not None:
             P = self.plan
-            if self.world > 1:
+            if self.world > 1 and not self.plan_comm:  # MPB_STEP_NCCL=0: torch collectives
                 import torch.distributed as dist
                 P.run(P.LAYERS)
                 dist.all_reduce(self.stats.view(torch.int64), group=group)
                 P.run(P.SCORE)
                 self._gather_scores(group)
-            else:
+            else:  # the plan's own NCCL collectives (attach_comm) run inside
                 P.run(P.LAYERS | P.SCORE)
             self._plan_launched += P.launches(P.LAYERS | P.SCORE)
             return

@@ -29,3 +29,20 @@ def test_k6_multirank_bit_identity(world):
     res = json.loads(lines[-1])
     assert res["all_ranks_ok"], res
     assert res["rank0"]["recv_rows"] > 0
+
+
+@pytest.mark.parametrize("world", [2])
+def test_step_nccl_in_plan_equals_torch_collectives(world):
+    """The C++ step's own NCCL collectives (inside its CUDA graph) produce the
+    same statistics and LayerSim tables as torch.distributed collectives
+    between the phases, bit for bit, on every rank (tools/step_nccl_check.py)."""
+    if not torch.cuda.is_available() or torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        f"--nproc-per-node={world}", "--master-addr=127.0.0.1",
+                        f"--master-port={29640 + world}",
+                        str(ROOT / "tools" / "step_nccl_check.py")],
+                       capture_output=True, text=True, timeout=600, cwd=ROOT)
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert r.returncode == 0 and lines, r.stdout[-3000:] + r.stderr[-3000:]
+    assert json.loads(lines[-1])["all_ranks_bit_identical"]

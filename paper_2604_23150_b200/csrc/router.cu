@@ -209,9 +209,11 @@ __device__ __forceinline__ void cluster_tail(const RouterParams &p, const WorkIt
     }
     const uint32_t owner = q * S / 4u;
     const uint32_t rloc = q * 32u + lane - owner * RPS;  // row within the owner's share
-    if (owner != h) {  // stage the rows other CTAs own (local, conflict-free 16-byte stores)
+    {  // stage this CTA's partial of every row: other owners' shares for the bulk
+       // copies, its own share into the tile (local, conflict-free 16-byte stores)
         const uint32_t i = owner < h ? owner : owner - 1;
-        float *dst = snd + (static_cast<size_t>(i) * RPS + rloc) * RS;
+        float *dst = owner == h ? tile + static_cast<size_t>(rloc) * RS
+                                : snd + (static_cast<size_t>(i) * RPS + rloc) * RS;
 #pragma unroll 1
         for (int c = half * NH; c < (half + 1) * NH; c += 16) {
             uint32_t r[16];
@@ -223,11 +225,14 @@ __device__ __forceinline__ void cluster_tail(const RouterParams &p, const WorkIt
                     make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
                                 __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
         }
-        ptx::fence_proxy_async_smem();  // generic writes -> visible to the bulk-copy engine
+        if (owner != h) ptx::fence_proxy_async_smem();  // generic writes -> visible to the bulk-copy engine
     }
     asm volatile("bar.sync 5, 256;" ::: "memory");  // every share staged
     if (t == 0) {
         ptx::mbar_wait_cluster(peer_free, 0);  // every peer's pipeline smem is free
+#ifdef MPB_ROUTER_TRACE
+        RTRACE(14, gtime());
+#endif
         for (uint32_t o = 0; o < S; ++o) {
             if (o == h) continue;
             const uint32_t i = o < h ? o : o - 1;  // my share slot for owner o / my slot at o
@@ -237,38 +242,33 @@ __device__ __forceinline__ void cluster_tail(const RouterParams &p, const WorkIt
                           ptx::mapa(ptx::smem_u32(rx_full), o));
         }
     }
-    if (owner == h) {
-        ptx::mbar_wait_cluster(rx_full, 0);  // the peers' partials of my rows have landed
-#pragma unroll 1
-        for (int c = half * NH; c < (half + 1) * NH; c += 16) {
-            uint32_t r[16];
-            ptx::tmem_ld_32x32b_x16(taddr_q + c, r);
-            ptx::tmem_ld_wait();
+    ptx::mbar_wait_cluster(rx_full, 0);  // the peers' partials of my rows have landed
+#ifdef MPB_ROUTER_TRACE
+    if (t == 0) RTRACE(15, gtime());
+#endif
+    // every epilogue thread sums RPS*N/256 values of the share in K-part order
+    // 0..S-1 (a fixed fp32 order: the global-memory tail's), in place in the tile
+    for (uint32_t e4 = t; e4 < RPS * (N / 4); e4 += 256) {
+        const uint32_t rr = e4 / (N / 4), cc = (e4 % (N / 4)) * 4;
+        float4 *own = reinterpret_cast<float4 *>(tile + static_cast<size_t>(rr) * RS + cc);
+        float4 v[4];
 #pragma unroll
-            for (int j4 = 0; j4 < 4; ++j4) {
-                float4 tot;
-#pragma unroll 1
-                for (uint32_t part = 0; part < S; ++part) {  // K-part order: fixed fp32 sum order
-                    float4 v;
-                    if (part == h) {
-                        v = make_float4(__uint_as_float(r[4 * j4]), __uint_as_float(r[4 * j4 + 1]),
-                                        __uint_as_float(r[4 * j4 + 2]), __uint_as_float(r[4 * j4 + 3]));
-                    } else {
-                        const uint32_t i = part < h ? part : part - 1;
-                        v = *reinterpret_cast<const float4 *>(rx + (static_cast<size_t>(i) * RPS + rloc) * RS + c + 4 * j4);
-                    }
-                    if (part == 0) {
-                        tot = v;
-                    } else {
-                        tot.x += v.x;
-                        tot.y += v.y;
-                        tot.z += v.z;
-                        tot.w += v.w;
-                    }
-                }
-                *reinterpret_cast<float4 *>(tile + static_cast<size_t>(rloc) * RS + c + 4 * j4) = tot;
+        for (uint32_t part = 0; part < 4; ++part)
+            if (part < S) {
+                const uint32_t i = part < h ? part : part - 1;
+                v[part] = part == h ? *own
+                                    : *reinterpret_cast<const float4 *>(rx + (static_cast<size_t>(i) * RPS + rr) * RS + cc);
             }
-        }
+        float4 tot = v[0];
+#pragma unroll
+        for (uint32_t part = 1; part < 4; ++part)
+            if (part < S) {
+                tot.x += v[part].x;
+                tot.y += v[part].y;
+                tot.z += v[part].z;
+                tot.w += v[part].w;
+            }
+        *own = tot;
     }
     asm volatile("bar.sync 5, 256;" ::: "memory");  // the owned rows are summed
 #ifdef MPB_ROUTER_TRACE

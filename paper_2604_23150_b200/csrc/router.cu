@@ -396,10 +396,11 @@ __device__ __forceinline__ void cluster_tail(const RouterParams &p, const WorkIt
     }
     if (p.logits && token < p.T)
         for (uint32_t c = c0; c < c0 + CW && c < p.E; ++c) p.logits[out_row * p.E + c] = row[c];
-    if (sub != 0 || token >= p.T) return;
 #ifdef MPB_ROUTER_TRACE
     if (t == 0) RTRACE(13, gtime());
 #endif
+    // every lane of a row holds the same merged list: lane `sub` writes output
+    // slots sub, sub + TPR, ... (the renormalising sum over the row's lanes)
     const int k = static_cast<int>(p.k);
     int last = ti[0];  // ti[k - 1] without a dynamic register index (local memory)
 #pragma unroll
@@ -423,23 +424,39 @@ __device__ __forceinline__ void cluster_tail(const RouterParams &p, const WorkIt
             }
     }
     const float mlog = m * 1.4426950408889634f;
-    float w[KMAX];
-    float wsum = 0.f;
+    auto weight = [&](float v) {
+        if (isnan(v)) return 0.f;
+        return p.score_fn == MPB_SCORE_SOFTMAX ? exp2f(fmaf(v, 1.4426950408889634f, -mlog)) / ssum
+                                               : 1.f / (1.f + expf(-v));
+    };
+    auto slot = [&](int j, float &v, int &id) {  // tv[j], ti[j] with static indices
+        v = tv[0];
+        id = ti[0];
 #pragma unroll
-    for (int j = 0; j < KMAX; ++j) {
-        float x = 0.f;
-        if (j < k && !isnan(tv[j]))
-            x = p.score_fn == MPB_SCORE_SOFTMAX ? exp2f(fmaf(tv[j], 1.4426950408889634f, -mlog)) / ssum
-                                                : 1.f / (1.f + expf(-tv[j]));
-        w[j] = x;
-        wsum += x;
+        for (int jj = 1; jj < KMAX; ++jj)
+            if (jj == j) {
+                v = tv[jj];
+                id = ti[jj];
+            }
+    };
+    float wpart = 0.f;
+    for (int j = static_cast<int>(sub); j < k; j += static_cast<int>(TPR)) {
+        float v;
+        int id;
+        slot(j, v, id);
+        wpart += weight(v);
     }
-#pragma unroll
-    for (int j = 0; j < KMAX; ++j) {
-        if (j >= k) continue;
-        p.idx[out_row * p.k + j] = ti[j];
-        p.w[out_row * p.k + j] = p.renorm ? (wsum > 0.f ? w[j] / wsum : 0.f) : w[j];
-    }
+    float wsum = wpart;
+    for (uint32_t o = 1; o < TPR; o <<= 1) wsum += __shfl_xor_sync(0xffffffffu, wsum, o);
+    if (token < p.T)
+        for (int j = static_cast<int>(sub); j < k; j += static_cast<int>(TPR)) {
+            float v;
+            int id;
+            slot(j, v, id);
+            const float x = weight(v);
+            p.idx[out_row * p.k + j] = id;
+            p.w[out_row * p.k + j] = p.renorm ? (wsum > 0.f ? x / wsum : 0.f) : x;
+        }
 #ifdef MPB_ROUTER_TRACE
     if (t == 0) RTRACE(6, gtime());
 #endif

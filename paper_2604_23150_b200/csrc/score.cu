@@ -137,8 +137,10 @@ __global__ void __launch_bounds__(kScoreWarps * 32) k_score(const uint64_t *dema
     const uint32_t cols = kPrivate ? 32u : 1u;
     uint8_t *s_g2n = reinterpret_cast<uint8_t *>(s_acc + kScoreWarps * D * cols);
     const uint32_t b = b0 + blockIdx.x;  // batches [b0, b0 + gridDim.x) of B
+    pdl_trigger();
     for (uint32_t i = threadIdx.x; i < D; i += blockDim.x) s_g2n[i] = g2n_g[i];
     for (uint32_t i = threadIdx.x; i < NE; i += blockDim.x) s_nd[i] = 0;
+    pdl_wait();  // the demand / outputs belong to the previous kernels
     __syncthreads();
     const uint64_t *a = demand + static_cast<size_t>(b) * rows * E;
     for (uint32_t i = threadIdx.x; i < rows * E; i += blockDim.x) {
@@ -237,8 +239,10 @@ __global__ void __launch_bounds__(kScoreWarps * 32) k_score16(const uint64_t *de
     __shared__ uint8_t s_g2n[256];
     const uint32_t NE = nodes * E;
     const uint32_t b = b0 + blockIdx.x;  // batches [b0, b0 + gridDim.x) of B
+    pdl_trigger();
     for (uint32_t i = threadIdx.x; i < D; i += blockDim.x) s_g2n[i] = g2n_g[i];
     for (uint32_t i = threadIdx.x; i < NE; i += blockDim.x) s_nd[i] = 0;
+    pdl_wait();  // the demand / outputs belong to the previous kernels
     __syncthreads();
     const uint64_t *a = demand + static_cast<size_t>(b) * rows * E;
     for (uint32_t i = threadIdx.x; i < rows * E; i += blockDim.x) {
@@ -387,9 +391,11 @@ mpb_status launch_score(mpb_context *ctx, const char *fn, const uint64_t *demand
     gy = std::min(gy, (P + kScoreWarps - 1) / kScoreWarps);
     gy = std::min(gy, 65535u);
     dim3 grid(nb, gy);
-    kern<<<grid, kScoreWarps * 32, fast ? 0 : smem, ctx->stream>>>(demand, B, rows, row_node, luts, P,
-                                                           group_to_node, D, nodes, E, inter,
-                                                           intra, rank_pairs, ctx->d_error, fin, b0);
+    // programmatic launch: the prologue (smem zeroing, g2n staging) overlaps
+    // the previous kernel's drain; the demand is read after griddepcontrol.wait
+    MPB_CUDA(launch_pdl(kern, grid, dim3(kScoreWarps * 32), fast ? 0 : smem, ctx->stream, demand, B,
+                        rows, row_node, luts, P, group_to_node, D, nodes, E, inter, intra, rank_pairs,
+                        ctx->d_error, fin, b0));
     MPB_LAUNCHED(ctx);
     return MPB_OK;
 }

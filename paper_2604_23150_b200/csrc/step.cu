@@ -204,8 +204,17 @@ mpb_status launch_router(mpb_step *s, size_t c) {
                                     d.k, d.score_fn, d.renorm, d.idx + l0 * pairs,
                                     d.weights + l0 * pairs, nullptr);
     if (st) return st;
-    if ((st = record(s, s->ev_r1[set + c], s->s_main, true))) return st;
-    MPB_CUDA(cudaEventRecord(s->ev_done[c], s->s_main));
+    if (s->overlapped) {
+        if ((st = record(s, s->ev_r1[set + c], s->s_main, true))) return st;
+        MPB_CUDA(cudaEventRecord(s->ev_done[c], s->s_main));
+    } else {
+        // one layer: the end stamp is taken on the (idle) side stream, so no
+        // event-record node sits between the router and the layout on the main
+        // stream (which would cut their programmatic-launch overlap)
+        MPB_CUDA(cudaEventRecord(s->ev_done[c], s->s_main));
+        MPB_CUDA(cudaStreamWaitEvent(s->s_side, s->ev_done[c], 0));
+        if ((st = record(s, s->ev_r1[set + c], s->s_side, true))) return st;
+    }
     return MPB_OK;
 }
 

@@ -138,3 +138,39 @@ def test_placement_search_scores_match_oracle(monkeypatch, oracle):
     assert rep["searched"] == oracle_inter(searched.groups)
     assert rep["searched"] <= rep[rep["start"]]
     assert any(p.R_redundancy == SPEC.groups for _, p in pool)
+
+
+def test_native_schedule_matches_serial_at_dsv3_shape(monkeypatch):
+    """At the bench's own DSv3 shape (58 layers x 65,536 tokens, 1,024
+    candidates) the C++ step — grouped routers, tails and per-chunk scoring
+    beside the next routers, one CUDA graph — gives exactly the statistics,
+    LayerSims and results of the Python serial schedule (one stream, router then
+    tail per layer)."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2604_23150_b200.pipeline import spec_for
+    spec = spec_for("dsv3")
+    # the serial schedule's per-layer routers on 148 SMs would split the last
+    # wave's K range (a different fp32 order than the step's grouped launches,
+    # which fill their waves exactly): same order in both for a bitwise compare
+    monkeypatch.setenv("MPB_ROUTER_NO_SPLIT", "1")
+    outs = {}
+    for native in (True, False):
+        monkeypatch.setenv("MPB_STEP_NATIVE", "1" if native else "0")
+        monkeypatch.setenv("MPB_SIDE_STREAM", "3" if native else "0")
+        cur = torch.cuda.current_stream()
+        eng = mp.Engine(0)
+        pipe = RoutingPipeline(spec, eng, 0, 1, resident=True)
+        if native:
+            assert pipe.capture()
+        pipe.step()
+        torch.cuda.synchronize()
+        torch.cuda.set_stream(cur)
+        outs[native] = (pipe.stats.clone(), pipe.fin_cl[0].clone(), pipe.fin_rr[0].clone(),
+                        pipe.results())
+        del pipe
+        torch.cuda.empty_cache()
+    a, b = outs[True], outs[False]
+    assert torch.equal(a[0], b[0])
+    assert torch.equal(a[1], b[1]) and torch.equal(a[2], b[2])
+    assert a[3] == b[3]

@@ -200,7 +200,8 @@ mpb_status launch_router(mpb_step *s, size_t c) {
     // one layer: both stamps go on the side stream (run_layers takes the start
     // stamp there), so no event-record node sits on the main stream's router ->
     // layout chain (each costs ~3 us in a graph)
-    if (s->overlapped)
+    // consecutive routers share a stamp: the end of chunk c-1 is the start of c
+    if (s->overlapped && c == 0)
         if (mpb_status st = record(s, s->ev_r0[set + c], s->s_main, true)) return st;
     mpb_status st;
     if (l1 - l0 == 1)
@@ -498,7 +499,7 @@ mpb_status capture_graph(mpb_step *s, uint32_t phases, cudaGraphExec_t *exec, cu
 #ifdef MPB_EXP_NO_TIMING
     return MPB_OK;
 #endif
-    if (rec->size() != 2 * s->chunks.size())
+    if (rec->size() != (s->overlapped ? s->chunks.size() + 1 : 2 * s->chunks.size()))
         return fail(MPB_CUDA_ERROR, "mpb_step_capture: router timing nodes not found in the graph");
     return MPB_OK;
 }
@@ -587,7 +588,8 @@ mpb_status mpb_step_router_ms(const mpb_step *s, float *ms, uint32_t *n_runs) {
         const size_t set = (r % mpb_step::kRing) * nc;
         for (size_t c = 0; c < nc; ++c) {
             float t = 0.f;
-            MPB_CUDA(cudaEventElapsedTime(&t, s->ev_r0[set + c], s->ev_r1[set + c]));
+            const cudaEvent_t start = (s->overlapped && c > 0) ? s->ev_r1[set + c - 1] : s->ev_r0[set + c];
+            MPB_CUDA(cudaEventElapsedTime(&t, start, s->ev_r1[set + c]));
             const auto [l0, l1] = s->chunks[c];
             for (uint32_t l = l0; l < l1; ++l) ms[l] += t / static_cast<float>(l1 - l0);
         }

@@ -481,11 +481,15 @@ __device__ __forceinline__ void scatter_body(const LayoutParams &p, int32_t *sor
             // lanes holding the same slot: AND of per-bit ballots (short, independent
             // ballots pipeline better than one long-latency MATCH.ANY)
             const uint32_t key = slot == kNone ? (1u << p.key_bits) - 1u : slot;
+#ifdef MPB_EXP_MATCH  // experiment: one MATCH.ANY instead of key_bits ballots
+            const unsigned peers = __match_any_sync(0xffffffffu, key);
+#else
             unsigned peers = 0xffffffffu;
             for (uint32_t b = 0; b < p.key_bits; ++b) {
                 const unsigned m = __ballot_sync(0xffffffffu, (key >> b) & 1u);
                 peers &= ((key >> b) & 1u) ? m : ~m;
             }
+#endif
             uint32_t pos = 0;
             if (slot != kNone) pos = mine[slot] + __popc(peers & lt);
             __syncwarp();

@@ -333,7 +333,8 @@ MPB_API mpb_status mpb_combine_p2p(mpb_context *ctx, const int32_t *pair_pos,
  *     co-activation beside it on the side stream.
  *   SCORE phase: mpb_score_placements_finalize of score_jobs[0] on the main
  *     stream, the other jobs on the side stream beside it.
- * Multi-GPU callers all-reduce the statistics between the phases. Both
+ * Multi-GPU: the plan issues its own NCCL collectives (mpb_step_attach_comm),
+ * or the caller all-reduces the statistics between the two phases. Both
  * phases are asynchronous and ordered after / before the work already on
  * ctx's stream. mpb_step_capture replays them from CUDA graphs (captured
  * after one eager run that sizes every workspace). Per-chunk router times

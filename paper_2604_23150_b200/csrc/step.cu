@@ -93,8 +93,8 @@ struct mpb_step {
     static constexpr uint32_t kRing = 64;
     std::vector<cudaEvent_t> ev_r0, ev_r1;  // [kRing][chunk]
     uint64_t runs = 0, timing_from = 0;
-    // graphs: the LAYERS phase, the SCORE phase (multi-GPU: the caller's
-    // all-reduce runs between them) and both in one graph (single GPU)
+    // graphs: the LAYERS phase, the SCORE phase (a caller that all-reduces the
+    // statistics itself runs them separately) and both in one graph
     using RecNodes = std::vector<std::pair<cudaGraphNode_t, uint32_t>>;  // (node, chunk*2 + end)
     cudaGraph_t graph_layers = nullptr, graph_all = nullptr;
     RecNodes rec_layers, rec_all;

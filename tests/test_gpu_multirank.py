@@ -31,7 +31,7 @@ def test_k6_multirank_bit_identity(world):
     assert res["rank0"]["recv_rows"] > 0
 
 
-@pytest.mark.parametrize("world", [2])
+@pytest.mark.parametrize("world", [2, 4])
 def test_step_nccl_in_plan_equals_torch_collectives(world):
     """The C++ step's own NCCL collectives (inside its CUDA graph) produce the
     same statistics and LayerSim tables as torch.distributed collectives

@@ -251,3 +251,25 @@ def test_router_topk_layers_errors(eng):
     c = eng.router_topk_layers(Xs, Ws, k, 0, False)
     torch.cuda.synchronize()
     assert torch.equal(a[0], c[0]) and torch.equal(a[0][0], b[0][1]) and torch.equal(a[0][1], b[0][0])
+
+
+@pytest.mark.parametrize("sms", [148, 64, 20, 8])
+def test_cluster_tail_under_sm_budgets(oracle, sms):
+    """The decode-shape router (single-CTA tiles, split-K tail through
+    distributed shared memory) in contexts sized for fewer SMs: the unit count,
+    the K split and the resident-cluster cap all change, the top-k stays the
+    oracle's on the launch's own logits and the weights agree with it."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    T, H, E, k = 4096, 4096, 128, 8
+    g = torch.Generator(device="cuda").manual_seed(sms)
+    X = torch.randn(T, H, device="cuda", generator=g).to(torch.bfloat16)
+    W = (torch.randn(E, H, device="cuda", generator=g) / H ** 0.5).to(torch.bfloat16)
+    e = mp.Engine(0)
+    e.set_sm_budget(sms)
+    for fn in (0, 1):
+        idx, w, logits = e.router_topk(X, W, k, fn, True, want_logits=True)
+        torch.cuda.synchronize()
+        ri, rw = oracle.topk_logits(logits.cpu().numpy(), k, fn, True)
+        np.testing.assert_array_equal(idx.cpu().numpy(), ri)
+        np.testing.assert_allclose(w.cpu().numpy(), rw, rtol=2e-6, atol=1e-7)

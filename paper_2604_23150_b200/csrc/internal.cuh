@@ -124,6 +124,8 @@ mpb_status launch_layout(mpb_context *ctx, const mpb_tokens *tk, const mpb_place
                          uint64_t *demand, uint64_t *demand2, uint64_t *tag_pop,
                          int32_t *sorted_pairs, int32_t *pair_pos, int64_t *key_offsets);
 mpb_status score_finalize_range(mpb_context *ctx, const mpb_score_job &job, uint32_t b0, uint32_t nb);
+mpb_status score_finalize_pair(mpb_context *ctx, const mpb_score_job &a, const mpb_score_job &b,
+                               uint32_t b0, uint32_t nb);
 mpb_status launch_layout_derive(mpb_context *ctx, const mpb_placement *pl, const uint64_t *demand,
                                 uint64_t *expert_count, uint64_t *group_pairs,
                                 uint64_t *node_demand, uint64_t *inter_intra);

@@ -223,16 +223,24 @@ constexpr uint32_t kFastMaxD = 16;  // static smem: lane-private rank columns fo
 // candidate ahead. Rank totals pass to the finalizing lane through shared
 // memory (no global read-back). Same integer sums and the same finalize_cell:
 // bit-identical to k_score.
-__global__ void __launch_bounds__(kScoreWarps * 32) k_score16(const uint64_t *demand, uint32_t B,
-                                                              uint32_t rows,
-                                                              const uint8_t *row_node_g,
-                                                              const uint8_t *luts, uint32_t P,
-                                                              const uint8_t *g2n_g, uint32_t D,
-                                                              uint32_t nodes, uint32_t E,
-                                                              uint64_t *inter_out,
-                                                              uint64_t *intra_out,
-                                                              uint64_t *rank_out, uint32_t *err,
-                                                              FinalizeArgs fin, uint32_t b0) {
+struct Job16 {
+    const uint64_t *demand;
+    uint32_t B, rows;
+    const uint8_t *row_node_g;
+    const uint8_t *luts;
+    uint32_t P;
+    const uint8_t *g2n_g;
+    uint32_t D, nodes, E;
+    uint64_t *inter_out, *intra_out, *rank_out;
+    FinalizeArgs fin;
+};
+
+__device__ __forceinline__ void score16_body(const Job16 &J, uint32_t *err, uint32_t b0) {
+    const uint64_t *demand = J.demand;
+    const uint32_t B = J.B, rows = J.rows, P = J.P, D = J.D, nodes = J.nodes, E = J.E;
+    const uint8_t *row_node_g = J.row_node_g, *luts = J.luts, *g2n_g = J.g2n_g;
+    uint64_t *inter_out = J.inter_out, *intra_out = J.intra_out, *rank_out = J.rank_out;
+    const FinalizeArgs &fin = J.fin;
     __shared__ unsigned long long s_nd[512];
     __shared__ unsigned long long s_acc[kScoreWarps][kFastMaxD][32];
     __shared__ unsigned long long s_rank[kScoreWarps][kFastMaxD];
@@ -309,6 +317,20 @@ __global__ void __launch_bounds__(kScoreWarps * 32) k_score16(const uint64_t *de
     }
 }
 
+__global__ void __launch_bounds__(kScoreWarps * 32) k_score16(Job16 job, uint32_t *err, uint32_t b0) {
+    score16_body(job, err, b0);
+}
+
+// Two scoring jobs of the same batch range in ONE launch (blockIdx.z = job):
+// the step's candidate and baseline tables, no second stream, no fork / join.
+__global__ void __launch_bounds__(kScoreWarps * 32) k_score16x2(Job16 j0, Job16 j1, uint32_t *err,
+                                                                uint32_t b0) {
+    if (blockIdx.z == 0)
+        score16_body(j0, err, b0);
+    else
+        score16_body(j1, err, b0);
+}
+
 __global__ void k_finalize(const uint64_t *inter, const uint64_t *intra, const uint64_t *rank,
                            uint64_t N, uint32_t D, CostParams c, uint32_t tp_exp, int spans,
                            double *out, double *payload) {
@@ -380,7 +402,7 @@ mpb_status launch_score(mpb_context *ctx, const char *fn, const uint64_t *demand
     // register-resident fast path: 16 cells per lane, one 16-byte LUT load per candidate
     const bool fast = size_t(nodes) * E <= 512 && E % 16 == 0 && D <= kFastMaxD &&
                       (reinterpret_cast<uintptr_t>(luts) & 15) == 0 && !std::getenv("MPB_SCORE_SLOW");
-    auto kern = fast ? k_score16 : priv ? k_score<true> : k_score<false>;
+    auto kern = priv ? k_score<true> : k_score<false>;
     if (!fast)
         MPB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     // one CTA per batch; split candidates over grid.y until the machine is full
@@ -393,9 +415,15 @@ mpb_status launch_score(mpb_context *ctx, const char *fn, const uint64_t *demand
     dim3 grid(nb, gy);
     // programmatic launch: the prologue (smem zeroing, g2n staging) overlaps
     // the previous kernel's drain; the demand is read after griddepcontrol.wait
-    MPB_CUDA(launch_pdl(kern, grid, dim3(kScoreWarps * 32), fast ? 0 : smem, ctx->stream, demand, B,
-                        rows, row_node, luts, P, group_to_node, D, nodes, E, inter, intra, rank_pairs,
-                        ctx->d_error, fin, b0));
+    if (fast) {
+        const Job16 job{demand, B, rows, row_node, luts, P, group_to_node, D, nodes, E, inter, intra,
+                        rank_pairs, fin};
+        MPB_CUDA(launch_pdl(k_score16, grid, dim3(kScoreWarps * 32), 0, ctx->stream, job, ctx->d_error, b0));
+    } else {
+        MPB_CUDA(launch_pdl(kern, grid, dim3(kScoreWarps * 32), smem, ctx->stream, demand, B, rows,
+                            row_node, luts, P, group_to_node, D, nodes, E, inter, intra, rank_pairs,
+                            ctx->d_error, fin, b0));
+    }
     MPB_LAUNCHED(ctx);
     return MPB_OK;
 }
@@ -448,6 +476,40 @@ mpb_status mpb_finalize_layer_sims(mpb_context *ctx, const uint64_t *inter, cons
 }  // extern "C"
 
 namespace mpb {
+// Two finalized scoring jobs over the same batch range in one launch when both
+// take the register-resident path (else one launch each, in job order).
+mpb_status score_finalize_pair(mpb_context *ctx, const mpb_score_job &a, const mpb_score_job &b,
+                               uint32_t b0, uint32_t nb) {
+    auto eligible = [](const mpb_score_job &j) {
+        return size_t(j.nodes) * j.E <= 512 && j.E % 16 == 0 && j.D <= kFastMaxD && j.D >= 1 &&
+               j.rows >= 1 && j.rows <= 255 && (reinterpret_cast<uintptr_t>(j.luts) & 15) == 0 && j.out &&
+               j.demand && j.row_node && j.luts && j.group_to_node && j.inter && j.intra && j.rank_pairs;
+    };
+    if (!ctx || !eligible(a) || !eligible(b) || a.B != b.B || std::getenv("MPB_SCORE_SLOW") ||
+        b0 + nb > a.B) {
+        if (mpb_status st = score_finalize_range(ctx, a, b0, nb)) return st;
+        return score_finalize_range(ctx, b, b0, nb);
+    }
+    if (mpb_status st = check_cost(a.cost, a.tp_exp)) return st;
+    if (mpb_status st = check_cost(b.cost, b.tp_exp)) return st;
+    if (nb == 0 || (a.P == 0 && b.P == 0)) return MPB_OK;
+    auto job = [](const mpb_score_job &j) {
+        return Job16{j.demand, j.B, j.rows, j.row_node, j.luts, j.P, j.group_to_node, j.D, j.nodes, j.E,
+                     j.inter, j.intra, j.rank_pairs,
+                     FinalizeArgs{CostParams{j.cost[0], j.cost[1], j.cost[2], j.cost[3], j.cost[4], j.cost[5]},
+                                  j.tp_exp, j.spans_nodes, j.out, j.payload}};
+    };
+    const uint32_t want = 4u * static_cast<uint32_t>(ctx->num_sms);
+    const uint32_t P = std::max(a.P, b.P);
+    uint32_t gy = std::max(1u, want / std::max(1u, nb));
+    gy = std::min(gy, (P + kScoreWarps - 1) / kScoreWarps);
+    gy = std::min(gy, 65535u);
+    MPB_CUDA(launch_pdl(k_score16x2, dim3(nb, gy, 2), dim3(kScoreWarps * 32), 0, ctx->stream, job(a), job(b),
+                        ctx->d_error, b0));
+    MPB_LAUNCHED(ctx);
+    return MPB_OK;
+}
+
 // Batches [b0, b0 + nb) of an mpb_score_placements_finalize job (the step plan
 // prices each chunk of layers as soon as its statistics are in).
 mpb_status score_finalize_range(mpb_context *ctx, const mpb_score_job &j, uint32_t b0, uint32_t nb) {

@@ -279,8 +279,12 @@ mpb_status run_layers(mpb_step *s) {
             // multi-GPU: this chunk's demand becomes global before it is priced
             if ((st = reduce_stats(s, l0, l1, c + 1 == nc, tc->stream))) return st;
             if (d.score_per_chunk) {
-                for (const mpb_score_job &j : s->jobs)
-                    if (j.B == d.layers && (st = score_finalize_range(tc, j, l0, l1 - l0))) return st;
+                if (s->jobs.size() == 2 && s->jobs[0].B == d.layers && s->jobs[1].B == d.layers) {
+                    if ((st = score_finalize_pair(tc, s->jobs[0], s->jobs[1], l0, l1 - l0))) return st;
+                } else {
+                    for (const mpb_score_job &j : s->jobs)
+                        if (j.B == d.layers && (st = score_finalize_range(tc, j, l0, l1 - l0))) return st;
+                }
                 if (c + 1 == nc && (st = gather_scores(s, tc->stream))) return st;
             }
         }
@@ -320,6 +324,15 @@ mpb_status run_score(mpb_step *s) {
     if (!any) return MPB_OK;
     MPB_CUDA(cudaEventRecord(s->ev_in, s->origin));
     MPB_CUDA(cudaStreamWaitEvent(s->s_main, s->ev_in, 0));
+    if (s->jobs.size() == 2 && s->jobs[0].B == s->jobs[1].B && !score_in_layers(s, s->jobs[0]) &&
+        !score_in_layers(s, s->jobs[1])) {
+        // both tables in one launch on the main stream (no side stream, no join)
+        if (mpb_status st = score_finalize_pair(s->main, s->jobs[0], s->jobs[1], 0, s->jobs[0].B)) return st;
+        if (mpb_status st = gather_scores(s, s->s_main)) return st;
+        MPB_CUDA(cudaEventRecord(s->ev_out, s->s_main));
+        MPB_CUDA(cudaStreamWaitEvent(s->origin, s->ev_out, 0));
+        return MPB_OK;
+    }
     MPB_CUDA(cudaStreamWaitEvent(s->s_side, s->ev_in, 0));
     for (size_t j = 0; j < s->jobs.size(); ++j) {
         const mpb_score_job &b = s->jobs[j];

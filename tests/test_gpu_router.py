@@ -154,7 +154,10 @@ def test_router_split_k_parts(eng, oracle, shape, monkeypatch):
 
 @pytest.mark.parametrize("shape", [(4096, 4096, 128, 8, 0, True), (4096, 4096, 128, 1, 1, False),
                                    (2048, 1024, 64, 4, 0, False), (1000, 2048, 96, 6, 1, True),
-                                   (3000, 512, 128, 16, 0, True), (4096, 2048, 256, 8, 1, True)])
+                                   (3000, 512, 128, 16, 0, True), (4096, 2048, 256, 8, 1, True),
+                                   # 60 tiles -> 2 K parts (64-row shares, 4 threads per row)
+                                   (7680, 2048, 128, 8, 0, True), (7000, 1024, 64, 16, 1, False),
+                                   (1024, 512, 64, 16, 0, True)])
 def test_router_cluster_tail_equals_global_tail(eng, oracle, shape, monkeypatch):
     """Single-CTA tiles run the split-K tail through distributed shared memory
     (the K parts of a tile in one cluster, reduce-scatter of the partials with

@@ -94,8 +94,6 @@ mpb_status mpb_context_create(int device, void *stream, mpb_context **out) {
     ctx->device_sms = ctx->num_sms;
     cudaError_t e = cudaMalloc(&ctx->d_error, sizeof(uint32_t));
     if (e == cudaSuccess) e = cudaMemset(ctx->d_error, 0, sizeof(uint32_t));
-    if (e == cudaSuccess) e = cudaMalloc(&ctx->d_gbar, 64);
-    if (e == cudaSuccess) e = cudaMemset(ctx->d_gbar, 0, 64);
     if (e != cudaSuccess) {
         delete ctx;
         return cuda_fail(e, "mpb_context_create");
@@ -109,7 +107,6 @@ mpb_status mpb_context_destroy(mpb_context *ctx) {
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     if (ctx->d_error) cudaFree(ctx->d_error);
-    if (ctx->d_gbar) cudaFree(ctx->d_gbar);
     if (ctx->scratch) cudaFree(ctx->scratch);
     if (ctx->router_ws) cudaFree(ctx->router_ws);
     for (void *p : ctx->retired) cudaFree(p);

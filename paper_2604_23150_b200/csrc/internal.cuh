@@ -82,7 +82,6 @@ struct mpb_context {
     // SMs another context uses, so the router keeps PDL
     bool confined = false;
     uint32_t *d_error = nullptr;
-    uint32_t *d_gbar = nullptr;  // grid-barrier words of single-launch kernels (self-resetting)
     uint64_t launches = 0;
     // grow-only scratch (permutation block histograms, co-activation partials)
     void *scratch = nullptr;

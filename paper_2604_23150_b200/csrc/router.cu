@@ -274,6 +274,11 @@ __device__ __forceinline__ void cluster_tail(const RouterParams &p, const WorkIt
 #ifdef MPB_ROUTER_TRACE
     if (t == 0) RTRACE(5, gtime());
 #endif
+#ifdef MPB_EXP_NOSEL  // experiment: timing without the selection (wrong output)
+    if (t < RPS && row_tile0 + h * RPS + t < p.T)
+        p.idx[(out_row_tile0 + h * RPS + t) * p.k] = static_cast<int>(tile[t * RS]);
+    return;
+#endif
     // ---- top-k of the RPS owned rows from shared memory, TPR threads per row
     const uint32_t TPR = 256u / RPS;          // 8 (S = 4) or 4 (S = 2)
     const uint32_t r = t / TPR, sub = t % TPR;

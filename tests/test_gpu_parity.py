@@ -182,7 +182,9 @@ LAYOUT_CASES = [  # T, E, D, nodes, k, redundancy, block_src
     (4096, 128, 8, 2, 8, 0, False), (5000, 256, 8, 4, 8, 2, True), (70000, 128, 8, 8, 1, 0, False),
     (65536, 256, 8, 2, 8, 0, True), (3333, 64, 16, 4, 6, 3, False),
     # > 4 groups of 128 pairs per warp: slot ids recomputed in the rank pass
-    (1048576, 128, 8, 2, 8, 0, False)]
+    (1048576, 128, 8, 2, 8, 0, False),
+    # single-cluster layout limits: 16 CTAs x 4 groups exactly, and one pair more
+    (16384, 128, 8, 2, 8, 0, False), (16385, 64, 8, 2, 8, 1, True)]
 
 
 @pytest.mark.parametrize("case", LAYOUT_CASES)
@@ -447,11 +449,15 @@ def test_score_and_finalize_fused_equals_two_launches(oracle, spans):
     assert torch.equal(f1, f2) and torch.equal(p1, p2)
 
 
-def test_fused_small_batch_layout_matches_oracle(tmp_path):
-    """MPB_LAYOUT_FUSE=1 (read once per process, so in a child): small batches
-    run count, scan and scatter as ONE launch with two grid barriers; the
-    histograms and the stable permutation equal the oracle's, twice in a row
-    (the barrier words reset themselves)."""
+def test_cluster_layout_equals_three_kernel_layout():
+    """The single-cluster layout (decode-size batches: one launch, DSMEM
+    exchanges) and the clustered count kernel (tables summed over DSMEM) against
+    the plain count / scan / scatter kernels (MPB_LAYOUT_CLUSTER=0 and
+    MPB_LAYOUT_COUNT_CLUSTER=0, in a child: read once per process): identical
+    demand, second-routing
+    demand, tag histograms, permutation, offsets and error words — every group
+    count and cluster size, odd k, a misaligned idx view, block sources, and
+    uncovered / out-of-range experts."""
     import os
     import subprocess
     import sys
@@ -462,32 +468,57 @@ def test_fused_small_batch_layout_matches_oracle(tmp_path):
     code = r'''
 import sys; sys.path.insert(0, %r)
 import numpy as np, torch
-from oracle.pyoracle import Oracle
 from paper_2604_23150_b200 import moeplace as mp
-O = Oracle(); eng = mp.Engine(0)
-for T, E, k, D, red in ((4096, 128, 8, 8, 0), (1000, 256, 8, 8, 3), (37, 64, 4, 4, 0)):
-    rng = np.random.default_rng(T)
+from paper_2604_23150_b200.errors import Error as MoeplaceError
+eng = mp.Engine(0)
+out = []
+cases = [(1, 16, 2, 2, 0, 0), (37, 64, 4, 3, 0, 0), (4096, 128, 8, 8, 0, 0), (4097, 128, 8, 8, 0, 1),
+         (5000, 256, 8, 8, 2, 0), (16384, 128, 8, 8, 0, 0), (20000, 64, 16, 6, 3, 1),
+         (70000, 128, 8, 1, 0, 0), (40000, 256, 8, 8, 1, 0), (33333, 64, 4, 8, 0, 1),
+         (2048, 128, 8, 8, 0, 2), (3000, 128, 8, 8, 0, 3), (50000, 128, 8, 8, 0, 2)]
+for T, E, D, k, red, mode in cases:
+    rng = np.random.default_rng(T * 31 + E)
     idx = np.argsort(rng.random((T, E)), axis=1)[:, :k].astype(np.int32)
     groups = [list(range(d * E // D, (d + 1) * E // D)) for d in range(D)]
     for g in groups:
         g += [e for e in rng.permutation(E).tolist() if e not in g][:red]
-    pl = mp.Placement(groups, E, red * D, len(groups[0]))
+    if mode == 2:  # expert 0 held by nobody
+        groups = [[e for e in g if e != 0] + ([1] if 0 in g else []) for g in groups]
+    pl = mp.Placement(groups, E, sum(len(g) for g in groups) - E, max(len(g) for g in groups))
     top = mp.Topology.contiguous(D, 1, D, 1, 2)
-    src = rng.integers(0, D, T).astype(np.uint8)
     dp = eng.placement(pl, top)
-    lut = O.dest_lut(pl.groups, top.group_to_node, E)
-    ref = O.dispatch_layout(idx, src.astype(np.uint32), lut, D, E, top.group_to_node)
-    for _ in range(2):
-        lay = eng.dispatch_layout(torch.from_numpy(idx).cuda(), dp, src=torch.from_numpy(src).cuda())
+    flat = np.zeros(T * k + 1, np.int32)
+    flat[1:] = idx.reshape(-1)
+    if mode == 3:
+        flat[5] = E + 3  # out-of-range expert
+    x = torch.from_numpy(flat).cuda()
+    idx_d = x[1:].view(T, k) if mode == 1 else x[1:].clone().view(T, k)  # mode 1: misaligned
+    src = torch.from_numpy(rng.integers(0, D, T).astype(np.uint8)).cuda()
+    src2 = torch.from_numpy(rng.integers(0, D, T).astype(np.uint8)).cuda()
+    tag = torch.from_numpy(rng.integers(0, 7, T).astype(np.uint16)).cuda()
+    kw = dict(src_base=0, src_span=D) if T %% 2 else dict(src=src)
+    err = None
+    try:
+        lay = eng.dispatch_layout(idx_d, dp, tag=tag, n_tags=6, src2=src2, **kw)
         eng.sync()
-        assert np.array_equal(lay["sorted_pairs"].cpu().numpy(), ref["sorted_pairs"])
-        assert np.array_equal(lay["demand"].cpu().numpy().reshape(-1), ref["demand"].reshape(-1))
-print("fused ok")
+    except MoeplaceError as e:
+        err = type(e).__name__
+        lay = None
+    out.append((T, err, None if lay is None else [lay[n].cpu().numpy().tolist() for n in
+               ("demand", "demand2", "tag_pop", "sorted_pairs", "pair_pos", "key_offsets")]))
+import json; print("RESULT" + json.dumps(out))
 ''' % str(root)
-    env = dict(os.environ, MPB_LAYOUT_FUSE="1")
-    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
-                       timeout=300)
-    assert r.returncode == 0 and "fused ok" in r.stdout, r.stdout + r.stderr
+    res = []
+    for flag in ("1", "0"):  # "0": neither cluster path (decode kernel, count-table sums)
+        env = dict(os.environ, MPB_LAYOUT_CLUSTER=flag, MPB_LAYOUT_COUNT_CLUSTER=flag)
+        r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
+                           timeout=600)
+        assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
+        res.append(next(ln for ln in r.stdout.splitlines() if ln.startswith("RESULT")))
+    assert res[0] == res[1]
+    import json
+    got = json.loads(res[0][6:])
+    assert [e for _, e, _ in got][-3:] == ["ValidationError"] * 3
 
 
 @pytest.mark.parametrize("P,B,nodes,D,E", [(1022, 58, 2, 8, 256), (254, 1, 2, 8, 128),

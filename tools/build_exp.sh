@@ -4,7 +4,7 @@
 set -e
 NAME=$1; shift
 cd "$(dirname "$0")/.."
-O=exp_libs/$NAME; mkdir -p $O
+O=/tmp/exp_objs/$NAME; mkdir -p $O
 for f in paper_2604_23150_b200/csrc/*.cu; do
   /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 \
     -Xcompiler -fPIC,-fvisibility=hidden --expt-relaxed-constexpr -Iinclude \

@@ -169,6 +169,175 @@ __device__ __forceinline__ bool ranks_before(float v, int id, float w, int jd) {
     return v > w || (v == w && id < jd);
 }
 
+// Order-preserving u32 key of a logit for the top-k: larger key ranks first.
+// Real values (+-inf included) descend, -0 == +0 (a tie), NaN (key 1) ranks
+// after every real value; 0 is reserved for padding / taken columns. Equal keys
+// are broken by the lower expert id: exactly the oracle's beats()
+// (oracle/moeplace_oracle.c, the reference's lowest-index tie rule,
+// placement.cpp:143-152).
+__device__ __forceinline__ uint32_t rank_key(float v) {
+    if (v != v) return 1u;
+    uint32_t b = __float_as_uint(v);
+    if (b == 0x80000000u) b = 0u;
+    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);  // -inf -> 0x007FFFFF
+}
+__device__ __forceinline__ float key_value(uint32_t key) {
+    return key == 1u ? __uint_as_float(0x7FC00000u)
+                     : __uint_as_float((key & 0x80000000u) ? (key & 0x7FFFFFFFu) : ~key);
+}
+
+// Compare-exchange of (key, slot) pairs into descending key order (equal keys:
+// the lower slot first, i.e. the lower expert id of the lane's columns).
+__device__ __forceinline__ void cx_desc(uint32_t &ka, uint32_t &sa, uint32_t &kb, uint32_t &sb) {
+    const bool sw = kb > ka || (kb == ka && sb < sa);
+    const uint32_t k0 = sw ? kb : ka, k1 = sw ? ka : kb, s0 = sw ? sb : sa, s1 = sw ? sa : sb;
+    ka = k0;
+    kb = k1;
+    sa = s0;
+    sb = s1;
+}
+
+// Sum and top-k of a cluster-tail row share (RPS = 8R rows) from shared memory.
+// Warp ew (of the 8 epilogue warps) owns rows ew, ew+8, ...; lane l holds
+// columns l, l+32, ... of each (conflict-free LDS; the K parts summed in part
+// order 0..S-1: the global tail's fp32 order, bit-identical logits). Each lane
+// sorts its V rank keys once (a 1- or 5-exchange network); the row's top-k is
+// then k rounds of: redux.sync max over the 32 lane heads, a ballot of the
+// lanes holding it (several only on an exact tie: the lowest column id wins,
+// warp-uniform slow path), the winning lane pops its head. The R rows are
+// interleaved so one row's reductions hide the others' latency; no branches
+// outside the tie path, no dynamic register indexing. Lane j ends with slot j.
+// Weights: softmax shifts by the row max (the first round's winner); with
+// renormalisation the softmax denominator cancels and is never formed.
+// Micro-benchmark (tools/micro/sel_bench.cu, 32 rows x 128 logits, top-8):
+// 5.2K SM cycles against 8.6K for the per-thread insertion + shuffle merge.
+template <int N, int KMAX, int R>
+__device__ __forceinline__ void tail_select(const RouterParams &p, const float *rx, const float *tile,
+                                            uint32_t h, uint32_t ew, uint32_t lane,
+                                            uint64_t row_tile0, uint64_t out_row_tile0) {
+    constexpr uint32_t RS = N + 4, V = N / 32;
+    static_assert(V == 2 || V == 4, "cluster tail: N = 64 or 128");
+    constexpr uint32_t RPS = 8u * R, SP = 128u / RPS;  // SP = S: 4 K parts (R = 4) or 2 (R = 8)
+    constexpr float kL2E = 1.4426950408889634f;
+    uint32_t key[R][V], perm[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const uint32_t rr = ew + 8u * r;
+        float x[V];
+#pragma unroll
+        for (int i = 0; i < static_cast<int>(V); ++i) {
+            const uint32_t c = lane + 32u * i;
+            float tot = 0.f;
+#pragma unroll
+            for (uint32_t part = 0; part < SP; ++part) {
+                const uint32_t j = part < h ? part : part - 1;
+                const float v = part == h ? tile[rr * RS + c] : rx[(j * RPS + rr) * RS + c];
+                tot = part == 0 ? v : tot + v;
+            }
+            x[i] = tot;
+        }
+        if (p.logits && row_tile0 + h * RPS + rr < p.T) {
+            float *out = p.logits + (out_row_tile0 + h * RPS + rr) * p.E;
+#pragma unroll
+            for (int i = 0; i < static_cast<int>(V); ++i)
+                if (lane + 32u * i < p.E) out[lane + 32u * i] = x[i];
+        }
+        uint32_t sl[V];
+#pragma unroll
+        for (int i = 0; i < static_cast<int>(V); ++i) {
+            key[r][i] = lane + 32u * i < p.E ? rank_key(x[i]) : 0u;  // padding: 0, never selected
+            sl[i] = i;
+        }
+        cx_desc(key[r][0], sl[0], key[r][1], sl[1]);
+        if constexpr (V == 4) {
+            cx_desc(key[r][2], sl[2], key[r][3], sl[3]);
+            cx_desc(key[r][0], sl[0], key[r][2], sl[2]);
+            cx_desc(key[r][1], sl[1], key[r][3], sl[3]);
+            cx_desc(key[r][1], sl[1], key[r][2], sl[2]);
+        }
+        perm[r] = 0;
+#pragma unroll
+        for (int i = 0; i < static_cast<int>(V); ++i) perm[r] |= sl[i] << (2 * i);
+    }
+#ifdef MPB_ROUTER_TRACE
+    if (ew == 0 && lane == 0) RTRACE(5, gtime());
+#endif
+    const uint32_t k = p.k;
+    const bool softmax = p.score_fn == MPB_SCORE_SOFTMAX;
+    uint32_t skey[R], sid[R], mkey[R];
+    float spart[R];  // the lane's share of the softmax denominator (formed only without renormalisation)
+#pragma unroll
+    for (int j = 0; j < KMAX; ++j) {
+        if (static_cast<uint32_t>(j) >= k) break;
+        uint32_t km[R], b[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) km[r] = __reduce_max_sync(0xffffffffu, key[r][0]);
+        if (j == 0) {
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                mkey[r] = km[r];
+                spart[r] = 0.f;
+                if (softmax && !p.renorm) {  // every column still at its place: sum them now
+                    const float mlog = (km[r] <= 1u ? -INFINITY : key_value(km[r])) * kL2E;
+#pragma unroll
+                    for (int i = 0; i < static_cast<int>(V); ++i)
+                        spart[r] += key[r][i] > 1u ? exp2f(fmaf(key_value(key[r][i]), kL2E, -mlog)) : 0.f;
+                }
+            }
+        }
+        bool tie = false;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            b[r] = __ballot_sync(0xffffffffu, key[r][0] == km[r]);
+            tie |= __popc(b[r]) != 1;
+        }
+        if (tie) {  // equal keys at several lane heads: the lowest column id (slot, then lane)
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const bool at = key[r][0] == km[r];
+                const uint32_t ms = __reduce_min_sync(0xffffffffu, at ? (perm[r] & 3u) : 0xffu);
+                b[r] = __ballot_sync(0xffffffffu, at && (perm[r] & 3u) == ms);
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const uint32_t wl = __ffs(b[r]) - 1;
+            const uint32_t id = __shfl_sync(0xffffffffu, lane + 32u * (perm[r] & 3u), wl);
+            skey[r] = lane == static_cast<uint32_t>(j) ? km[r] : skey[r];
+            sid[r] = lane == static_cast<uint32_t>(j) ? id : sid[r];
+            const bool pop = lane == wl;
+#pragma unroll
+            for (int i = 0; i + 1 < static_cast<int>(V); ++i) key[r][i] = pop ? key[r][i + 1] : key[r][i];
+            key[r][V - 1] = pop ? 0u : key[r][V - 1];
+            perm[r] = pop ? perm[r] >> 2 : perm[r];
+        }
+    }
+    float e[R], tsum[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const float mlog = (mkey[r] <= 1u ? -INFINITY : key_value(mkey[r])) * kL2E;
+        const float v = key_value(skey[r]);
+        e[r] = lane < k && !isnan(v) ? (softmax ? exp2f(fmaf(v, kL2E, -mlog)) : 1.f / (1.f + expf(-v))) : 0.f;
+        tsum[r] = e[r];
+    }
+#pragma unroll
+    for (uint32_t o = 16; o >= 1; o >>= 1)
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            tsum[r] += __shfl_xor_sync(0xffffffffu, tsum[r], o);
+            spart[r] += __shfl_xor_sync(0xffffffffu, spart[r], o);
+        }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const uint32_t rr = ew + 8u * r;
+        if (lane < k && row_tile0 + h * RPS + rr < p.T) {
+            const uint64_t o = (out_row_tile0 + h * RPS + rr) * p.k + lane;
+            p.idx[o] = static_cast<int32_t>(sid[r]);
+            p.w[o] = p.renorm ? (tsum[r] > 0.f ? e[r] / tsum[r] : 0.f) : softmax ? e[r] / spart[r] : e[r];
+        }
+    }
+}
+
 // Split-K tail through distributed shared memory (single-CTA tiles, PAIR off).
 // The S = p.splits K-part units of a tail tile are one cluster; CTA h (K part
 // h, cluster rank h) ends with rows [h*RPS, (h+1)*RPS) of the tile (RPS =
@@ -178,13 +347,9 @@ __device__ __forceinline__ bool ranks_before(float v, int id, float w, int jd) {
 //   2. each epilogue warp pushes the TMEM rows it does not own into the
 //      owner's shared memory with st.async (completion counted in bytes on the
 //      owner's mbarrier) — no global memory, no flags, no fences;
-//   3. the owner sums its rows in K-part order 0..S-1 (the fp32 order of the
-//      global-memory tail) into a shared-memory tile;
-//   4. all 8 epilogue warps select top-k for the RPS rows from shared memory:
-//      TPR = 256/RPS threads per row, each a column slice; a lower bound t0 on
-//      the k-th logit (minimum of >= KMAX group maxima) filters the insertions;
-//      the TPR partial lists merge over warp shuffles (top half of A u rev(B),
-//      then a bitonic clean-up: static register indices only).
+//   3.+4. one warp per owned row sums it in K-part order 0..S-1 (the fp32
+//      order of the global-memory tail) in registers and selects its top-k by
+//      k warp arg-max rounds (tail_select).
 // The whole 128-row epilogue of a decode batch's tiles is thus spread over the S
 // CTAs and over 8 warps per row group instead of 2.
 template <int N, int KMAX>
@@ -192,6 +357,9 @@ __device__ __forceinline__ void cluster_tail(const RouterParams &p, const WorkIt
                                              uint32_t taddr_q, uint8_t *stage_base,
                                              uint64_t *peer_free, uint64_t *rx_full, uint32_t warp,
                                              uint32_t lane, uint64_t row_tile0, uint64_t out_row_tile0) {
+    if constexpr (N > 128) {  // the host runs the cluster tail only for N <= 128
+        return;
+    } else {
     const uint32_t S = p.splits, h = it.part;
     const uint32_t RPS = 128u / S;
     constexpr uint32_t RS = N + 4;  // padded row stride (floats): conflict-free 16-byte stores
@@ -214,17 +382,15 @@ __device__ __forceinline__ void cluster_tail(const RouterParams &p, const WorkIt
         const uint32_t i = owner < h ? owner : owner - 1;
         float *dst = owner == h ? tile + static_cast<size_t>(rloc) * RS
                                 : snd + (static_cast<size_t>(i) * RPS + rloc) * RS;
-#pragma unroll 1
-        for (int c = half * NH; c < (half + 1) * NH; c += 16) {
-            uint32_t r[16];
-            ptx::tmem_ld_32x32b_x16(taddr_q + c, r);
-            ptx::tmem_ld_wait();
+        uint32_t r[NH];  // the thread's half row: every TMEM load in flight before one wait
 #pragma unroll
-            for (int j = 0; j < 4; ++j)
-                *reinterpret_cast<float4 *>(dst + c + 4 * j) =
-                    make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
-                                __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
-        }
+        for (int c = 0; c < NH; c += 16) ptx::tmem_ld_32x32b_x16(taddr_q + half * NH + c, *reinterpret_cast<uint32_t(*)[16]>(r + c));
+        ptx::tmem_ld_wait();
+#pragma unroll
+        for (int c = 0; c < NH; c += 4)
+            *reinterpret_cast<float4 *>(dst + half * NH + c) =
+                make_float4(__uint_as_float(r[c]), __uint_as_float(r[c + 1]), __uint_as_float(r[c + 2]),
+                            __uint_as_float(r[c + 3]));
         if (owner != h) ptx::fence_proxy_async_smem();  // generic writes -> visible to the bulk-copy engine
     }
     asm volatile("bar.sync 5, 256;" ::: "memory");  // every share staged
@@ -246,225 +412,15 @@ __device__ __forceinline__ void cluster_tail(const RouterParams &p, const WorkIt
 #ifdef MPB_ROUTER_TRACE
     if (t == 0) RTRACE(15, gtime());
 #endif
-    // every epilogue thread sums RPS*N/256 values of the share in K-part order
-    // 0..S-1 (a fixed fp32 order: the global-memory tail's), in place in the tile
-    for (uint32_t e4 = t; e4 < RPS * (N / 4); e4 += 256) {
-        const uint32_t rr = e4 / (N / 4), cc = (e4 % (N / 4)) * 4;
-        float4 *own = reinterpret_cast<float4 *>(tile + static_cast<size_t>(rr) * RS + cc);
-        float4 v[4];
-#pragma unroll
-        for (uint32_t part = 0; part < 4; ++part)
-            if (part < S) {
-                const uint32_t i = part < h ? part : part - 1;
-                v[part] = part == h ? *own
-                                    : *reinterpret_cast<const float4 *>(rx + (static_cast<size_t>(i) * RPS + rr) * RS + cc);
-            }
-        float4 tot = v[0];
-#pragma unroll
-        for (uint32_t part = 1; part < 4; ++part)
-            if (part < S) {
-                tot.x += v[part].x;
-                tot.y += v[part].y;
-                tot.z += v[part].z;
-                tot.w += v[part].w;
-            }
-        *own = tot;
-    }
-    asm volatile("bar.sync 5, 256;" ::: "memory");  // the owned rows are summed
-#ifdef MPB_ROUTER_TRACE
-    if (t == 0) RTRACE(5, gtime());
-#endif
-#ifdef MPB_EXP_NOSEL  // experiment: timing without the selection (wrong output)
-    if (t < RPS && row_tile0 + h * RPS + t < p.T)
-        p.idx[(out_row_tile0 + h * RPS + t) * p.k] = static_cast<int>(tile[t * RS]);
-    return;
-#endif
-    // ---- top-k of the RPS owned rows from shared memory, TPR threads per row
-    const uint32_t TPR = 256u / RPS;          // 8 (S = 4) or 4 (S = 2)
-    const uint32_t r = t / TPR, sub = t % TPR;
-    const uint32_t CW = N / TPR;              // columns per thread (multiple of 8)
-    const float *row = tile + static_cast<size_t>(r) * RS;
-    const uint64_t token = row_tile0 + h * RPS + r;
-    const uint64_t out_row = out_row_tile0 + h * RPS + r;
-    const uint32_t c0 = sub * CW;
-    // pass 1: max and the k-th-logit lower bound t0 (groups: >= KMAX over the row)
-    const uint32_t G = KMAX > static_cast<int>(TPR) ? KMAX / TPR : 1u;  // groups per thread
-    const uint32_t GSZ = CW / G;
-    float m = -INFINITY, t0 = INFINITY;
-    for (uint32_t g = 0; g < G; ++g) {
-        float gm = -INFINITY;
-        for (uint32_t c = c0 + g * GSZ; c < c0 + (g + 1) * GSZ; c += 4) {
-            const float4 v = *reinterpret_cast<const float4 *>(row + c);
-            if (c < p.E) gm = fmaxf(gm, v.x);
-            if (c + 1 < p.E) gm = fmaxf(gm, v.y);
-            if (c + 2 < p.E) gm = fmaxf(gm, v.z);
-            if (c + 3 < p.E) gm = fmaxf(gm, v.w);
-        }
-        t0 = fminf(t0, gm);
-        m = fmaxf(m, gm);
-    }
-    for (uint32_t o = 1; o < TPR; o <<= 1) {
-        t0 = fminf(t0, __shfl_xor_sync(0xffffffffu, t0, o));
-        m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-    }
-    if (KMAX == 1) t0 = m;
-    // pass 2: local top-KMAX of the slice (ascending ids: equal logits keep the lower id)
-#ifdef MPB_ROUTER_TRACE
-    if (t == 0) RTRACE(10, gtime());
-#endif
-    float tv[KMAX];
-    int ti[KMAX];
-#pragma unroll
-    for (int j = 0; j < KMAX; ++j) {
-        tv[j] = -INFINITY;
-        ti[j] = 0x7FFFFFFF;
-    }
-    for (uint32_t c = c0; c < c0 + CW; c += 8) {
-        uint32_t rr[16];
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-            const float4 v = *reinterpret_cast<const float4 *>(row + c + 4 * j);
-            rr[4 * j] = __float_as_uint(v.x);
-            rr[4 * j + 1] = __float_as_uint(v.y);
-            rr[4 * j + 2] = __float_as_uint(v.z);
-            rr[4 * j + 3] = __float_as_uint(v.w);
-        }
-#pragma unroll
-        for (int j = 8; j < 16; ++j) rr[j] = __float_as_uint(-INFINITY);
-        uint32_t hit = 0;
-        const float thr = fmaxf(tv[KMAX - 1], t0);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const float v = __uint_as_float(rr[i]);
-            const bool real = c + i < p.E;
-            hit |= static_cast<uint32_t>(real && (v > thr || (v == t0 && v > tv[KMAX - 1]))) << i;
-        }
-        while (hit) {
-            const int i = __ffs(hit) - 1;
-            hit &= hit - 1;
-            const float v = pick16(rr, i);
-            const int e = static_cast<int>(c) + i;
-#pragma unroll
-            for (int j = KMAX - 1; j >= 0; --j) {
-                const bool here = v > tv[j];
-                const bool above = j > 0 && v > tv[j > 0 ? j - 1 : 0];
-                tv[j] = above ? tv[j > 0 ? j - 1 : 0] : (here ? v : tv[j]);
-                ti[j] = above ? ti[j > 0 ? j - 1 : 0] : (here ? e : ti[j]);
-            }
-        }
-    }
-    // merge the TPR sorted lists: top-KMAX of A u B = pairwise best of A[j], B[K-1-j]
-    // (a bitonic sequence), sorted by half-cleaners
-#ifdef MPB_ROUTER_TRACE
-    if (t == 0) RTRACE(11, gtime());
-#endif
-    for (uint32_t o = 1; o < TPR; o <<= 1) {
-        float bv[KMAX];
-        int bi[KMAX];
-#pragma unroll
-        for (int j = 0; j < KMAX; ++j) {
-            bv[j] = __shfl_xor_sync(0xffffffffu, tv[j], o);
-            bi[j] = __shfl_xor_sync(0xffffffffu, ti[j], o);
-        }
-#pragma unroll
-        for (int j = 0; j < KMAX; ++j) {
-            const bool a = ranks_before(tv[j], ti[j], bv[KMAX - 1 - j], bi[KMAX - 1 - j]);
-            tv[j] = a ? tv[j] : bv[KMAX - 1 - j];
-            ti[j] = a ? ti[j] : bi[KMAX - 1 - j];
-        }
-#pragma unroll
-        for (int d = KMAX / 2; d >= 1; d >>= 1)
-#pragma unroll
-            for (int j = 0; j < KMAX; ++j)
-                if ((j & d) == 0) {
-                    const bool a = ranks_before(tv[j], ti[j], tv[j + d], ti[j + d]);
-                    const float xv = a ? tv[j] : tv[j + d], yv = a ? tv[j + d] : tv[j];
-                    const int xi = a ? ti[j] : ti[j + d], yi = a ? ti[j + d] : ti[j];
-                    tv[j] = xv;
-                    tv[j + d] = yv;
-                    ti[j] = xi;
-                    ti[j + d] = yi;
-                }
-    }
-    // softmax denominator over the row (shuffle tree over the TPR slices)
-#ifdef MPB_ROUTER_TRACE
-    if (t == 0) RTRACE(12, gtime());
-#endif
-    float ssum = 0.f;
-    if (p.score_fn == MPB_SCORE_SOFTMAX) {
-        const float mlog = m * 1.4426950408889634f;
-        for (uint32_t c = c0; c < c0 + CW; ++c) {
-            const float v = row[c];
-            ssum += (c < p.E && v == v) ? exp2f(fmaf(v, 1.4426950408889634f, -mlog)) : 0.f;
-        }
-        for (uint32_t o = 1; o < TPR; o <<= 1) ssum += __shfl_xor_sync(0xffffffffu, ssum, o);
-    }
-    if (p.logits && token < p.T)
-        for (uint32_t c = c0; c < c0 + CW && c < p.E; ++c) p.logits[out_row * p.E + c] = row[c];
-#ifdef MPB_ROUTER_TRACE
-    if (t == 0) RTRACE(13, gtime());
-#endif
-    // every lane of a row holds the same merged list: lane `sub` writes output
-    // slots sub, sub + TPR, ... (the renormalising sum over the row's lanes)
-    const int k = static_cast<int>(p.k);
-    int last = ti[0];  // ti[k - 1] without a dynamic register index (local memory)
-#pragma unroll
-    for (int j = 1; j < KMAX; ++j)
-        if (j == k - 1) last = ti[j];
-    if (last == 0x7FFFFFFF) {
-        // fewer than k logits above -inf: fill with -inf ids, then NaN ids, ascending
-        for (int pass = 0; pass < 2; ++pass)
-            for (uint32_t c = 0; c < p.E; ++c) {
-                const float v = row[c];
-                const bool want = pass == 0 ? v == -INFINITY : v != v;
-                if (!want) continue;
-                bool placed = false;
-#pragma unroll
-                for (int j = 0; j < KMAX; ++j)
-                    if (!placed && j < k && ti[j] == 0x7FFFFFFF) {
-                        ti[j] = static_cast<int>(c);
-                        tv[j] = v;
-                        placed = true;
-                    }
-            }
-    }
-    const float mlog = m * 1.4426950408889634f;
-    auto weight = [&](float v) {
-        if (isnan(v)) return 0.f;
-        return p.score_fn == MPB_SCORE_SOFTMAX ? exp2f(fmaf(v, 1.4426950408889634f, -mlog)) / ssum
-                                               : 1.f / (1.f + expf(-v));
-    };
-    auto slot = [&](int j, float &v, int &id) {  // tv[j], ti[j] with static indices
-        v = tv[0];
-        id = ti[0];
-#pragma unroll
-        for (int jj = 1; jj < KMAX; ++jj)
-            if (jj == j) {
-                v = tv[jj];
-                id = ti[jj];
-            }
-    };
-    float wpart = 0.f;
-    for (int j = static_cast<int>(sub); j < k; j += static_cast<int>(TPR)) {
-        float v;
-        int id;
-        slot(j, v, id);
-        wpart += weight(v);
-    }
-    float wsum = wpart;
-    for (uint32_t o = 1; o < TPR; o <<= 1) wsum += __shfl_xor_sync(0xffffffffu, wsum, o);
-    if (token < p.T)
-        for (int j = static_cast<int>(sub); j < k; j += static_cast<int>(TPR)) {
-            float v;
-            int id;
-            slot(j, v, id);
-            const float x = weight(v);
-            p.idx[out_row * p.k + j] = id;
-            p.w[out_row * p.k + j] = p.renorm ? (wsum > 0.f ? x / wsum : 0.f) : x;
-        }
+    // sum + top-k of the RPS owned rows (tail_select): one warp per row
+    if (S == 4)
+        tail_select<N, KMAX, 4>(p, rx, tile, h, warp - 4u, lane, row_tile0, out_row_tile0);
+    else
+        tail_select<N, KMAX, 8>(p, rx, tile, h, warp - 4u, lane, row_tile0, out_row_tile0);
 #ifdef MPB_ROUTER_TRACE
     if (t == 0) RTRACE(6, gtime());
 #endif
+    }
 }
 
 // Hands an accumulator's TMEM back to the MMA issuer after this thread's
@@ -972,9 +928,11 @@ __global__ void __launch_bounds__(kThreadsR, 1)
                     ssum = ssum * a0 + s1 * a1;
                 }
                 m = mm;
-                if (ti[KMAX - 1] == 0x7FFFFFFF) {
+                const bool short_row = ti[KMAX - 1] == 0x7FFFFFFF;
+                if (__any_sync(0xffffffffu, short_row)) {
                     // rare: fewer than k logits above -inf — fill with -inf ids, then
-                    // NaN ids, ascending (NaN ranks lowest)
+                    // NaN ids, ascending (NaN ranks lowest). tcgen05.ld is warp-collective:
+                    // the whole warp loads, only the short rows place
 #pragma unroll 1
                     for (int pass = 0; pass < 2; ++pass)
 #pragma unroll 1
@@ -986,7 +944,7 @@ __global__ void __launch_bounds__(kThreadsR, 1)
                             for (int i = 0; i < 16; ++i) {
                                 const float v = __uint_as_float(r[i]);
                                 const bool want = pass == 0 ? v == -INFINITY : v != v;
-                                if (!want || static_cast<uint32_t>(c + i) >= p.E) continue;
+                                if (!short_row || !want || static_cast<uint32_t>(c + i) >= p.E) continue;
                                 bool placed = false;
 #pragma unroll
                                 for (int j = 0; j < KMAX; ++j)

@@ -276,3 +276,41 @@ def test_cluster_tail_under_sm_budgets(oracle, sms):
         ri, rw = oracle.topk_logits(logits.cpu().numpy(), k, fn, True)
         np.testing.assert_array_equal(idx.cpu().numpy(), ri)
         np.testing.assert_allclose(w.cpu().numpy(), rw, rtol=2e-6, atol=1e-7)
+
+
+@pytest.mark.parametrize("tail", ["cluster", "global", "none"])
+@pytest.mark.parametrize("shape", [(4096, 1024, 128, 8, 0), (4096, 1024, 128, 16, 1), (2048, 512, 64, 16, 0)])
+def test_router_ties_inf_nan(eng, oracle, shape, tail, monkeypatch):
+    """Non-finite and tied logits follow the oracle's order on every epilogue
+    (cluster tail, global split tail, no split): real values (+-inf included)
+    descend, equal logits keep the lower expert id (duplicated W rows give
+    bit-equal columns), -0 ties +0, -inf fills before NaN, NaN last in id
+    order. Rows with X[t, 0] = +-inf make +-inf / NaN logits through W[:, 0]."""
+    T, H, E, k, fn = shape
+    g = torch.Generator(device="cuda").manual_seed(T + E + k)
+    X = torch.randn(T, H, device="cuda", generator=g)
+    W = torch.randn(E, H, device="cuda", generator=g) / H ** 0.5
+    W[:, 0] = W[:, 0].abs() + 0.01
+    W[2, 0] = W[E - 14, 0] = -0.5       # X = -inf rows: +inf here, -inf elsewhere
+    W[5, 0] = W[9, 0] = W[E - 51, 0] = 0.0  # inf * 0 -> NaN
+    W[E // 2:E // 2 + 8, 0] = 0.0         # a NaN-heavy block
+    W[7] = W[3]                           # exact ties on normal rows
+    W[E - 1] = W[3]
+    W[E - 20, 1:] = W[11, 1:]
+    X[1::7, 0] = float("inf")
+    X[3::7, 0] = -float("inf")
+    X[5::7, 0] = 0.0
+    X[5::7, 1:] = 0.0                     # an all-zero row: every logit +-0, all ties
+    X, W = X.to(torch.bfloat16), W.to(torch.bfloat16)
+    if tail == "global":
+        monkeypatch.setenv("MPB_ROUTER_GLOBAL_TAIL", "1")
+    elif tail == "none":
+        monkeypatch.setenv("MPB_ROUTER_NO_SPLIT", "1")
+    idx, w, logits = eng.router_topk(X, W, k, fn, True, want_logits=True)
+    torch.cuda.synchronize()
+    L = logits.cpu().numpy()
+    assert np.isnan(L).any() and np.isinf(L).any()
+    ri, rw = oracle.topk_logits(L, k, fn, True)
+    np.testing.assert_array_equal(idx.cpu().numpy(), ri)
+    fin = np.isfinite(L).all(1)
+    np.testing.assert_allclose(w.cpu().numpy()[fin], rw[fin], rtol=2e-6, atol=1e-7)

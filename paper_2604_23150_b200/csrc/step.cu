@@ -9,8 +9,9 @@
 //             memset(stats) ; for each chunk c of layers [l0, l1):
 //               ev_r0[c] ; mpb_router_topk_layers(l0..l1) ; ev_r1[c] ; ev_done[c]
 //           side stream (low priority, side_sms): for each chunk c:
-//               wait ev_done[c] ; for l in [l0, l1): mpb_dispatch_layout(l),
-//               mpb_coactivation(l)        -- beside router chunk c+1
+//               wait ev_done[c] ; for l in [l0, l1): mpb_dispatch_layout(l) ;
+//               mpb_coactivation(layers l0..l1 as one token list)
+//                                          -- beside router chunk c+1
 //           main waits for the side stream's last tail.
 //           One layer (nothing to overlap): router on every SM, then the layout
 //           on main with the co-activation beside it on the side stream.
@@ -271,11 +272,14 @@ mpb_status run_layers(mpb_step *s) {
                 MPB_CUDA(cudaStreamWaitEvent(s->s_side, s->ev_done[c], 0));
             }
             const auto [l0, l1] = s->chunks[c];
-            for (uint32_t l = l0; l < l1; ++l) {
+            for (uint32_t l = l0; l < l1; ++l)
                 if ((st = tail(s, tc, l))) return st;
-                if (d.coact && (st = mpb_coactivation(tc, d.idx + l * pairs, d.T, d.k, d.E, d.coact)))
-                    return st;
-            }
+            // the co-activation sums over tokens and layers alike: the chunk's
+            // contiguous [l1 - l0][T][k] routing is ONE token list (one launch pair
+            // per chunk instead of per layer; integer sums, the same matrix)
+            if (d.coact && (st = mpb_coactivation(tc, d.idx + l0 * pairs, uint64_t(l1 - l0) * d.T, d.k,
+                                                  d.E, d.coact)))
+                return st;
             // multi-GPU: this chunk's demand becomes global before it is priced
             if ((st = reduce_stats(s, l0, l1, c + 1 == nc, tc->stream))) return st;
             if (d.score_per_chunk) {

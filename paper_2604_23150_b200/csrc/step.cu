@@ -25,6 +25,7 @@
 #include <nccl.h>  // types and prototypes only: the functions are resolved at run time
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <utility>
 #include <vector>
@@ -109,6 +110,12 @@ struct mpb_step {
     ncclComm_t comm = nullptr;
     int world = 1, rank = 0;
     std::vector<mpb_gather_spec> gather;
+    // MPB_STEP_PROBE=1 (experiments, eager runs only): timing events at the
+    // step's start, after each chunk's router (main) and after each chunk's
+    // statistics tails + pricing (their stream), and at the end
+    bool probe = false;
+    cudaEvent_t ev_p0 = nullptr, ev_p1 = nullptr;
+    std::vector<cudaEvent_t> ev_pr, ev_pt;
 };
 
 namespace {
@@ -216,6 +223,7 @@ mpb_status launch_router(mpb_step *s, size_t c) {
     if (s->overlapped) {
         if ((st = record(s, s->ev_r1[set + c], s->s_main, true))) return st;
         MPB_CUDA(cudaEventRecord(s->ev_done[c], s->s_main));
+        if (s->probe && !s->capturing) MPB_CUDA(cudaEventRecord(s->ev_pr[c], s->s_main));
     } else {
         // one layer: the end stamp is taken on the (idle) side stream, so no
         // event-record node sits between the router and the layout on the main
@@ -244,6 +252,8 @@ mpb_status run_layers(mpb_step *s) {
         MPB_CUDA(cudaMemsetAsync(d.zero_base, 0, d.zero_bytes, s->s_side));
         MPB_CUDA(cudaEventRecord(s->ev_zero, s->s_side));
     }
+    const bool probe = s->probe && !s->capturing;
+    if (probe) MPB_CUDA(cudaEventRecord(s->ev_p0, s->s_main));
     bool main_zeroed = !(d.zero_base && d.zero_bytes);
     auto main_waits_zero = [&]() -> mpb_status {
         if (!main_zeroed) {
@@ -291,6 +301,7 @@ mpb_status run_layers(mpb_step *s) {
                 }
                 if (c + 1 == nc && (st = gather_scores(s, tc->stream))) return st;
             }
+            if (probe) MPB_CUDA(cudaEventRecord(s->ev_pt[c], tc->stream));
         }
     } else {
         for (size_t c = 0; c < s->chunks.size(); ++c) {
@@ -313,6 +324,7 @@ mpb_status run_layers(mpb_step *s) {
     MPB_CUDA(cudaEventRecord(s->ev_join, s->s_side));
     MPB_CUDA(cudaStreamWaitEvent(s->s_main, s->ev_join, 0));
     if (!s->overlapped && (st = reduce_stats(s, 0, d.layers, true, s->s_main))) return st;
+    if (probe) MPB_CUDA(cudaEventRecord(s->ev_p1, s->s_main));
     MPB_CUDA(cudaEventRecord(s->ev_out, s->s_main));
     MPB_CUDA(cudaStreamWaitEvent(s->origin, s->ev_out, 0));
     return MPB_OK;
@@ -421,6 +433,17 @@ mpb_status mpb_step_create(mpb_context *ctx, const mpb_step_desc *desc, mpb_step
         e = cudaEventCreate(&s->ev_r0[i]);
         if (e == cudaSuccess) e = cudaEventCreate(&s->ev_r1[i]);
     }
+    if (const char *pe = std::getenv("MPB_STEP_PROBE"); pe && pe[0] == '1' && e == cudaSuccess) {
+        s->probe = true;
+        s->ev_pr.assign(nc, nullptr);
+        s->ev_pt.assign(nc, nullptr);
+        e = cudaEventCreate(&s->ev_p0);
+        if (e == cudaSuccess) e = cudaEventCreate(&s->ev_p1);
+        for (size_t c = 0; c < nc && e == cudaSuccess; ++c) {
+            e = cudaEventCreate(&s->ev_pr[c]);
+            if (e == cudaSuccess) e = cudaEventCreate(&s->ev_pt[c]);
+        }
+    }
     if (e != cudaSuccess) return cleanup(cuda_fail(e, "mpb_step_create"));
     if (mpb_status st = mpb_context_create(ctx->device, s->s_main, &s->main)) return cleanup(st);
     if (mpb_status st = mpb_context_create(ctx->device, s->s_side, &s->side)) return cleanup(st);
@@ -446,9 +469,9 @@ mpb_status mpb_step_destroy(mpb_step *s) {
     if (s->comm) nccl().destroy(s->comm);
     mpb_context_destroy(s->main);
     mpb_context_destroy(s->side);
-    for (cudaEvent_t ev : {s->ev_in, s->ev_out, s->ev_fork, s->ev_join, s->ev_zero})
+    for (cudaEvent_t ev : {s->ev_in, s->ev_out, s->ev_fork, s->ev_join, s->ev_zero, s->ev_p0, s->ev_p1})
         if (ev) cudaEventDestroy(ev);
-    for (auto *v : {&s->ev_done, &s->ev_r0, &s->ev_r1})
+    for (auto *v : {&s->ev_done, &s->ev_r0, &s->ev_r1, &s->ev_pr, &s->ev_pt})
         for (cudaEvent_t ev : *v)
             if (ev) cudaEventDestroy(ev);
     if (s->s_main) cudaStreamDestroy(s->s_main);
@@ -487,7 +510,9 @@ mpb_status capture_graph(mpb_step *s, uint32_t phases, cudaGraphExec_t *exec, cu
         return st;
     }
     if (e != cudaSuccess) return cuda_fail(e, "mpb_step_capture: cudaStreamEndCapture");
-    const cudaError_t e2 = cudaGraphInstantiate(exec, g, 0);
+    // per-node priorities (captured from the streams): the routers keep their
+    // high priority over the statistics tails inside the graph too
+    const cudaError_t e2 = cudaGraphInstantiate(exec, g, cudaGraphInstantiateFlagUseNodePriority);
     if (e2 != cudaSuccess) {
         cudaGraphDestroy(g);
         return cuda_fail(e2, "mpb_step_capture: cudaGraphInstantiate");
@@ -665,3 +690,20 @@ mpb_status mpb_step_attach_comm(mpb_step *s, const uint8_t id[128], int world, i
 }
 
 }  // extern "C"
+
+// Experiments (MPB_STEP_PROBE=1, eager runs): the last run's timeline in ms from
+// its start — out[c] = router chunk c done, out[nc + c] = chunk c's statistics
+// tails + pricing done, out[2 nc] = step end. Returns the number written.
+extern "C" __attribute__((visibility("default"))) int mpb_debug_step_probe(const mpb_step *s, float *out,
+                                                                          size_t n) {
+    if (!s || !s->probe || !out) return -1;
+    const size_t nc = s->chunks.size();
+    if (n < 2 * nc + 1) return -1;
+    if (cudaEventSynchronize(s->ev_p1) != cudaSuccess) return -1;
+    for (size_t c = 0; c < nc; ++c) {
+        if (cudaEventElapsedTime(&out[c], s->ev_p0, s->ev_pr[c]) != cudaSuccess) return -1;
+        if (cudaEventElapsedTime(&out[nc + c], s->ev_p0, s->ev_pt[c]) != cudaSuccess) return -1;
+    }
+    if (cudaEventElapsedTime(&out[2 * nc], s->ev_p0, s->ev_p1) != cudaSuccess) return -1;
+    return static_cast<int>(2 * nc + 1);
+}

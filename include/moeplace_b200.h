@@ -13,6 +13,8 @@
  *   mpb_router_topk        (new) router GEMM + top-k; feeds what route_tokens
  *                          produces (trace.cpp:240-259)
  *   mpb_router_topk_layers (new) the same for several layers in one launch
+ *   mpb_router_topk_demand (new) mpb_router_topk + simulate_layer's demand
+ *                          count (simulator.cpp:64-80) in its epilogue
  *   mpb_topk_logits        (new) top-k over given logits, tie rule of
  *                          placement.cpp:143-152
  *   mpb_dispatch_layout    simulate_layer's per-destination accounting
@@ -146,6 +148,18 @@ MPB_API mpb_status mpb_router_topk_layers(mpb_context *ctx, uint32_t layers, con
                                           const void *const *W, uint64_t T, uint32_t H, uint32_t E,
                                           uint32_t k, int score_fn, int renorm, int32_t *idx,
                                           float *weights, float *logits_out);
+/* mpb_router_topk that also counts the dispatch demand as it writes each
+ * selected (token, expert): demand[src_group[t]][e] += 1 (uint64 [D][E],
+ * device, accumulated — the caller zeroes it), and demand2 under src_group2
+ * when given (the same counts mpb_dispatch_layout produces: integer sums,
+ * bit-identical). A source group >= D is flagged (MPB_VALIDATION_ERROR at
+ * mpb_context_sync), not counted. Lets a single-layer step price the demand
+ * right after the router while the permutation is built beside it. */
+MPB_API mpb_status mpb_router_topk_demand(mpb_context *ctx, const void *X, const void *W, uint64_t T,
+                                          uint32_t H, uint32_t E, uint32_t k, int score_fn, int renorm,
+                                          int32_t *idx, float *weights, float *logits_out,
+                                          const uint8_t *src_group, const uint8_t *src_group2, uint32_t D,
+                                          uint64_t *demand, uint64_t *demand2);
 /* Top-k over given fp32 logits [T,E] (device), E <= 1024. */
 MPB_API mpb_status mpb_topk_logits(mpb_context *ctx, const float *logits, uint64_t T, uint32_t E,
                                    uint32_t k, int score_fn, int renorm, int32_t *idx,
@@ -428,6 +442,15 @@ MPB_API mpb_status mpb_step_router_ms(const mpb_step *step, float *ms, uint32_t 
  * launch) into chunks[] (capacity layers), *n_chunks. */
 MPB_API mpb_status mpb_step_info(const mpb_step *step, uint32_t phases, uint64_t *launches,
                                  uint32_t *chunks, uint32_t *n_chunks);
+/* Tests / experiments. mpb_debug_step_fused: 1 when the plan's single-layer
+ * step counts the demand in the router (mpb_router_topk_demand) and prices it
+ * beside the layout (one layer, one GPU, MPB_ROUTER_DEMAND != 0).
+ * mpb_debug_step_probe (plan created with MPB_STEP_PROBE=1, eager runs): the
+ * last run's timeline in ms from its start — out[c] = router chunk c done,
+ * out[nc + c] = chunk c's statistics tails + pricing done, out[2 nc] = step
+ * end; returns the count written (2 nc + 1) or -1. */
+MPB_API int mpb_debug_step_fused(const mpb_step *step);
+MPB_API int mpb_debug_step_probe(const mpb_step *step, float *out, size_t n);
 
 /* ---- host placement / grouping policies (no device needed) ----------------
  * Restatements of the reference policies with the same std::mt19937_64 /

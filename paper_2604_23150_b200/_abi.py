@@ -72,6 +72,8 @@ _SIGS = {
     "mpb_build_dest_lut": (C.c_int, [_u32p, _u32p, C.c_uint32, C.c_uint32, _u32p, _u8p]),
     "mpb_router_topk": (C.c_int, [_p, _p, _p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32,
                                   C.c_int, C.c_int, _p, _p, _p]),
+    "mpb_router_topk_demand": (C.c_int, [_p, _p, _p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32,
+                                         C.c_int, C.c_int, _p, _p, _p, _p, _p, C.c_uint32, _p, _p]),
     "mpb_router_topk_layers": (C.c_int, [_p, C.c_uint32, _p, _p, C.c_uint64, C.c_uint32, C.c_uint32,
                                          C.c_uint32, C.c_int, C.c_int, _p, _p, _p]),
     "mpb_topk_logits": (C.c_int, [_p, _p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_int, C.c_int,
@@ -111,6 +113,8 @@ _SIGS = {
     "mpb_step_timing_reset": (C.c_int, [_p]),
     "mpb_step_router_ms": (C.c_int, [_p, _f32p, _u32p]),
     "mpb_step_info": (C.c_int, [_p, C.c_uint32, _u64p, _u32p, _u32p]),
+    "mpb_debug_step_fused": (C.c_int, [_p]),
+    "mpb_debug_step_probe": (C.c_int, [_p, C.POINTER(C.c_float), C.c_size_t]),
     "mpb_nccl_get_unique_id": (C.c_int, [_p]),
     "mpb_step_attach_comm": (C.c_int, [_p, _p, C.c_int, C.c_int, _p, C.c_uint32]),
     "mpb_linear_placement": (C.c_int, [C.c_uint32, C.c_uint32, _p]),

@@ -117,7 +117,32 @@ struct RouterParams {
     // split-K tail through distributed shared memory (single-CTA tiles): the S
     // K-part units of a tail tile form one cluster (cluster_tail != 0)
     uint32_t cluster_tail;
+    // fused dispatch demand (mpb_router_topk_demand, one layer): every selected
+    // (token, expert) adds 1 to demand[src[token]][expert] (and demand2 under
+    // src2) as it is written; nullptr: off
+    const uint8_t *src, *src2;
+    unsigned long long *demand, *demand2;
+    uint32_t D;
+    uint32_t *err;
 };
+
+// The fused demand count of one selected (token, expert) pair (the layout's
+// K2 demand histogram, simulator.cpp:64-80 semantics: source group >= D is
+// flagged, not counted).
+__device__ __forceinline__ void count_demand(const RouterParams &p, uint64_t token, uint32_t e) {
+    const uint32_t s = p.src[token];
+    if (s < p.D)
+        atomicAdd(p.demand + static_cast<size_t>(s) * p.E + e, 1ull);
+    else
+        atomicOr(p.err, kErrSourceRange);
+    if (p.demand2) {
+        const uint32_t s2 = p.src2[token];
+        if (s2 < p.D)
+            atomicAdd(p.demand2 + static_cast<size_t>(s2) * p.E + e, 1ull);
+        else
+            atomicOr(p.err, kErrSourceRange);
+    }
+}
 
 // Work item n of a scheduling unit: full waves of whole tiles, then (split
 // tail) unit u takes K part (u % S) of tail tile u / S. role 0 = whole tile,
@@ -334,6 +359,7 @@ __device__ __forceinline__ void tail_select(const RouterParams &p, const float *
             const uint64_t o = (out_row_tile0 + h * RPS + rr) * p.k + lane;
             p.idx[o] = static_cast<int32_t>(sid[r]);
             p.w[o] = p.renorm ? (tsum[r] > 0.f ? e[r] / tsum[r] : 0.f) : softmax ? e[r] / spart[r] : e[r];
+            if (p.demand) count_demand(p, row_tile0 + h * RPS + rr, sid[r]);
         }
     }
 }
@@ -983,6 +1009,7 @@ __global__ void __launch_bounds__(kThreadsR, 1)
                         const float x = p.renorm ? (wsum > 0.f ? w[j] / wsum : 0.f) : w[j];
                         p.idx[out_row * p.k + (j - off)] = ti[j];
                         p.w[out_row * p.k + (j - off)] = x;
+                        if (p.demand) count_demand(p, row, static_cast<uint32_t>(ti[j]));
                     }
                 }
             }
@@ -1232,12 +1259,36 @@ extern "C" mpb_status mpb_router_topk(mpb_context *ctx, const void *X, const voi
         return fail(MPB_CONFIG_ERROR, "mpb_router_topk: X and W must be 16-byte aligned");
     if (T == 0) return MPB_OK;
     RouterParams p{T, H, k, score_fn, renorm, 0, idx, weights, logits_out, 1, nullptr, nullptr, E,
-                   nullptr, 0, 1};
+                   nullptr, 0, 1, 0, nullptr, nullptr, nullptr, nullptr, 0, nullptr};
     bool pair;
     const uint32_t N = router_tile_n(E, &pair);
     CUtensorMap mx, mw;
     if (!make_map(&mx, X, T, H, kBM) || !make_map(&mw, W, E, H, pair ? N / 2 : N))
         return fail(MPB_CUDA_ERROR, "mpb_router_topk: cuTensorMapEncodeTiled failed");
+    return router_dispatch(ctx, N, pair, mx, mw, p);
+}
+
+extern "C" mpb_status mpb_router_topk_demand(mpb_context *ctx, const void *X, const void *W, uint64_t T,
+                                             uint32_t H, uint32_t E, uint32_t k, int score_fn, int renorm,
+                                             int32_t *idx, float *weights, float *logits_out,
+                                             const uint8_t *src_group, const uint8_t *src_group2,
+                                             uint32_t D, uint64_t *demand, uint64_t *demand2) {
+    if (!ctx || (T && (!X || !W || !idx || !weights || !src_group || !demand)) || (src_group2 && !demand2))
+        return fail(MPB_VALIDATION_ERROR, "mpb_router_topk_demand: NULL argument");
+    if (mpb_status st = router_check("mpb_router_topk_demand", T, H, E, k, score_fn)) return st;
+    if (D == 0 || D > 255) return fail(MPB_CONFIG_ERROR, "mpb_router_topk_demand: need 1 <= D <= 255");
+    if ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(W)) & 15)
+        return fail(MPB_CONFIG_ERROR, "mpb_router_topk_demand: X and W must be 16-byte aligned");
+    if (T == 0) return MPB_OK;
+    RouterParams p{T, H, k, score_fn, renorm, 0, idx, weights, logits_out, 1, nullptr, nullptr, E,
+                   nullptr, 0, 1, 0, src_group, src_group2,
+                   reinterpret_cast<unsigned long long *>(demand),
+                   src_group2 ? reinterpret_cast<unsigned long long *>(demand2) : nullptr, D, ctx->d_error};
+    bool pair;
+    const uint32_t N = router_tile_n(E, &pair);
+    CUtensorMap mx, mw;
+    if (!make_map(&mx, X, T, H, kBM) || !make_map(&mw, W, E, H, pair ? N / 2 : N))
+        return fail(MPB_CUDA_ERROR, "mpb_router_topk_demand: cuTensorMapEncodeTiled failed");
     return router_dispatch(ctx, N, pair, mx, mw, p);
 }
 
@@ -1296,7 +1347,8 @@ extern "C" mpb_status mpb_router_topk_layers(mpb_context *ctx, uint32_t layers, 
         it = ctx->router_maps.emplace(std::move(key), d).first;
     }
     RouterParams p{T, H, k, score_fn, renorm, 0, idx, weights, logits_out, 1, nullptr, nullptr, E,
-                   static_cast<const CUtensorMap *>(it->second), 0, layers};
+                   static_cast<const CUtensorMap *>(it->second), 0, layers, 0, nullptr, nullptr, nullptr,
+                   nullptr, 0, nullptr};
     CUtensorMap unused{};
     return router_dispatch(ctx, N, pair, unused, unused, p);
 }

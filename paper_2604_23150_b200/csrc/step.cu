@@ -85,6 +85,17 @@ struct mpb_step {
     std::vector<mpb_score_job> jobs;
     std::vector<std::pair<uint32_t, uint32_t>> chunks;
     bool overlapped = false;
+    // one layer, one GPU: the router counts the demand tables itself
+    // (mpb_router_topk_demand) and the layout writes its copy into scratch, so
+    // the pricing follows the router directly while the layout + permutation
+    // and the co-activation run beside it (MPB_ROUTER_DEMAND=0: off)
+    bool fused_ok = false;
+    uint64_t *scratch_demand = nullptr;  // [2][D][E]
+    // fused single layer: the layout + permutation on a third stream, beside
+    // the pricing (main) and the co-activation (side)
+    cudaStream_t s_lay = nullptr;
+    mpb_context *lay = nullptr;
+    cudaEvent_t ev_join2 = nullptr;
     cudaEvent_t ev_in = nullptr, ev_out = nullptr, ev_fork = nullptr, ev_join = nullptr,
                 ev_zero = nullptr;
     std::vector<cudaEvent_t> ev_done;
@@ -143,6 +154,8 @@ std::vector<std::pair<uint32_t, uint32_t>> taper_chunks(uint32_t L, uint32_t G) 
     return out;
 }
 
+bool fused_single(const mpb_step *s) { return s->fused_ok && !s->comm; }
+
 mpb_status record(mpb_step *s, cudaEvent_t ev, cudaStream_t st, bool timing) {
 #ifdef MPB_EXP_NO_TIMING  // experiment: the step without its router timing events
     if (timing) return MPB_OK;
@@ -152,15 +165,19 @@ mpb_status record(mpb_step *s, cudaEvent_t ev, cudaStream_t st, bool timing) {
     return MPB_OK;
 }
 
-mpb_status tail(mpb_step *s, mpb_context *c, uint32_t l) {
+mpb_status tail(mpb_step *s, mpb_context *c, uint32_t l, bool scratch_demand = false) {
     const mpb_step_desc &d = s->d;
     const uint32_t D = d.deployed->D, E = d.E;
     const size_t pairs = static_cast<size_t>(d.T) * d.k;
     mpb_tokens tk{d.idx + l * pairs, d.T, d.k, d.src_group, 0, 0, d.tag, d.n_tags, d.src_group2};
-    if (mpb_status st = mpb_dispatch_layout(
-            c, &tk, d.deployed, d.demand + static_cast<size_t>(l) * D * E,
-            d.demand2 ? d.demand2 + static_cast<size_t>(l) * D * E : nullptr, d.tag_pop,
-            d.sorted_pairs, d.pair_pos, d.key_offsets))
+    uint64_t *dem = d.demand + static_cast<size_t>(l) * D * E;
+    uint64_t *dem2 = d.demand2 ? d.demand2 + static_cast<size_t>(l) * D * E : nullptr;
+    if (scratch_demand) {  // the router counted the demand; the layout's copy is discarded
+        dem = s->scratch_demand;
+        dem2 = d.demand2 ? s->scratch_demand + static_cast<size_t>(D) * E : nullptr;
+    }
+    if (mpb_status st = mpb_dispatch_layout(c, &tk, d.deployed, dem, dem2, d.tag_pop, d.sorted_pairs,
+                                            d.pair_pos, d.key_offsets))
         return st;
     return MPB_OK;
 }
@@ -212,7 +229,11 @@ mpb_status launch_router(mpb_step *s, size_t c) {
     if (s->overlapped && c == 0)
         if (mpb_status st = record(s, s->ev_r0[set + c], s->s_main, true)) return st;
     mpb_status st;
-    if (l1 - l0 == 1)
+    if (fused_single(s))
+        st = mpb_router_topk_demand(s->main, s->X[l0], s->W[l0], d.T, d.H, d.E, d.k, d.score_fn, d.renorm,
+                                    d.idx + l0 * pairs, d.weights + l0 * pairs, nullptr, d.src_group,
+                                    d.src_group2, d.deployed->D, d.demand, d.demand2);
+    else if (l1 - l0 == 1)
         st = mpb_router_topk(s->main, s->X[l0], s->W[l0], d.T, d.H, d.E, d.k, d.score_fn, d.renorm,
                              d.idx + l0 * pairs, d.weights + l0 * pairs, nullptr);
     else
@@ -303,6 +324,24 @@ mpb_status run_layers(mpb_step *s) {
             }
             if (probe) MPB_CUDA(cudaEventRecord(s->ev_pt[c], tc->stream));
         }
+    } else if (fused_single(s)) {
+        // router (with the demand count) -> pricing on main; the layout +
+        // permutation and the co-activation beside the pricing on the side
+        if ((st = main_waits_zero())) return st;
+        if ((st = launch_router(s, 0))) return st;
+        MPB_CUDA(cudaEventRecord(s->ev_fork, s->s_main));
+        MPB_CUDA(cudaStreamWaitEvent(s->s_side, s->ev_fork, 0));
+        MPB_CUDA(cudaStreamWaitEvent(s->s_lay, s->ev_fork, 0));
+        if (d.coact && (st = mpb_coactivation(s->side, d.idx, d.T, d.k, d.E, d.coact))) return st;
+        if ((st = tail(s, s->lay, 0, true))) return st;
+        MPB_CUDA(cudaEventRecord(s->ev_join2, s->s_lay));
+        MPB_CUDA(cudaStreamWaitEvent(s->s_main, s->ev_join2, 0));
+        if (s->jobs.size() == 2 && s->jobs[0].B == d.layers && s->jobs[1].B == d.layers) {
+            if ((st = score_finalize_pair(s->main, s->jobs[0], s->jobs[1], 0, 1))) return st;
+        } else {
+            for (const mpb_score_job &j : s->jobs)
+                if (j.B == d.layers && (st = score_finalize_range(s->main, j, 0, 1))) return st;
+        }
     } else {
         for (size_t c = 0; c < s->chunks.size(); ++c) {
             if ((st = launch_router(s, c))) return st;
@@ -331,7 +370,7 @@ mpb_status run_layers(mpb_step *s) {
 }
 
 bool score_in_layers(const mpb_step *s, const mpb_score_job &j) {
-    return s->overlapped && s->d.score_per_chunk && j.B == s->d.layers;
+    return (s->overlapped || fused_single(s)) && s->d.score_per_chunk && j.B == s->d.layers;
 }
 
 mpb_status run_score(mpb_step *s) {
@@ -376,7 +415,9 @@ mpb_status run_phases(mpb_step *s, uint32_t phases) {
     return MPB_OK;
 }
 
-uint64_t launch_total(const mpb_step *s) { return s->main->launches + s->side->launches; }
+uint64_t launch_total(const mpb_step *s) {
+    return s->main->launches + s->side->launches + (s->lay ? s->lay->launches : 0);
+}
 
 }  // namespace
 
@@ -444,9 +485,22 @@ mpb_status mpb_step_create(mpb_context *ctx, const mpb_step_desc *desc, mpb_step
             if (e == cudaSuccess) e = cudaEventCreate(&s->ev_pt[c]);
         }
     }
+    {
+        const char *fe = std::getenv("MPB_ROUTER_DEMAND");
+        s->fused_ok = !s->overlapped && d.layers == 1 && d.score_per_chunk && d.src_group && d.demand &&
+                      d.deployed && d.deployed->D <= 255 && d.E <= 256 && !(fe && fe[0] == '0');
+        if (s->fused_ok && e == cudaSuccess)
+            e = cudaMalloc(&s->scratch_demand, 2 * sizeof(uint64_t) * d.deployed->D * d.E);
+    }
     if (e != cudaSuccess) return cleanup(cuda_fail(e, "mpb_step_create"));
     if (mpb_status st = mpb_context_create(ctx->device, s->s_main, &s->main)) return cleanup(st);
     if (mpb_status st = mpb_context_create(ctx->device, s->s_side, &s->side)) return cleanup(st);
+    if (s->fused_ok) {
+        cudaError_t e3 = cudaStreamCreateWithPriority(&s->s_lay, cudaStreamNonBlocking, lo);
+        if (e3 == cudaSuccess) e3 = cudaEventCreateWithFlags(&s->ev_join2, cudaEventDisableTiming);
+        if (e3 != cudaSuccess) return cleanup(cuda_fail(e3, "mpb_step_create"));
+        if (mpb_status st = mpb_context_create(ctx->device, s->s_lay, &s->lay)) return cleanup(st);
+    }
     if (s->overlapped) {
         const uint32_t dev_sms = static_cast<uint32_t>(ctx->device_sms);
         if (side_sms >= dev_sms) return cleanup(fail(MPB_CONFIG_ERROR, "mpb_step_create: side_sms >= SMs"));
@@ -461,6 +515,7 @@ mpb_status mpb_step_destroy(mpb_step *s) {
     if (!s) return MPB_OK;
     if (s->s_main) cudaStreamSynchronize(s->s_main);
     if (s->s_side) cudaStreamSynchronize(s->s_side);
+    if (s->s_lay) cudaStreamSynchronize(s->s_lay);
     if (s->g_layers) cudaGraphExecDestroy(s->g_layers);
     if (s->graph_layers) cudaGraphDestroy(s->graph_layers);
     if (s->g_all) cudaGraphExecDestroy(s->g_all);
@@ -469,11 +524,15 @@ mpb_status mpb_step_destroy(mpb_step *s) {
     if (s->comm) nccl().destroy(s->comm);
     mpb_context_destroy(s->main);
     mpb_context_destroy(s->side);
+    if (s->lay) mpb_context_destroy(s->lay);
+    if (s->ev_join2) cudaEventDestroy(s->ev_join2);
+    if (s->s_lay) cudaStreamDestroy(s->s_lay);
     for (cudaEvent_t ev : {s->ev_in, s->ev_out, s->ev_fork, s->ev_join, s->ev_zero, s->ev_p0, s->ev_p1})
         if (ev) cudaEventDestroy(ev);
     for (auto *v : {&s->ev_done, &s->ev_r0, &s->ev_r1, &s->ev_pr, &s->ev_pt})
         for (cudaEvent_t ev : *v)
             if (ev) cudaEventDestroy(ev);
+    if (s->scratch_demand) cudaFree(s->scratch_demand);
     if (s->s_main) cudaStreamDestroy(s->s_main);
     if (s->s_side) cudaStreamDestroy(s->s_side);
     if (s->s_cap) cudaStreamDestroy(s->s_cap);
@@ -611,7 +670,8 @@ mpb_status mpb_step_sync(mpb_step *s) {
     MPB_CUDA(cudaStreamSynchronize(s->ctx->stream));
     mpb_status a = mpb_context_sync(s->main);
     mpb_status b = mpb_context_sync(s->side);
-    return a ? a : b;
+    mpb_status c = s->lay ? mpb_context_sync(s->lay) : MPB_OK;
+    return a ? a : b ? b : c;
 }
 
 mpb_status mpb_step_timing_reset(mpb_step *s) {
@@ -694,7 +754,7 @@ mpb_status mpb_step_attach_comm(mpb_step *s, const uint8_t id[128], int world, i
 // Experiments (MPB_STEP_PROBE=1, eager runs): the last run's timeline in ms from
 // its start — out[c] = router chunk c done, out[nc + c] = chunk c's statistics
 // tails + pricing done, out[2 nc] = step end. Returns the number written.
-extern "C" __attribute__((visibility("default"))) int mpb_debug_step_probe(const mpb_step *s, float *out,
+extern "C" MPB_API int mpb_debug_step_probe(const mpb_step *s, float *out,
                                                                           size_t n) {
     if (!s || !s->probe || !out) return -1;
     const size_t nc = s->chunks.size();
@@ -706,4 +766,10 @@ extern "C" __attribute__((visibility("default"))) int mpb_debug_step_probe(const
     }
     if (cudaEventElapsedTime(&out[2 * nc], s->ev_p0, s->ev_p1) != cudaSuccess) return -1;
     return static_cast<int>(2 * nc + 1);
+}
+
+// Tests: 1 when this plan's single-layer step counts the demand in the router
+// (mpb_router_topk_demand) and prices it beside the layout.
+extern "C" MPB_API int mpb_debug_step_fused(const mpb_step *s) {
+    return s && fused_single(s) ? 1 : 0;
 }

@@ -378,6 +378,26 @@ class Engine:
                   int(renorm), _ptr(idx), _ptr(w), _ptr(logits))
         return (idx, w, logits) if want_logits else (idx, w)
 
+    def router_topk_demand(self, X: torch.Tensor, W: torch.Tensor, k: int, score_fn: int,
+                           renorm: bool, src: torch.Tensor, D: int, demand: torch.Tensor,
+                           src2: Optional[torch.Tensor] = None,
+                           demand2: Optional[torch.Tensor] = None, want_logits: bool = False):
+        """router_topk that also adds every selected (token, expert) to
+        demand[src[token], expert] (uint64 [D, E], accumulated), and to demand2
+        under src2 (mpb_router_topk_demand): the dispatch demand of
+        simulate_layer (simulator.cpp:64-80) counted in the router's epilogue."""
+        T, H = X.shape
+        E = W.shape[0]
+        idx = torch.empty(T, k, dtype=torch.int32, device=self.device)
+        w = torch.empty(T, k, dtype=torch.float32, device=self.device)
+        logits = torch.empty(T, E, dtype=torch.float32, device=self.device) if want_logits \
+            else None
+        assert src.dtype == torch.uint8 and demand.dtype == torch.uint64
+        _abi.call("mpb_router_topk_demand", self.ctx, _ptr(X), _ptr(W), T, H, E, k, score_fn,
+                  int(renorm), _ptr(idx), _ptr(w), _ptr(logits), _ptr(src), _ptr(src2), D,
+                  _ptr(demand), _ptr(demand2))
+        return (idx, w, logits) if want_logits else (idx, w)
+
     def router_topk_layers(self, Xs, Ws, k: int, score_fn: int = 0, renorm: bool = False,
                            out=None, logits_out: Optional[torch.Tensor] = None):
         """Router + top-k of several layers (same T, H, E) in one launch

@@ -28,6 +28,7 @@ from typing import Optional
 import numpy as np
 import torch
 
+from . import _abi
 from . import moeplace as mp
 from . import policies as pol
 
@@ -823,6 +824,10 @@ class RoutingPipeline:
                     batch_size=batch_size, seed=seed,
                     a2a_bytes_saved_pct=100.0 * (1.0 - summ["data_based"].normalized_median),
                     normalized={k: v.normalized_median for k, v in summ.items()})
+
+    def plan_fused(self) -> bool:
+        """The C++ step counts the demand in the router (one layer, one GPU)."""
+        return self.plan is not None and bool(_abi.lib().mpb_debug_step_fused(self.plan.handle))
 
     def results(self):
         """Per-layer LayerSims of the named strategies and the search winner

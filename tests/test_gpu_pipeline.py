@@ -89,6 +89,44 @@ def test_graph_replay_matches_eager(monkeypatch):
     assert torch.equal(pipe.fin_cl[0], fin_cl) and torch.equal(pipe.fin_rr[0], fin_rr)
 
 
+def test_single_layer_fused_demand_step(monkeypatch, oracle):
+    """One layer, one GPU: the router counts the demand tables in its epilogue
+    (mpb_router_topk_demand) and the step prices them right after it, the
+    layout + permutation and the co-activation beside the pricing. Statistics
+    and LayerSims equal the unfused schedule's (MPB_ROUTER_DEMAND=0) bit for
+    bit, eagerly and replayed from the graph; the demand equals the oracle's
+    histogram of the step's routing."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    spec = WorkloadSpec("tiny1", 1, 4096, 512, 128, 8, 0, True, groups=8, nodes=2, domains=8,
+                        preferred=16, candidates=64)
+    out = {}
+    for fused in ("0", "1"):
+        monkeypatch.setenv("MPB_ROUTER_DEMAND", fused)
+        eng = mp.Engine(0)
+        pipe = RoutingPipeline(spec, eng, 0, 1, resident=True)
+        assert pipe.plan is not None and pipe.plan_fused() == (fused == "1")
+        pipe.step()
+        torch.cuda.synchronize()
+        eager = (pipe.stats.clone(), pipe.fin_cl[0].clone(), pipe.fin_rr[0].clone(), pipe.results())
+        assert pipe.capture()
+        for _ in range(2):
+            pipe.step()
+        torch.cuda.synchronize()
+        assert torch.equal(pipe.stats, eager[0])
+        assert torch.equal(pipe.fin_cl[0], eager[1]) and torch.equal(pipe.fin_rr[0], eager[2])
+        out[fused] = (eager, pipe)
+    (e0, _), (e1, p1) = out["0"], out["1"]
+    assert torch.equal(e0[0], e1[0]) and torch.equal(e0[1], e1[1]) and torch.equal(e0[2], e1[2])
+    assert e0[3] == e1[3]
+    top = p1.topology
+    db = {e.label: e for e in p1.calib.strategies}["data_based"].placement
+    lut = oracle.dest_lut(db.groups, top.group_to_node, spec.experts)
+    ref = oracle.dispatch_layout(p1.idx_buf[0].cpu().numpy(), p1.h_src_cl.astype(np.uint32), lut,
+                                 spec.groups, spec.experts, top.group_to_node)
+    np.testing.assert_array_equal(p1.dem_cl[0].cpu().numpy(), ref["demand"])
+
+
 def test_sm_partition_confines_kernels(monkeypatch):
     """mpb_sm_partition_create: two green-context streams on disjoint SM sets;
     the library's kernels run on them (here the overlapped schedule with the

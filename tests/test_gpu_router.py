@@ -314,3 +314,37 @@ def test_router_ties_inf_nan(eng, oracle, shape, tail, monkeypatch):
     np.testing.assert_array_equal(idx.cpu().numpy(), ri)
     fin = np.isfinite(L).all(1)
     np.testing.assert_allclose(w.cpu().numpy()[fin], rw[fin], rtol=2e-6, atol=1e-7)
+
+
+@pytest.mark.parametrize("shape", [(4096, 4096, 128, 8, 0, 8), (2048, 7168, 256, 8, 1, 8),
+                                   (3000, 1024, 64, 4, 0, 5), (65536, 1024, 128, 8, 1, 16)])
+def test_router_topk_demand(eng, shape):
+    """mpb_router_topk_demand: the same routing as mpb_router_topk (bit for
+    bit: same kernel, same tile schedule) and demand / demand2 equal to the
+    histogram of (source group, selected expert) — what mpb_dispatch_layout
+    counts (simulator.cpp:64-80). Covers the cluster tail (decode shape), the
+    2-SM pair epilogue (E = 256), E = 64 and a multi-wave batch. A source
+    group >= D raises ValidationError at sync."""
+    from paper_2604_23150_b200.errors import ValidationError
+    T, H, E, k, fn, D = shape
+    g = torch.Generator(device="cuda").manual_seed(T + E + D)
+    X = torch.randn(T, H, device="cuda", generator=g).to(torch.bfloat16)
+    W = (torch.randn(E, H, device="cuda", generator=g) / H ** 0.5).to(torch.bfloat16)
+    src = torch.randint(0, D, (T,), device="cuda", generator=g).to(torch.uint8)
+    src2 = ((torch.arange(T, device="cuda") * 7) % D).to(torch.uint8)
+    dem = torch.zeros(D, E, dtype=torch.uint64, device="cuda")
+    dem2 = torch.zeros(D, E, dtype=torch.uint64, device="cuda")
+    ri, rw = eng.router_topk(X, W, k, fn, True)
+    idx, w = eng.router_topk_demand(X, W, k, fn, True, src, D, dem, src2, dem2)
+    eng.sync()
+    assert torch.equal(idx, ri) and torch.equal(w, rw)
+    ih = idx.cpu().numpy().astype(np.int64)
+    for s_, d_ in ((src, dem), (src2, dem2)):
+        ref = np.zeros((D, E), np.uint64)
+        np.add.at(ref, (np.repeat(s_.cpu().numpy().astype(np.int64), k), ih.reshape(-1)), 1)
+        np.testing.assert_array_equal(d_.cpu().numpy(), ref)
+    bad = src.clone()
+    bad[T // 2] = D
+    eng.router_topk_demand(X, W, k, fn, True, bad, D, dem)
+    with pytest.raises(ValidationError):
+        eng.sync()

@@ -37,6 +37,17 @@ METRIC = "routed tokens/sec (gate+place+dispatch) at 1/2/4/8 B200; a2a bytes sav
 UNIT = "tokens/s"
 
 
+# The JSON line is the only thing on stdout: fd 1 is pointed at stderr for the
+# run (NCCL, CUDA libraries and extensions print to the process's stdout at C
+# level, e.g. "NCCL version ..."), and the line goes to a saved copy of it.
+_JSON_OUT = None
+
+
+def emit(line: dict) -> None:
+    out = _JSON_OUT if _JSON_OUT is not None else sys.stdout
+    print(json.dumps(line), file=out, flush=True)
+
+
 def log(msg: str) -> None:
     if int(os.environ.get("RANK", "0")) == 0:
         print(f"[bench] {msg}", file=sys.stderr, flush=True)
@@ -221,7 +232,7 @@ def run_reference_arm(args, spec):
                              "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 # ---------------------------------------------------------------- GPU arm
@@ -516,13 +527,18 @@ def run_gpu_arm(args, spec):
                 "normalized_inter_node_bytes_per_layer_median": res["normalized"],
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "a2a": a2a,
                 "gpu_launches": launches, "cuda_graph": graphed, "clocks": clocks.summary()}
-        print(json.dumps(line), flush=True)
+        emit(line)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
 
 
 def main():
+    global _JSON_OUT
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
+    sys.stdout = sys.stderr
     ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)

@@ -90,6 +90,10 @@ struct mpb_step {
     // the pricing follows the router directly while the layout + permutation
     // and the co-activation run beside it (MPB_ROUTER_DEMAND=0: off)
     bool fused_ok = false;
+    // MPB_TAIL_BOOST = n: the last n router chunks run on a smaller grid budget
+    // and the side stream's grids double from the tails that run beside them,
+    // so the statistics backlog left after the last router drains sooner
+    uint32_t tail_boost = 0, side_sms = 0, dev_sms = 0;
     uint64_t *scratch_demand = nullptr;  // [2][D][E]
     // fused single layer: the layout + permutation on a third stream, beside
     // the pricing (main) and the co-activation (side)
@@ -287,9 +291,17 @@ mpb_status run_layers(mpb_step *s) {
     if (s->overlapped) {
         // router c+1 is enqueued before the tails of chunk c, so the main stream
         // never idles while the host enqueues the side stream's launches
-        if ((st = launch_router(s, 0))) return st;
         const size_t nc = s->chunks.size();
+        const uint32_t boost = std::min<uint32_t>(s->tail_boost, static_cast<uint32_t>(nc) - 1);
+        auto budgets = [&](bool boosted) {
+            const uint32_t side = boosted ? 2 * s->side_sms : s->side_sms;
+            mpb_context_set_sm_budget(s->side, side);
+            mpb_context_set_sm_budget(s->main, s->dev_sms - side);
+        };
+        if (boost) budgets(false);
+        if ((st = launch_router(s, 0))) return st;
         for (size_t c = 0; c < nc; ++c) {
+            if (boost && c + 1 == nc - boost) budgets(true);  // routers nc-boost.. and the tails beside them
             if (c + 1 < nc && (st = launch_router(s, c + 1))) return st;
             mpb_context *tc = s->side;
             if (d.score_per_chunk && c + 1 == nc) {
@@ -506,6 +518,10 @@ mpb_status mpb_step_create(mpb_context *ctx, const mpb_step_desc *desc, mpb_step
         if (side_sms >= dev_sms) return cleanup(fail(MPB_CONFIG_ERROR, "mpb_step_create: side_sms >= SMs"));
         mpb_context_set_sm_budget(s->side, side_sms);
         mpb_context_set_sm_budget(s->main, dev_sms - side_sms);
+        s->side_sms = side_sms;
+        s->dev_sms = dev_sms;
+        if (const char *tb = std::getenv("MPB_TAIL_BOOST"))
+            s->tail_boost = 2 * side_sms < dev_sms ? static_cast<uint32_t>(std::max(0, std::atoi(tb))) : 0;
     }
     *out = s;
     return MPB_OK;

@@ -19,6 +19,7 @@
  *                          placement.cpp:143-152
  *   mpb_dispatch_layout    simulate_layer's per-destination accounting
  *                          (simulator.cpp:61-88) + the token permutation
+ *   mpb_dispatch_layout_layers  the same for several layers in one launch set
  *   mpb_layout_derive      per_rank_payload / tokens_per_group / inter-intra
  *                          split (simulator.cpp:81-88); column sums
  *                          (pipeline.cpp:76-82, simulator.cpp:253-258)
@@ -200,6 +201,17 @@ MPB_API mpb_status mpb_dispatch_layout(mpb_context *ctx, const mpb_tokens *token
                                        uint64_t *demand2, uint64_t *tag_pop,
                                        int32_t *sorted_pairs, int32_t *pair_pos,
                                        int64_t *key_offsets);
+/* mpb_dispatch_layout for `layers` layers of the same T, k and placement in
+ * ONE set of launches (grids over (block, layer)): tokens->idx is [layers][T][k];
+ * demand / demand2 [layers][D][E], sorted_pairs / pair_pos [layers][T*k],
+ * key_offsets [layers][D*E+1]; tag_pop sums over the layers. Per-token arrays
+ * (src_group, src_group2, tag) are shared by every layer. Results equal
+ * `layers` single-layer calls (integer counts, stable permutations). */
+MPB_API mpb_status mpb_dispatch_layout_layers(mpb_context *ctx, uint32_t layers, const mpb_tokens *tokens,
+                                              const mpb_placement *placement, uint64_t *demand,
+                                              uint64_t *demand2, uint64_t *tag_pop,
+                                              int32_t *sorted_pairs, int32_t *pair_pos,
+                                              int64_t *key_offsets);
 
 /* From demand[D*E] (device): expert_count[E] (column sums), group_pairs[D]
  * (tokens_per_group / per_rank payload in pairs), node_demand[nodes*E],

@@ -79,6 +79,8 @@ _SIGS = {
     "mpb_topk_logits": (C.c_int, [_p, _p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_int, C.c_int,
                                   _p, _p]),
     "mpb_dispatch_layout": (C.c_int, [_p, C.POINTER(MpbTokens), _p, _p, _p, _p, _p, _p, _p]),
+    "mpb_dispatch_layout_layers": (C.c_int, [_p, C.c_uint32, C.POINTER(MpbTokens), _p, _p, _p, _p, _p,
+                                             _p, _p]),
     "mpb_layout_derive": (C.c_int, [_p, _p, _p, _p, _p, _p, _p]),
     "mpb_coactivation": (C.c_int, [_p, _p, C.c_uint64, C.c_uint32, C.c_uint32, _p]),
     "mpb_sample_batches": (C.c_int, [_p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, _p,

@@ -121,7 +121,8 @@ namespace mpb {
 // Kernel launchers (defined per .cu file); all async on ctx->stream.
 mpb_status launch_layout(mpb_context *ctx, const mpb_tokens *tk, const mpb_placement *pl,
                          uint64_t *demand, uint64_t *demand2, uint64_t *tag_pop,
-                         int32_t *sorted_pairs, int32_t *pair_pos, int64_t *key_offsets);
+                         int32_t *sorted_pairs, int32_t *pair_pos, int64_t *key_offsets,
+                         uint32_t layers = 1);
 mpb_status score_finalize_range(mpb_context *ctx, const mpb_score_job &job, uint32_t b0, uint32_t nb);
 mpb_status score_finalize_pair(mpb_context *ctx, const mpb_score_job &a, const mpb_score_job &b,
                                uint32_t b0, uint32_t nb);

@@ -67,7 +67,26 @@ struct LayoutParams {
     int cell_smem;
     int demand2_smem;
     int tag_smem;
+    // several layers in one launch (blockIdx.y = layer): idx [L][P], demand /
+    // demand2 [L][D][E], each layer's block counts + totals bh_stride words apart
+    uint32_t layers;
+    uint32_t bh_stride;
 };
+
+// The view of layer blockIdx.y of a multi-layer launch (tag_pop: shared sums).
+__device__ __forceinline__ LayoutParams layer_view(LayoutParams p) {
+    if (p.layers > 1) {
+        const size_t l = blockIdx.y, DE = size_t(p.D) * p.E;
+        p.idx += l * p.P;
+        p.demand += l * DE;
+        if (p.demand2) p.demand2 += l * DE;
+        if (p.bhist) {
+            p.bhist += l * p.bh_stride;
+            p.totals += l * p.bh_stride;
+        }
+    }
+    return p;
+}
 
 __device__ __forceinline__ uint32_t source_of(const LayoutParams &p, uint64_t t) {
     return p.src_group ? static_cast<uint32_t>(p.src_group[t])
@@ -420,7 +439,7 @@ __device__ __forceinline__ void count_body(const LayoutParams &p, uint32_t *sm) 
 template <bool kPerm, bool kClu>
 __global__ void __launch_bounds__(kThreads) k_layout_count(LayoutParams p) {
     extern __shared__ uint32_t sm[];
-    count_body<kPerm, kClu>(p, sm);
+    count_body<kPerm, kClu>(layer_view(p), sm);
 }
 
 // Block-wide exclusive scan of one value per thread (kThreads threads).
@@ -456,8 +475,11 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t *s_warp
 // scan of the sums, then the rewrite (one batch of loads each way for
 // nb <= 8 * kThreads).
 __global__ void __launch_bounds__(kThreads) k_layout_scan(uint32_t *bhist, uint32_t nb,
-                                                          uint32_t NS, uint32_t *totals) {
+                                                          uint32_t NS, uint32_t *totals,
+                                                          uint32_t layer_stride) {
     __shared__ uint32_t s_warp[32];
+    bhist += static_cast<size_t>(blockIdx.y) * layer_stride;  // multi-layer launch: layer blockIdx.y
+    totals += static_cast<size_t>(blockIdx.y) * layer_stride;
     pdl_trigger();
     pdl_wait();
     const uint32_t slot = blockIdx.x;
@@ -508,6 +530,12 @@ __global__ void __launch_bounds__(kThreads) k_layout_scatter(LayoutParams p, int
                                                              uint32_t nkeys,
                                                              int64_t *key_offsets) {
     extern __shared__ uint32_t s_w[];  // [kWarps][NS] counters -> bases, [NS+1] bases, [NS] prefixes, stash
+    if (p.layers > 1) {  // layer blockIdx.y of a multi-layer launch
+        sorted_pairs += static_cast<size_t>(blockIdx.y) * p.P;
+        pair_pos += static_cast<size_t>(blockIdx.y) * p.P;
+        key_offsets += static_cast<size_t>(blockIdx.y) * (nkeys + 1);
+        p = layer_view(p);
+    }
     __shared__ uint32_t s_warp[32];
     const uint32_t NS = p.NS;
     uint32_t *s_base = s_w + kWarps * NS;
@@ -987,7 +1015,10 @@ bool launch_layout_cluster(mpb_context *ctx, LayoutParams p, const mpb_placement
 
 mpb_status launch_layout(mpb_context *ctx, const mpb_tokens *tk, const mpb_placement *pl,
                          uint64_t *demand, uint64_t *demand2, uint64_t *tag_pop,
-                         int32_t *sorted_pairs, int32_t *pair_pos, int64_t *key_offsets) {
+                         int32_t *sorted_pairs, int32_t *pair_pos, int64_t *key_offsets,
+                         uint32_t layers) {
+    if (layers == 0) return MPB_OK;
+    if (layers > 65535) return fail(MPB_CONFIG_ERROR, "mpb_dispatch_layout_layers: too many layers");
     // the permutation is requested through key_offsets (never empty: D*E+1
     // entries); sorted_pairs / pair_pos may be NULL only when T*k == 0
     const bool perm = key_offsets != nullptr;
@@ -1008,8 +1039,8 @@ mpb_status launch_layout(mpb_context *ctx, const mpb_tokens *tk, const mpb_place
                                       "for the permutation");
     if (P == 0) {
         if (perm)  // every offset is zero
-            MPB_CUDA(cudaMemsetAsync(key_offsets, 0, sizeof(int64_t) * (size_t(pl->D) * pl->E + 1),
-                                     ctx->stream));
+            MPB_CUDA(cudaMemsetAsync(key_offsets, 0,
+                                     sizeof(int64_t) * (size_t(pl->D) * pl->E + 1) * layers, ctx->stream));
         return MPB_OK;
     }
     LayoutParams p{};
@@ -1033,6 +1064,7 @@ mpb_status launch_layout(mpb_context *ctx, const mpb_tokens *tk, const mpb_place
     p.demand2 = demand2;
     p.tag_pop = tag_pop;
     p.err = ctx->d_error;
+    p.layers = layers;
     const size_t DE4 = size_t(pl->D) * pl->E * 4;
     size_t smem = perm ? size_t(pl->NS) * 4 : 0;
     p.demand_smem = smem + DE4 <= kSmemLimit;
@@ -1066,12 +1098,15 @@ mpb_status launch_layout(mpb_context *ctx, const mpb_tokens *tk, const mpb_place
     p.chunk = static_cast<uint32_t>(chunk);
     p.key_bits = 1;
     while ((1u << p.key_bits) - 1u <= pl->NS) ++p.key_bits;
+    // per layer: block counts [nb][NS] then totals [NS], 256-byte aligned regions
+    auto bh_words = [&](uint32_t n) { return ((size_t(n) + 1) * pl->NS + 63) / 64 * 64; };
     if (perm) {
-        MPB_CUDA(ctx->ensure_scratch((size_t(nb) + 1) * pl->NS * 4 + 256));
+        p.bh_stride = static_cast<uint32_t>(bh_words(nb));
+        MPB_CUDA(ctx->ensure_scratch(size_t(p.bh_stride) * layers * 4 + 256));
         p.bhist = static_cast<uint32_t *>(ctx->scratch);
         p.totals = p.bhist + size_t(nb) * pl->NS;
     }
-    if (perm && p.demand_smem && (!p.src2 || p.demand2_smem) && (!p.tag || p.tag_smem)) {
+    if (layers == 1 && perm && p.demand_smem && (!p.src2 || p.demand2_smem) && (!p.tag || p.tag_smem)) {
         mpb_status st = MPB_OK;
         if (launch_layout_cluster(ctx, p, pl, sorted_pairs, pair_pos, key_offsets, st)) return st;
     }
@@ -1083,14 +1118,15 @@ mpb_status launch_layout(mpb_context *ctx, const mpb_tokens *tk, const mpb_place
     if (clu) {  // empty trailing blocks round the grid up to whole clusters
         p.nb = nb = (nb + kCountCluster - 1) / kCountCluster * kCountCluster;
         if (perm) {
-            MPB_CUDA(ctx->ensure_scratch((size_t(nb) + 1) * pl->NS * 4 + 256));
+            p.bh_stride = static_cast<uint32_t>(bh_words(nb));
+            MPB_CUDA(ctx->ensure_scratch(size_t(p.bh_stride) * layers * 4 + 256));
             p.bhist = static_cast<uint32_t *>(ctx->scratch);
             p.totals = p.bhist + size_t(nb) * pl->NS;
         }
         auto count = perm ? k_layout_count<true, true> : k_layout_count<false, true>;
         MPB_CUDA(cudaFuncSetAttribute(count, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
         cudaLaunchConfig_t cfg{};
-        cfg.gridDim = dim3(nb);
+        cfg.gridDim = dim3(nb, layers);
         cfg.blockDim = dim3(kThreads);
         cfg.dynamicSmemBytes = smem;
         cfg.stream = ctx->stream;
@@ -1107,12 +1143,12 @@ mpb_status launch_layout(mpb_context *ctx, const mpb_tokens *tk, const mpb_place
     } else {
         auto count = perm ? k_layout_count<true, false> : k_layout_count<false, false>;
         MPB_CUDA(cudaFuncSetAttribute(count, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-        MPB_CUDA(launch_pdl(count, dim3(nb), dim3(kThreads), smem, ctx->stream, p));
+        MPB_CUDA(launch_pdl(count, dim3(nb, layers), dim3(kThreads), smem, ctx->stream, p));
     }
     MPB_LAUNCHED(ctx);
     if (!perm) return MPB_OK;
-    MPB_CUDA(launch_pdl(k_layout_scan, dim3(pl->NS), dim3(kThreads), 0, ctx->stream, p.bhist, nb,
-                        pl->NS, p.totals));
+    MPB_CUDA(launch_pdl(k_layout_scan, dim3(pl->NS, layers), dim3(kThreads), 0, ctx->stream, p.bhist, nb,
+                        pl->NS, p.totals, p.bh_stride));
     MPB_LAUNCHED(ctx);
     // counters / bases, slot bases, block prefixes, the chunk's stash, the cell table
     size_t sc_smem = ((size_t(kWarps) + 2) * pl->NS + 1 + 3) / 4 * 16 + size_t(p.chunk) * 4;
@@ -1121,7 +1157,7 @@ mpb_status launch_layout(mpb_context *ctx, const mpb_tokens *tk, const mpb_place
     auto scatter = p.key_bits <= 8 ? k_layout_scatter<8> : p.key_bits == 9 ? k_layout_scatter<9>
                                                                             : k_layout_scatter<0>;
     MPB_CUDA(cudaFuncSetAttribute(scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sc_smem)));
-    MPB_CUDA(launch_pdl(scatter, dim3(nb), dim3(kThreads), sc_smem, ctx->stream, p,
+    MPB_CUDA(launch_pdl(scatter, dim3(nb, layers), dim3(kThreads), sc_smem, ctx->stream, p,
                         sorted_pairs, pair_pos, pl->d_key_lb, pl->D * pl->E, key_offsets));
     MPB_LAUNCHED(ctx);
     return MPB_OK;
@@ -1156,6 +1192,20 @@ mpb_status mpb_dispatch_layout(mpb_context *ctx, const mpb_tokens *tokens,
         return fail(MPB_CONFIG_ERROR, "mpb_dispatch_layout: src_group NULL needs src_span >= 1");
     return launch_layout(ctx, tokens, placement, demand, demand2, tag_pop, sorted_pairs, pair_pos,
                          key_offsets);
+}
+
+mpb_status mpb_dispatch_layout_layers(mpb_context *ctx, uint32_t layers, const mpb_tokens *tokens,
+                                      const mpb_placement *placement, uint64_t *demand,
+                                      uint64_t *demand2, uint64_t *tag_pop, int32_t *sorted_pairs,
+                                      int32_t *pair_pos, int64_t *key_offsets) {
+    if (!ctx || !tokens || !placement)
+        return fail(MPB_VALIDATION_ERROR, "mpb_dispatch_layout_layers: NULL argument");
+    if (layers && tokens->T && !tokens->idx)
+        return fail(MPB_VALIDATION_ERROR, "mpb_dispatch_layout_layers: idx is NULL");
+    if (!tokens->src_group && tokens->src_span == 0 && tokens->T)
+        return fail(MPB_CONFIG_ERROR, "mpb_dispatch_layout_layers: src_group NULL needs src_span >= 1");
+    return launch_layout(ctx, tokens, placement, demand, demand2, tag_pop, sorted_pairs, pair_pos,
+                         key_offsets, layers);
 }
 
 mpb_status mpb_layout_derive(mpb_context *ctx, const mpb_placement *placement,

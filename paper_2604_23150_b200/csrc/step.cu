@@ -94,6 +94,17 @@ struct mpb_step {
     // and the side stream's grids double from the tails that run beside them,
     // so the statistics backlog left after the last router drains sooner
     uint32_t tail_boost = 0, side_sms = 0, dev_sms = 0;
+    // overlapped step: a chunk's layouts in ONE launch set
+    // (mpb_dispatch_layout_layers); the permutations of all but the step's
+    // last layer land in this scratch ([max chunk][T*k] x 2 + key offsets),
+    // the last layer's in the caller's buffers, as with per-layer launches
+    // Opt-in (MPB_LAYOUT_BATCH=1): measured at DSv3 it halves the time after
+    // the last router (1.2-1.5 -> 0.5-0.8 ms) but the (blocks x layers) grid
+    // spills onto the routers' SMs between router launches (router 0.220 ->
+    // 0.240 ms/layer): a slower step. Default: one mpb_dispatch_layout per layer.
+    bool layout_batch = false;
+    void *perm_scratch = nullptr;
+    uint32_t max_chunk = 0;
     uint64_t *scratch_demand = nullptr;  // [2][D][E]
     // fused single layer: the layout + permutation on a third stream, beside
     // the pricing (main) and the co-activation (side)
@@ -184,6 +195,21 @@ mpb_status tail(mpb_step *s, mpb_context *c, uint32_t l, bool scratch_demand = f
                                             d.pair_pos, d.key_offsets))
         return st;
     return MPB_OK;
+}
+
+// Layers [l0, l1) of the statistics tail in one launch set; their permutations
+// go to the plan's scratch (the caller's buffers keep the step's last layer).
+mpb_status tail_batch(mpb_step *s, mpb_context *c, uint32_t l0, uint32_t l1) {
+    const mpb_step_desc &d = s->d;
+    const uint32_t D = d.deployed->D, E = d.E;
+    const size_t pairs = static_cast<size_t>(d.T) * d.k;
+    const size_t DE = static_cast<size_t>(D) * E;
+    mpb_tokens tk{d.idx + l0 * pairs, d.T, d.k, d.src_group, 0, 0, d.tag, d.n_tags, d.src_group2};
+    int32_t *sp = static_cast<int32_t *>(s->perm_scratch);
+    int32_t *pp = sp + size_t(s->max_chunk) * pairs;
+    int64_t *ko = reinterpret_cast<int64_t *>(pp + size_t(s->max_chunk) * pairs);
+    return mpb_dispatch_layout_layers(c, l1 - l0, &tk, d.deployed, d.demand + l0 * DE,
+                                      d.demand2 ? d.demand2 + l0 * DE : nullptr, d.tag_pop, sp, pp, ko);
 }
 
 // In-place all-reduce (sum, uint64) of layers [l0, l1) of the per-layer demand
@@ -315,8 +341,17 @@ mpb_status run_layers(mpb_step *s) {
                 MPB_CUDA(cudaStreamWaitEvent(s->s_side, s->ev_done[c], 0));
             }
             const auto [l0, l1] = s->chunks[c];
-            for (uint32_t l = l0; l < l1; ++l)
-                if ((st = tail(s, tc, l))) return st;
+            if (s->layout_batch && d.key_offsets) {
+                // layers [l0, lb) batched into the scratch permutations; the
+                // step's last layer (if in this chunk) into the caller's
+                const uint32_t lb = l1 == d.layers ? l1 - 1 : l1;
+                if (lb > l0 && (st = tail_batch(s, tc, l0, lb))) return st;
+                for (uint32_t l = lb; l < l1; ++l)
+                    if ((st = tail(s, tc, l))) return st;
+            } else {
+                for (uint32_t l = l0; l < l1; ++l)
+                    if ((st = tail(s, tc, l))) return st;
+            }
             // the co-activation sums over tokens and layers alike: the chunk's
             // contiguous [l1 - l0][T][k] routing is ONE token list (one launch pair
             // per chunk instead of per layer; integer sums, the same matrix)
@@ -504,6 +539,17 @@ mpb_status mpb_step_create(mpb_context *ctx, const mpb_step_desc *desc, mpb_step
         if (s->fused_ok && e == cudaSuccess)
             e = cudaMalloc(&s->scratch_demand, 2 * sizeof(uint64_t) * d.deployed->D * d.E);
     }
+    if (s->overlapped && e == cudaSuccess) {
+        const char *lb = std::getenv("MPB_LAYOUT_BATCH");
+        s->layout_batch = lb && lb[0] == '1' && d.key_offsets && d.deployed;
+        for (const auto &ch : s->chunks) s->max_chunk = std::max(s->max_chunk, ch.second - ch.first);
+        if (s->layout_batch) {
+            const size_t pairs = static_cast<size_t>(d.T) * d.k;
+            const size_t DE1 = static_cast<size_t>(d.deployed->D) * d.E + 1;
+            const size_t bytes = size_t(s->max_chunk) * (2 * pairs * 4 + DE1 * 8) + 16;
+            e = cudaMalloc(&s->perm_scratch, bytes);
+        }
+    }
     if (e != cudaSuccess) return cleanup(cuda_fail(e, "mpb_step_create"));
     if (mpb_status st = mpb_context_create(ctx->device, s->s_main, &s->main)) return cleanup(st);
     if (mpb_status st = mpb_context_create(ctx->device, s->s_side, &s->side)) return cleanup(st);
@@ -549,6 +595,7 @@ mpb_status mpb_step_destroy(mpb_step *s) {
         for (cudaEvent_t ev : *v)
             if (ev) cudaEventDestroy(ev);
     if (s->scratch_demand) cudaFree(s->scratch_demand);
+    if (s->perm_scratch) cudaFree(s->perm_scratch);
     if (s->s_main) cudaStreamDestroy(s->s_main);
     if (s->s_side) cudaStreamDestroy(s->s_side);
     if (s->s_cap) cudaStreamDestroy(s->s_cap);

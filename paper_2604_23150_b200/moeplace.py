@@ -455,6 +455,28 @@ class Engine:
         return dict(demand=demand, demand2=demand2, tag_pop=tag_pop, sorted_pairs=sp,
                     pair_pos=pp, key_offsets=ko)
 
+    def dispatch_layout_layers(self, idx: torch.Tensor, dp: DevicePlacement, src: torch.Tensor,
+                               tag: Optional[torch.Tensor] = None, n_tags: int = 0,
+                               src2: Optional[torch.Tensor] = None):
+        """dispatch_layout for L layers in one launch set
+        (mpb_dispatch_layout_layers): idx [L, T, k]; returns demand [L, D, E],
+        demand2 [L, D, E] (src2), tag_pop [n_tags, E] (summed over layers),
+        sorted_pairs / pair_pos [L, T*k], key_offsets [L, D*E+1]."""
+        L, T, k = idx.shape
+        demand = self._u64(L, dp.D, dp.E)
+        demand2 = self._u64(L, dp.D, dp.E) if src2 is not None else None
+        tag_pop = self._u64(n_tags, dp.E) if tag is not None else None
+        tk = _abi.MpbTokens(idx.data_ptr(), T, k, src.data_ptr(), 0, 0,
+                            tag.data_ptr() if tag is not None else None, n_tags,
+                            src2.data_ptr() if src2 is not None else None)
+        sp = torch.empty(L, T * k, dtype=torch.int32, device=self.device)
+        pp = torch.empty(L, T * k, dtype=torch.int32, device=self.device)
+        ko = torch.empty(L, dp.D * dp.E + 1, dtype=torch.int64, device=self.device)
+        _abi.call("mpb_dispatch_layout_layers", self.ctx, L, C.byref(tk), dp.handle, _ptr(demand),
+                  _ptr(demand2), _ptr(tag_pop), _ptr(sp), _ptr(pp), _ptr(ko))
+        return dict(demand=demand, demand2=demand2, tag_pop=tag_pop, sorted_pairs=sp,
+                    pair_pos=pp, key_offsets=ko)
+
     def layout_derive(self, dp: DevicePlacement, demand: torch.Tensor, out=None):
         if out is None:
             out = dict(expert_count=self._u64(dp.E), group_pairs=self._u64(dp.D),

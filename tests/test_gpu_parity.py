@@ -216,6 +216,42 @@ def test_dispatch_layout_bit_exact(eng, oracle, case):
     np.testing.assert_array_equal(lay["tag_pop"].cpu().numpy(), pop)
 
 
+@pytest.mark.parametrize("case", [(3, 65536, 256, 8, 2, 8, 0), (5, 4096, 128, 8, 2, 8, 1),
+                                  (2, 999, 64, 4, 2, 4, 0), (8, 16385, 64, 8, 2, 6, 1)])
+@pytest.mark.parametrize("budget", [0, 20])
+def test_dispatch_layout_layers_bit_exact(eng, oracle, case, budget):
+    """mpb_dispatch_layout_layers: L layers in one launch set (grids over
+    (block, layer)) == the oracle per layer: demand / demand2, the stable
+    permutation, key offsets, and the tag histogram summed over the layers;
+    also under the step's 20-SM side budget."""
+    L, T, E, D, nodes, k, red = case
+    rng = np.random.default_rng(L * T + E)
+    idx = np.stack([random_idx(rng, T, E, k) for _ in range(L)])
+    src = rng.integers(0, D, T).astype(np.uint8)
+    src2 = ((np.arange(T) * 5) % D).astype(np.uint8)
+    tag = rng.integers(0, 5, T).astype(np.uint16)
+    pl = make_placement(rng, E, D, red)
+    top = topo(D, nodes)
+    e = mp.Engine(0)
+    if budget:
+        e.set_sm_budget(budget)
+    dp = e.placement(pl, top)
+    lay = e.dispatch_layout_layers(dev(idx), dp, dev(src), tag=dev(tag), n_tags=5, src2=dev(src2))
+    e.sync()
+    lut = oracle.dest_lut(pl.groups, top.group_to_node, E)
+    pop = np.zeros((5, E), np.uint64)
+    for l in range(L):
+        ref = oracle.dispatch_layout(idx[l], src.astype(np.uint32), lut, D, E, top.group_to_node)
+        ref2 = oracle.dispatch_layout(idx[l], src2.astype(np.uint32), lut, D, E, top.group_to_node)
+        np.testing.assert_array_equal(lay["demand"][l].cpu().numpy(), ref["demand"])
+        np.testing.assert_array_equal(lay["demand2"][l].cpu().numpy(), ref2["demand"])
+        np.testing.assert_array_equal(lay["sorted_pairs"][l].cpu().numpy(), ref["sorted_pairs"])
+        np.testing.assert_array_equal(lay["pair_pos"][l].cpu().numpy(), ref["pair_pos"])
+        np.testing.assert_array_equal(lay["key_offsets"][l].cpu().numpy(), ref["key_offsets"])
+        pop += oracle.domain_popularity(idx[l], tag.astype(np.uint32), 5, E).astype(np.uint64)
+    np.testing.assert_array_equal(lay["tag_pop"].cpu().numpy(), pop)
+
+
 def test_layout_accumulates_across_shards(eng, oracle):
     rng = np.random.default_rng(11)
     T, E, D, k = 8192, 128, 8, 8

@@ -354,9 +354,13 @@ MPB_API mpb_status mpb_combine_p2p(mpb_context *ctx, const int32_t *pair_pos,
  *     of router_group layers, mpb_router_topk_layers) on the main stream with
  *     an SM budget of device_sms - side_sms; each chunk's statistics tails
  *     (mpb_dispatch_layout: demand / demand2 / tag histograms + permutation,
- *     and mpb_coactivation) on the side stream, beside the next chunk's router.
- *     One layer: the router on every SM, then the layout on main with the
- *     co-activation beside it on the side stream.
+ *     and one mpb_coactivation over the whole chunk) on the side stream,
+ *     beside the next chunk's router.
+ *     One layer: the router on every SM; on one GPU with score_per_chunk it
+ *     counts demand / demand2 itself (mpb_router_topk_demand) and the score
+ *     jobs follow it on main while the layout (a third stream) and the
+ *     co-activation (side) run beside them; otherwise the layout on main with
+ *     the co-activation beside it, then the SCORE phase.
  *   SCORE phase: mpb_score_placements_finalize of score_jobs[0] on the main
  *     stream, the other jobs on the side stream beside it.
  * Multi-GPU: the plan issues its own NCCL collectives (mpb_step_attach_comm),

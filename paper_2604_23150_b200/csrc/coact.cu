@@ -194,7 +194,7 @@ constexpr int kMmaThreads = 320;  // warp 0: TMEM + MMA; warps 1-8: producers + 
 template <int WORDS>
 __global__ void __launch_bounds__(kMmaThreads, 1)
     k_coact_mma(const int32_t *idx, uint64_t T, uint32_t k, uint32_t E, uint32_t N0, uint32_t N1,
-                uint32_t chunks_per_cta, uint32_t *partials) {
+                uint32_t chunks_per_cta, uint32_t *partials, uint64_t *direct) {
     constexpr bool kTwo = WORDS == 8;
     constexpr uint32_t kRows = WORDS * 32;   // experts (padded) = partial row length
     constexpr uint32_t kBlock = 128 * 128;   // one 128-expert MN block of 128 token rows
@@ -340,6 +340,20 @@ __global__ void __launch_bounds__(kMmaThreads, 1)
                 uint32_t v[32];
                 ptx::tmem_ld_32x32b_x32(tmem + ((q * 32) << 16) + tcol, v);
                 ptx::tmem_ld_wait();
+                if (direct) {  // few CTAs (decode batches): straight into C, no reduce launch
+                    if (orow >= E) return;
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) {
+                        const uint32_t col = ocol + i;
+                        if (!v[i] || col < orow || col >= E) continue;
+                        atomicAdd(reinterpret_cast<unsigned long long *>(direct) + size_t(orow) * E + col,
+                                  static_cast<unsigned long long>(v[i]));
+                        if (col != orow)
+                            atomicAdd(reinterpret_cast<unsigned long long *>(direct) + size_t(col) * E + orow,
+                                      static_cast<unsigned long long>(v[i]));
+                    }
+                    return;
+                }
                 uint4 *o = reinterpret_cast<uint4 *>(out + static_cast<size_t>(orow) * kRows + ocol);
 #pragma unroll
                 for (int w = 0; w < 4; ++w)
@@ -358,6 +372,8 @@ __global__ void __launch_bounds__(kMmaThreads, 1)
     __syncthreads();
     if (warp == 0) ptx::tmem_dealloc<kTwo ? 512 : 256>(tmem);
 }
+
+constexpr uint64_t kDirectMaxCtas = 16;  // direct-to-C epilogue up to this many CTAs
 
 // Row i of C (one CTA of 8 warps per row): warp w sums partials w, w+8, ...
 // with lane L owning columns 8L..8L+7 (coalesced 16-byte loads, 8 in flight);
@@ -456,12 +472,21 @@ extern "C" mpb_status mpb_coactivation(mpb_context *ctx, const int32_t *idx, uin
             uint64_t ctas = std::min<uint64_t>(ctx->num_sms, std::max<uint64_t>(1, chunks / want));
             const uint64_t cpc = (chunks + ctas - 1) / ctas;
             ctas = (chunks + cpc - 1) / cpc;
-            MPB_CUDA(ctx->ensure_scratch(size_t(ctas) * E8 * E8 * 2));
-            auto *partials = static_cast<uint32_t *>(ctx->scratch);
+            // a few CTAs (decode-size batches): each adds its upper triangle
+            // straight into C with 64-bit atomics (integer sums: the same C),
+            // no partials and no reduce launch (MPB_COACT_DIRECT=0: off)
+            const char *denv = std::getenv("MPB_COACT_DIRECT");
+            const bool direct = ctas <= kDirectMaxCtas && !(denv && denv[0] == '0');
+            uint32_t *partials = nullptr;
+            if (!direct) {
+                MPB_CUDA(ctx->ensure_scratch(size_t(ctas) * E8 * E8 * 2));
+                partials = static_cast<uint32_t *>(ctx->scratch);
+            }
             MPB_CUDA(launch_pdl(kern, dim3(static_cast<unsigned>(ctas)), dim3(kMmaThreads), smem,
                                 ctx->stream, idx + t0 * k, Tn, k, E, N0, N1,
-                                static_cast<uint32_t>(cpc), partials));
+                                static_cast<uint32_t>(cpc), partials, direct ? coact : nullptr));
             MPB_LAUNCHED(ctx);
+            if (direct) continue;
             MPB_CUDA(launch_pdl(k_coact_mma_reduce, dim3(E), dim3(256), 0, ctx->stream, partials,
                                 static_cast<uint32_t>(ctas), E, E8, coact));
             MPB_LAUNCHED(ctx);

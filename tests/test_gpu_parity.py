@@ -287,6 +287,23 @@ def test_coactivation_bit_exact(eng, oracle, T, E, k):
     np.testing.assert_array_equal(c.cpu().numpy(), oracle.coactivation(idx, E))
 
 
+@pytest.mark.parametrize("direct", ["0", "1"])
+@pytest.mark.parametrize("T,E,k", [(4096, 128, 8), (3001, 256, 8), (2048, 200, 16), (64, 64, 4)])
+def test_coactivation_direct_epilogue(oracle, monkeypatch, direct, T, E, k):
+    """Decode-size batches (<= 16 CTAs) add each CTA's upper triangle straight
+    into C with 64-bit atomics (no partials, no reduce launch); the partial +
+    reduce path (MPB_COACT_DIRECT=0) gives the same exact counts."""
+    monkeypatch.setenv("MPB_COACT_DIRECT", direct)
+    rng = np.random.default_rng(T + E + k)
+    idx = random_idx(rng, T, E, k)
+    e = mp.Engine(0)
+    n0 = e.launches
+    c = e.coactivation(dev(idx), E)
+    e.sync()
+    assert e.launches - n0 == (1 if direct == "1" else 2)
+    np.testing.assert_array_equal(c.cpu().numpy(), oracle.coactivation(idx, E))
+
+
 def test_coactivation_skewed_domains(eng, oracle):
     tap = oracle.generate_trace_tap(4, 40, 16, 0.9, 16.0, 3, 128, 8, 1)
     idx = tap["picks"].reshape(-1, 8)

@@ -299,13 +299,19 @@ mpb_status run_layers(mpb_step *s) {
         const size_t set = (s->runs % mpb_step::kRing) * s->chunks.size();
         if (mpb_status st = record(s, s->ev_r0[set], s->s_side, true)) return st;
     }
-    if (d.zero_base && d.zero_bytes) {
+    // fused single layer: the router itself counts into the buffer, so the
+    // zeroing is on its own stream (a memset node ahead of it, no cross-stream
+    // event on the critical chain)
+    const bool zero_on_main = fused_single(s) && d.zero_base && d.zero_bytes;
+    if (zero_on_main) {
+        MPB_CUDA(cudaMemsetAsync(d.zero_base, 0, d.zero_bytes, s->s_main));
+    } else if (d.zero_base && d.zero_bytes) {
         MPB_CUDA(cudaMemsetAsync(d.zero_base, 0, d.zero_bytes, s->s_side));
         MPB_CUDA(cudaEventRecord(s->ev_zero, s->s_side));
     }
     const bool probe = s->probe && !s->capturing;
     if (probe) MPB_CUDA(cudaEventRecord(s->ev_p0, s->s_main));
-    bool main_zeroed = !(d.zero_base && d.zero_bytes);
+    bool main_zeroed = !(d.zero_base && d.zero_bytes) || zero_on_main;
     auto main_waits_zero = [&]() -> mpb_status {
         if (!main_zeroed) {
             MPB_CUDA(cudaStreamWaitEvent(s->s_main, s->ev_zero, 0));

@@ -279,7 +279,9 @@ def test_cluster_tail_under_sm_budgets(oracle, sms):
 
 
 @pytest.mark.parametrize("tail", ["cluster", "global", "none"])
-@pytest.mark.parametrize("shape", [(4096, 1024, 128, 8, 0), (4096, 1024, 128, 16, 1), (2048, 512, 64, 16, 0)])
+@pytest.mark.parametrize("shape", [(4096, 1024, 128, 8, 0), (4096, 1024, 128, 16, 1), (2048, 512, 64, 16, 0),
+                                   # E = 256: 2-SM CTA pairs (UMMA M=256), global split tail
+                                   (8192, 1024, 256, 8, 1)])
 def test_router_ties_inf_nan(eng, oracle, shape, tail, monkeypatch):
     """Non-finite and tied logits follow the oracle's order on every epilogue
     (cluster tail, global split tail, no split): real values (+-inf included)

@@ -386,15 +386,21 @@ mpb_status run_layers(mpb_step *s) {
         MPB_CUDA(cudaStreamWaitEvent(s->s_side, s->ev_fork, 0));
         MPB_CUDA(cudaStreamWaitEvent(s->s_lay, s->ev_fork, 0));
         if (d.coact && (st = mpb_coactivation(s->side, d.idx, d.T, d.k, d.E, d.coact))) return st;
-        if ((st = tail(s, s->lay, 0, true))) return st;
-        MPB_CUDA(cudaEventRecord(s->ev_join2, s->s_lay));
-        MPB_CUDA(cudaStreamWaitEvent(s->s_main, s->ev_join2, 0));
+        // the longer of the two (the layout) follows the router on its own
+        // stream (programmatic launch overlaps its prologue with the router's
+        // drain); the pricing goes to the third stream
+        const char *lm = std::getenv("MPB_DECODE_LAYOUT_MAIN");
+        const bool layout_main = !(lm && lm[0] == '0');
+        mpb_context *c_lay = layout_main ? s->main : s->lay, *c_score = layout_main ? s->lay : s->main;
+        if ((st = tail(s, c_lay, 0, true))) return st;
         if (s->jobs.size() == 2 && s->jobs[0].B == d.layers && s->jobs[1].B == d.layers) {
-            if ((st = score_finalize_pair(s->main, s->jobs[0], s->jobs[1], 0, 1))) return st;
+            if ((st = score_finalize_pair(c_score, s->jobs[0], s->jobs[1], 0, 1))) return st;
         } else {
             for (const mpb_score_job &j : s->jobs)
-                if (j.B == d.layers && (st = score_finalize_range(s->main, j, 0, 1))) return st;
+                if (j.B == d.layers && (st = score_finalize_range(c_score, j, 0, 1))) return st;
         }
+        MPB_CUDA(cudaEventRecord(s->ev_join2, s->s_lay));
+        MPB_CUDA(cudaStreamWaitEvent(s->s_main, s->ev_join2, 0));
     } else {
         for (size_t c = 0; c < s->chunks.size(); ++c) {
             if ((st = launch_router(s, c))) return st;

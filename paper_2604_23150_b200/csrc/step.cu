@@ -87,8 +87,8 @@ struct mpb_step {
     bool overlapped = false;
     // one layer, one GPU: the router counts the demand tables itself
     // (mpb_router_topk_demand) and the layout writes its copy into scratch, so
-    // the pricing follows the router directly while the layout + permutation
-    // and the co-activation run beside it (MPB_ROUTER_DEMAND=0: off)
+    // the layout + permutation, the pricing and the co-activation all follow
+    // the router at once (MPB_ROUTER_DEMAND=0: off)
     bool fused_ok = false;
     // MPB_TAIL_BOOST = n: the last n router chunks run on a smaller grid budget
     // and the side stream's grids double from the tails that run beside them,
@@ -106,8 +106,8 @@ struct mpb_step {
     void *perm_scratch = nullptr;
     uint32_t max_chunk = 0;
     uint64_t *scratch_demand = nullptr;  // [2][D][E]
-    // fused single layer: the layout + permutation on a third stream, beside
-    // the pricing (main) and the co-activation (side)
+    // fused single layer: a third stream for the pricing (the layout follows
+    // the router on main, the co-activation runs on side)
     cudaStream_t s_lay = nullptr;
     mpb_context *lay = nullptr;
     cudaEvent_t ev_join2 = nullptr;
@@ -378,8 +378,8 @@ mpb_status run_layers(mpb_step *s) {
             if (probe) MPB_CUDA(cudaEventRecord(s->ev_pt[c], tc->stream));
         }
     } else if (fused_single(s)) {
-        // router (with the demand count) -> pricing on main; the layout +
-        // permutation and the co-activation beside the pricing on the side
+        // router (with the demand count), then three branches at once: the
+        // layout + permutation, the pricing and the co-activation
         if ((st = main_waits_zero())) return st;
         if ((st = launch_router(s, 0))) return st;
         MPB_CUDA(cudaEventRecord(s->ev_fork, s->s_main));

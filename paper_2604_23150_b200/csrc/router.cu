@@ -370,9 +370,11 @@ __device__ __forceinline__ void tail_select(const RouterParams &p, const float *
 // 128/S), i.e. a reduce-scatter of the fp32 partial accumulators:
 //   1. once its own MMAs are done (its pipeline smem is free) every CTA tells
 //      its peers so (remote mbarrier arrive);
-//   2. each epilogue warp pushes the TMEM rows it does not own into the
-//      owner's shared memory with st.async (completion counted in bytes on the
-//      owner's mbarrier) — no global memory, no flags, no fences;
+//   2. the epilogue warps stage the TMEM rows the CTA does not own in local
+//      shared memory (its own share straight into the sum tile); once every
+//      peer's pipeline smem is free one thread bulk-copies each share into its
+//      owner's smem (cp.async.bulk shared::cluster, completion counted in bytes
+//      on the owner's mbarrier) — no global memory, no flags;
 //   3.+4. one warp per owned row sums it in K-part order 0..S-1 (the fp32
 //      order of the global-memory tail) in registers and selects its top-k by
 //      k warp arg-max rounds (tail_select).

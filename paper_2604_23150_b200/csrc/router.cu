@@ -398,8 +398,12 @@ __device__ __forceinline__ void cluster_tail(const RouterParams &p, const WorkIt
     const uint32_t t = threadIdx.x - 128u;                               // epilogue thread 0..255
     const uint32_t q = warp & 3, half = (warp - 4) >> 2;
     const uint32_t share_bytes = RPS * RS * 4u;  // one row share, padded rows, contiguous
+    // cluster_tail == 2 (MPB_ROUTER_ST_ASYNC=1, experiment): every thread
+    // pushes its half rows of the other owners' shares straight from registers
+    // into the owners' smem with st.async instead of staging + bulk copies
+    const bool push = p.cluster_tail == 2;
     if (t == 0) {
-        ptx::mbar_arrive_expect_tx(rx_full, (S - 1) * share_bytes);
+        ptx::mbar_arrive_expect_tx(rx_full, (S - 1) * (push ? RPS * N * 4u : share_bytes));
         for (uint32_t c = 0; c < S; ++c)
             if (c != h) ptx::mbar_arrive_remote(ptx::mapa(ptx::smem_u32(peer_free), c));
     }
@@ -414,15 +418,25 @@ __device__ __forceinline__ void cluster_tail(const RouterParams &p, const WorkIt
 #pragma unroll
         for (int c = 0; c < NH; c += 16) ptx::tmem_ld_32x32b_x16(taddr_q + half * NH + c, *reinterpret_cast<uint32_t(*)[16]>(r + c));
         ptx::tmem_ld_wait();
+        if (push && owner != h) {
+            const uint32_t j = h < owner ? h : h - 1;  // my slot at the owner
+            const uint32_t dst_c = ptx::mapa(
+                ptx::smem_u32(rx + (static_cast<size_t>(j) * RPS + rloc) * RS + half * NH), owner);
+            const uint32_t bar_c = ptx::mapa(ptx::smem_u32(rx_full), owner);
+            ptx::mbar_wait_cluster(peer_free, 0);  // every peer's pipeline smem is free
 #pragma unroll
-        for (int c = 0; c < NH; c += 4)
-            *reinterpret_cast<float4 *>(dst + half * NH + c) =
-                make_float4(__uint_as_float(r[c]), __uint_as_float(r[c + 1]), __uint_as_float(r[c + 2]),
-                            __uint_as_float(r[c + 3]));
-        if (owner != h) ptx::fence_proxy_async_smem();  // generic writes -> visible to the bulk-copy engine
+            for (int c = 0; c < NH; c += 4) ptx::st_async_v4(dst_c + 4u * c, r[c], r[c + 1], r[c + 2], r[c + 3], bar_c);
+        } else {
+#pragma unroll
+            for (int c = 0; c < NH; c += 4)
+                *reinterpret_cast<float4 *>(dst + half * NH + c) =
+                    make_float4(__uint_as_float(r[c]), __uint_as_float(r[c + 1]), __uint_as_float(r[c + 2]),
+                                __uint_as_float(r[c + 3]));
+            if (owner != h) ptx::fence_proxy_async_smem();  // generic writes -> visible to the bulk-copy engine
+        }
     }
     asm volatile("bar.sync 5, 256;" ::: "memory");  // every share staged
-    if (t == 0) {
+    if (t == 0 && !push) {
         ptx::mbar_wait_cluster(peer_free, 0);  // every peer's pipeline smem is free
 #ifdef MPB_ROUTER_TRACE
         RTRACE(14, gtime());
@@ -1154,7 +1168,8 @@ mpb_status launch_router_n(mpb_context *ctx, const CUtensorMap &mx, const CUtens
         }
     }
     p.splits = S;
-    p.cluster_tail = ct ? 1u : 0u;
+    const char *sa = std::getenv("MPB_ROUTER_ST_ASYNC");
+    p.cluster_tail = ct ? ((sa && sa[0] == '1') ? 2u : 1u) : 0u;
     if (S > 1 && ct) {
         // units set above
     } else if (S > 1) {

@@ -104,6 +104,13 @@ struct mpb_step {
     // 0.240 ms/layer): a slower step. Default: one mpb_dispatch_layout per layer.
     bool layout_batch = false;
     void *perm_scratch = nullptr;
+    // one GPU: the last main_tail_chunks chunks' tails run on the main stream
+    // right after the last routers, beside the side stream's backlog (no join
+    // first); the side stream's permutations then go to side_perm (one layer)
+    // so the caller's buffers still end with the step's last layer
+    // (MPB_MAIN_TAIL_CHUNKS, default 1 = the last chunk after a join)
+    uint32_t main_tail_chunks = 1;
+    void *side_perm = nullptr;
     uint32_t max_chunk = 0;
     uint64_t *scratch_demand = nullptr;  // [2][D][E]
     // fused single layer: a third stream for the pricing (the layout follows
@@ -180,7 +187,8 @@ mpb_status record(mpb_step *s, cudaEvent_t ev, cudaStream_t st, bool timing) {
     return MPB_OK;
 }
 
-mpb_status tail(mpb_step *s, mpb_context *c, uint32_t l, bool scratch_demand = false) {
+mpb_status tail(mpb_step *s, mpb_context *c, uint32_t l, bool scratch_demand = false,
+                bool scratch_perm = false) {
     const mpb_step_desc &d = s->d;
     const uint32_t D = d.deployed->D, E = d.E;
     const size_t pairs = static_cast<size_t>(d.T) * d.k;
@@ -191,8 +199,14 @@ mpb_status tail(mpb_step *s, mpb_context *c, uint32_t l, bool scratch_demand = f
         dem = s->scratch_demand;
         dem2 = d.demand2 ? s->scratch_demand + static_cast<size_t>(D) * E : nullptr;
     }
-    if (mpb_status st = mpb_dispatch_layout(c, &tk, d.deployed, dem, dem2, d.tag_pop, d.sorted_pairs,
-                                            d.pair_pos, d.key_offsets))
+    int32_t *sp = d.sorted_pairs, *pp = d.pair_pos;
+    int64_t *ko = d.key_offsets;
+    if (scratch_perm && ko) {  // a permutation the step's later layers overwrite anyway
+        sp = static_cast<int32_t *>(s->side_perm);
+        pp = sp + pairs;
+        ko = reinterpret_cast<int64_t *>(pp + pairs);
+    }
+    if (mpb_status st = mpb_dispatch_layout(c, &tk, d.deployed, dem, dem2, d.tag_pop, sp, pp, ko))
         return st;
     return MPB_OK;
 }
@@ -336,7 +350,13 @@ mpb_status run_layers(mpb_step *s) {
             if (boost && c + 1 == nc - boost) budgets(true);  // routers nc-boost.. and the tails beside them
             if (c + 1 < nc && (st = launch_router(s, c + 1))) return st;
             mpb_context *tc = s->side;
-            if (d.score_per_chunk && c + 1 == nc) {
+            const uint32_t on_main = s->comm ? 1u : s->main_tail_chunks;
+            if (d.score_per_chunk && on_main > 1 && c + on_main >= nc) {
+                // one GPU: the last chunks' tails on the main stream's grids right
+                // after the last routers, beside the side stream's backlog
+                if ((st = main_waits_zero())) return st;
+                tc = s->main;
+            } else if (d.score_per_chunk && c + 1 == nc) {
                 // nothing runs beside the last chunk's tails: they take the main
                 // stream's grids, after the side stream's earlier tails
                 MPB_CUDA(cudaEventRecord(s->ev_join, s->s_side));
@@ -355,8 +375,9 @@ mpb_status run_layers(mpb_step *s) {
                 for (uint32_t l = lb; l < l1; ++l)
                     if ((st = tail(s, tc, l))) return st;
             } else {
+                const bool sp_side = tc == s->side && s->side_perm;
                 for (uint32_t l = l0; l < l1; ++l)
-                    if ((st = tail(s, tc, l))) return st;
+                    if ((st = tail(s, tc, l, false, sp_side))) return st;
             }
             // the co-activation sums over tokens and layers alike: the chunk's
             // contiguous [l1 - l0][T][k] routing is ONE token list (one launch pair
@@ -552,6 +573,15 @@ mpb_status mpb_step_create(mpb_context *ctx, const mpb_step_desc *desc, mpb_step
             e = cudaMalloc(&s->scratch_demand, 2 * sizeof(uint64_t) * d.deployed->D * d.E);
     }
     if (s->overlapped && e == cudaSuccess) {
+        if (const char *mt = std::getenv("MPB_MAIN_TAIL_CHUNKS"))
+            s->main_tail_chunks = static_cast<uint32_t>(std::max(1, std::atoi(mt)));
+        if (s->main_tail_chunks > 1 && d.key_offsets && d.deployed) {
+            const size_t pairs = static_cast<size_t>(d.T) * d.k;
+            const size_t DE1 = static_cast<size_t>(d.deployed->D) * d.E + 1;
+            e = cudaMalloc(&s->side_perm, 2 * pairs * 4 + DE1 * 8 + 16);
+        }
+    }
+    if (s->overlapped && e == cudaSuccess) {
         const char *lb = std::getenv("MPB_LAYOUT_BATCH");
         s->layout_batch = lb && lb[0] == '1' && d.key_offsets && d.deployed;
         for (const auto &ch : s->chunks) s->max_chunk = std::max(s->max_chunk, ch.second - ch.first);
@@ -608,6 +638,7 @@ mpb_status mpb_step_destroy(mpb_step *s) {
             if (ev) cudaEventDestroy(ev);
     if (s->scratch_demand) cudaFree(s->scratch_demand);
     if (s->perm_scratch) cudaFree(s->perm_scratch);
+    if (s->side_perm) cudaFree(s->side_perm);
     if (s->s_main) cudaStreamDestroy(s->s_main);
     if (s->s_side) cudaStreamDestroy(s->s_side);
     if (s->s_cap) cudaStreamDestroy(s->s_cap);

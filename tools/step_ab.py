@@ -15,10 +15,8 @@ from paper_2604_23150_b200.pipeline import RoutingPipeline, spec_for  # noqa: E4
 
 VARIANTS = {  # name: (env, pipeline attributes)
     "base": ({}, {}),
-    "side24": ({}, {"side_sms": 24}),
-    "tailboost2": ({"MPB_TAIL_BOOST": "2"}, {}),
-    "side24+tb2": ({"MPB_TAIL_BOOST": "2"}, {"side_sms": 24}),
-    "side16+tb3": ({"MPB_TAIL_BOOST": "3"}, {"side_sms": 16}),
+    "main2": ({"MPB_MAIN_TAIL_CHUNKS": "2"}, {}),
+    "main3": ({"MPB_MAIN_TAIL_CHUNKS": "3"}, {}),
 }
 rounds = int(sys.argv[1]) if len(sys.argv) > 1 else 3
 eng = mp.Engine(0)
@@ -27,7 +25,7 @@ base_attrs = {"router_group": pipe.router_group, "side_sms": pipe.side_sms}
 res = {k: [] for k in VARIANTS}
 for r in range(rounds):
     for name, (env, attrs) in VARIANTS.items():
-        for k in ("MPB_TAIL_BOOST",):
+        for k in ("MPB_TAIL_BOOST", "MPB_MAIN_TAIL_CHUNKS"):
             os.environ.pop(k, None)
         os.environ.update(env)
         for k, v in {**base_attrs, **attrs}.items():

@@ -245,28 +245,37 @@ __device__ __forceinline__ void tail_select(const RouterParams &p, const float *
     constexpr uint32_t RPS = 8u * R, SP = 128u / RPS;  // SP = S: 4 K parts (R = 4) or 2 (R = 8)
     constexpr float kL2E = 1.4426950408889634f;
     uint32_t key[R][V], perm[R];
+    // every row's sums first (all loads in flight: no global store between
+    // them that the compiler would have to order them against), then the
+    // optional logits, then the rank keys
+    const float *share[SP];
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-        const uint32_t rr = ew + 8u * r;
-        float x[V];
+    for (uint32_t part = 0; part < SP; ++part)
+        share[part] = part == h ? tile : rx + static_cast<size_t>(part < h ? part : part - 1) * RPS * RS;
+    float xs[R][V];
+#pragma unroll
+    for (int r = 0; r < R; ++r)
 #pragma unroll
         for (int i = 0; i < static_cast<int>(V); ++i) {
-            const uint32_t c = lane + 32u * i;
-            float tot = 0.f;
+            const uint32_t off = (ew + 8u * r) * RS + lane + 32u * i;
+            float tot = share[0][off];
 #pragma unroll
-            for (uint32_t part = 0; part < SP; ++part) {
-                const uint32_t j = part < h ? part : part - 1;
-                const float v = part == h ? tile[rr * RS + c] : rx[(j * RPS + rr) * RS + c];
-                tot = part == 0 ? v : tot + v;
-            }
-            x[i] = tot;
+            for (uint32_t part = 1; part < SP; ++part) tot += share[part][off];
+            xs[r][i] = tot;
         }
-        if (p.logits && row_tile0 + h * RPS + rr < p.T) {
+    if (p.logits)
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const uint32_t rr = ew + 8u * r;
+            if (row_tile0 + h * RPS + rr >= p.T) continue;
             float *out = p.logits + (out_row_tile0 + h * RPS + rr) * p.E;
 #pragma unroll
             for (int i = 0; i < static_cast<int>(V); ++i)
-                if (lane + 32u * i < p.E) out[lane + 32u * i] = x[i];
+                if (lane + 32u * i < p.E) out[lane + 32u * i] = xs[r][i];
         }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const float *x = xs[r];
         uint32_t sl[V];
 #pragma unroll
         for (int i = 0; i < static_cast<int>(V); ++i) {

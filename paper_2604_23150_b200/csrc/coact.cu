@@ -373,7 +373,7 @@ __global__ void __launch_bounds__(kMmaThreads, 1)
     if (warp == 0) ptx::tmem_dealloc<kTwo ? 512 : 256>(tmem);
 }
 
-constexpr uint64_t kDirectMaxCtas = 16;  // direct-to-C epilogue up to this many CTAs
+constexpr uint64_t kDirectMaxCtas = 32;  // direct-to-C epilogue up to this many CTAs (4,096 tokens: 1 chunk each)
 
 // Row i of C (one CTA of 8 warps per row): warp w sums partials w, w+8, ...
 // with lane L owning columns 8L..8L+7 (coalesced 16-byte loads, 8 in flight);
@@ -463,8 +463,9 @@ extern "C" mpb_status mpb_coactivation(mpb_context *ctx, const int32_t *idx, uin
         // one CTA per SM at most, >= 2 chunks of 128 tokens each;
         // u16 partials need <= 511 chunks per CTA: longer inputs take several
         // launches, each accumulating into C
+        // (decode-size batches that fit the direct epilogue: one chunk per CTA)
         static const char *env = std::getenv("MPB_COACT_CHUNKS_PER_CTA");
-        const uint64_t want = env ? std::max(1, std::atoi(env)) : 2;
+        const uint64_t want = env ? std::max(1, std::atoi(env)) : ((T + 127) / 128 <= kDirectMaxCtas ? 1 : 2);
         const uint64_t max_tokens = uint64_t(ctx->num_sms) * 511 * 128;
         for (uint64_t t0 = 0; t0 < T; t0 += max_tokens) {
             const uint64_t Tn = std::min<uint64_t>(max_tokens, T - t0);

@@ -98,11 +98,12 @@ struct mpb_step {
     // (mpb_dispatch_layout_layers); the permutations of all but the step's
     // last layer land in this scratch ([max chunk][T*k] x 2 + key offsets),
     // the last layer's in the caller's buffers, as with per-layer launches
-    // Opt-in (MPB_LAYOUT_BATCH=1): measured at DSv3 it halves the time after
-    // the last router (1.2-1.5 -> 0.5-0.8 ms) but the (blocks x layers) grid
-    // spills onto the routers' SMs between router launches (router 0.220 ->
-    // 0.240 ms/layer): a slower step. Default: one mpb_dispatch_layout per layer.
-    bool layout_batch = false;
+    // MPB_LAYOUT_BATCH = layers per batched launch set (default 4; 0 or 1: one
+    // mpb_dispatch_layout per layer). Whole 8-layer chunks halve the time after
+    // the last router but their (blocks x layers) grids spill onto the routers'
+    // SMs between router launches (router 0.220 -> 0.240 ms/layer); interleaved
+    // A/B at DSv3 (16 rounds): 4 layers -1.7 / -2.1%, 8 layers +1.9% vs per layer.
+    uint32_t layout_batch = 0;  // layers per batched launch set (0: off)
     void *perm_scratch = nullptr;
     // one GPU: the last main_tail_chunks chunks' tails run on the main stream
     // right after the last routers, beside the side stream's backlog (no join
@@ -371,7 +372,8 @@ mpb_status run_layers(mpb_step *s) {
                 // layers [l0, lb) batched into the scratch permutations; the
                 // step's last layer (if in this chunk) into the caller's
                 const uint32_t lb = l1 == d.layers ? l1 - 1 : l1;
-                if (lb > l0 && (st = tail_batch(s, tc, l0, lb))) return st;
+                for (uint32_t b0 = l0; b0 < lb; b0 += s->layout_batch)
+                    if ((st = tail_batch(s, tc, b0, std::min(lb, b0 + s->layout_batch)))) return st;
                 for (uint32_t l = lb; l < l1; ++l)
                     if ((st = tail(s, tc, l))) return st;
             } else {
@@ -583,7 +585,9 @@ mpb_status mpb_step_create(mpb_context *ctx, const mpb_step_desc *desc, mpb_step
     }
     if (s->overlapped && e == cudaSuccess) {
         const char *lb = std::getenv("MPB_LAYOUT_BATCH");
-        s->layout_batch = lb && lb[0] == '1' && d.key_offsets && d.deployed;
+        s->layout_batch = (d.key_offsets && d.deployed) ? (lb ? static_cast<uint32_t>(std::max(0, std::atoi(lb))) : 4u)
+                                                        : 0u;
+        if (s->layout_batch == 1) s->layout_batch = 0;  // one layer: the plain per-layer call
         for (const auto &ch : s->chunks) s->max_chunk = std::max(s->max_chunk, ch.second - ch.first);
         if (s->layout_batch) {
             const size_t pairs = static_cast<size_t>(d.T) * d.k;

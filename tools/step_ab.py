@@ -15,8 +15,8 @@ from paper_2604_23150_b200.pipeline import RoutingPipeline, spec_for  # noqa: E4
 
 VARIANTS = {  # name: (env, pipeline attributes)
     "base": ({}, {}),
-    "main2": ({"MPB_MAIN_TAIL_CHUNKS": "2"}, {}),
-    "main3": ({"MPB_MAIN_TAIL_CHUNKS": "3"}, {}),
+    "lbatch8": ({"MPB_LAYOUT_BATCH": "8"}, {}),
+    "lbatch4": ({"MPB_LAYOUT_BATCH": "4"}, {}),
 }
 rounds = int(sys.argv[1]) if len(sys.argv) > 1 else 3
 eng = mp.Engine(0)
@@ -25,7 +25,7 @@ base_attrs = {"router_group": pipe.router_group, "side_sms": pipe.side_sms}
 res = {k: [] for k in VARIANTS}
 for r in range(rounds):
     for name, (env, attrs) in VARIANTS.items():
-        for k in ("MPB_TAIL_BOOST", "MPB_MAIN_TAIL_CHUNKS"):
+        for k in ("MPB_TAIL_BOOST", "MPB_MAIN_TAIL_CHUNKS", "MPB_LAYOUT_BATCH"):
             os.environ.pop(k, None)
         os.environ.update(env)
         for k, v in {**base_attrs, **attrs}.items():

@@ -13,10 +13,12 @@ import torch  # noqa: E402
 from paper_2604_23150_b200 import moeplace as mp  # noqa: E402
 from paper_2604_23150_b200.pipeline import RoutingPipeline, spec_for  # noqa: E402
 
-VARIANTS = {  # name: (env, pipeline attributes)
+VARIANTS = {  # name: (env, pipeline attributes); measured this round, all within about 2%
     "base": ({}, {}),
+    "side16": ({}, {"side_sms": 16}),
+    "group12": ({}, {"router_group": 12}),
     "lbatch8": ({"MPB_LAYOUT_BATCH": "8"}, {}),
-    "lbatch4": ({"MPB_LAYOUT_BATCH": "4"}, {}),
+    "tailboost2": ({"MPB_TAIL_BOOST": "2"}, {}),
 }
 rounds = int(sys.argv[1]) if len(sys.argv) > 1 else 3
 eng = mp.Engine(0)

@@ -90,7 +90,7 @@ def launch_shares(w, bench):
     ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
     scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "ns": 1e-3, "us": 1.0, "ms": 1e3}
     seq = [(r[ki], num(r[vi]) * scale.get(r[ui], float("nan"))) for r in rows[start + 1:]
-           if len(r) > vi]
+           if len(r) > vi and num(r[vi]) is not None and num(r[vi]) == num(r[vi])]  # ncu "nan": unmeasured launch
     # the last routed step: from its first router launch onwards, up to the
     # reference-statistic kernels the bench runs after the timed loop
     n_router = bench["config"]["schedule"]["router_launches_per_step"]
